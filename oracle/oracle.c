@@ -1,0 +1,537 @@
+/*
+ * oracle.c — CPU restatement of the reference's Flash hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library, and
+ * only as the checker or as the reported CPU baseline — never as the product
+ * path.  The product path (paper_2502_18113_b200) has no CPU fallback.
+ *
+ * Everything here is restated from the reference's behaviour, citing
+ * /root/reference/pkg/src/flashann/... file:line:
+ *   or_l2sq_f32      _kernels/_simd.h:44-51 (fp32 tree of the gcc -O3
+ *                    -march=native -ffast-math build; pinned by golden vectors)
+ *   or_quantize      _kernels/_simd.h:99-107
+ *   or_encode_adt    _kernels/_simd.h:211-228
+ *   or_batch_lanes   _kernels/_simd.h:111-121 (scalar semantic definition)
+ *   or_sdt_sum       _kernels/_simd.h:87-95
+ *   or_select        _kernels/_core.pyx:388-408
+ *   or_layer_search  _kernels/_core.pyx:278-342 with the (d, id) total order
+ *                    of SURVEY §8(c) (T-only stop rule)
+ *   or_hill_climb    _kernels/_core.pyx:345-385
+ *   or_reverse_add   _kernels/_core.pyx:441-477 (+ fa_sort_pairs :232-247)
+ *   or_build         _kernels/_core.pyx:501-536 / :711-764 under the
+ *                    deterministic insertion-batch schedule of the GPU build
+ *                    (batch size 1 everywhere = the sequential reference)
+ *   or_search        _kernels/_core.pyx:784-888
+ *
+ * Compile: gcc -O2 -ffp-contract=off (explicit fmaf where the tree fuses).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "oracle.h"
+
+/* ---- numerics ------------------------------------------------------------ */
+
+double or_l2sq_f32(const float *a, const float *b, int d) {
+    int i = 0;
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, s;
+    int have_v = 0;
+    if (d >= 8) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (; i + 8 <= d; i += 8)
+            for (int k = 0; k < 8; ++k) {
+                float e = a[i + k] - b[i + k];
+                float sq = e * e;
+                acc[k] = acc[k] + sq;
+            }
+        v0 = acc[0] + acc[4];
+        v1 = acc[1] + acc[5];
+        v2 = acc[2] + acc[6];
+        v3 = acc[3] + acc[7];
+        have_v = 1;
+    }
+    if (d - i >= 4) {
+        float e0 = a[i] - b[i], e1 = a[i + 1] - b[i + 1];
+        float e2 = a[i + 2] - b[i + 2], e3 = a[i + 3] - b[i + 3];
+        float w0 = fmaf(e0, e0, v0), w1 = fmaf(e1, e1, v1);
+        float w2 = fmaf(e2, e2, v2), w3 = fmaf(e3, e3, v3);
+        float t0 = w0 + w2, t1 = w1 + w3;
+        s = t0 + t1;
+        i += 4;
+    } else if (have_v) {
+        float t0 = v0 + v2, t1 = v1 + v3;
+        s = t0 + t1;
+    } else {
+        s = 0.f;
+    }
+    for (; i < d; ++i) {
+        float e = a[i] - b[i];
+        s = fmaf(e, e, s);
+    }
+    return (double)s;
+}
+
+uint8_t or_quantize(double d, double dmin, double delta) {
+    double dmax = dmin + delta;
+    if (d >= dmax) return 255;
+    if (d < dmin) d = dmin;
+    double t = floor((d - dmin) / delta * 255.0);
+    if (t >= 255.0) return 255;
+    if (t <= 0.0) return 0;
+    return (uint8_t)t;
+}
+
+void or_encode_adt(const float *red, const float *cent, const int32_t *dims, const int32_t *offs,
+                   int m, int dmax, double dmin, double delta, uint8_t *code, uint8_t *adt) {
+    for (int i = 0; i < m; ++i) {
+        int best = 0;
+        double bestd = INFINITY;
+        for (int j = 0; j < 16; ++j) {
+            double d = or_l2sq_f32(red + offs[i], cent + ((size_t)i * 16 + j) * dmax, dims[i]);
+            if (adt) adt[i * 16 + j] = or_quantize(d, dmin, delta);
+            if (d < bestd) {
+                bestd = d;
+                best = j;
+            }
+        }
+        code[i] = (uint8_t)best;
+    }
+}
+
+void or_batch_lanes(const uint8_t *adt, const uint8_t *codes, int m, int nb, uint8_t *out) {
+    for (int b = 0; b < nb; ++b)
+        for (int lane = 0; lane < 16; ++lane) {
+            uint32_t acc = 0;
+            for (int i = 0; i < m; ++i) {
+                acc += adt[i * 16 + codes[(size_t)b * m * 16 + i * 16 + lane]];
+                if (acc > 255u) acc = 255u;
+            }
+            out[b * 16 + lane] = (uint8_t)acc;
+        }
+}
+
+int or_sdt_sum(const uint8_t *sdt, const uint8_t *ca, const uint8_t *cb, int m) {
+    uint32_t acc = 0;
+    for (int i = 0; i < m; ++i) {
+        acc += sdt[((size_t)i * 16 + ca[i]) * 16 + cb[i]];
+        if (acc > 255u) acc = 255u;
+    }
+    return (int)acc;
+}
+
+static int adt_sum(const uint8_t *adt, const uint8_t *code, int m) {
+    uint32_t acc = 0;
+    for (int i = 0; i < m; ++i) {
+        acc += adt[i * 16 + code[i]];
+        if (acc > 255u) acc = 255u;
+    }
+    return (int)acc;
+}
+
+int or_select(const uint8_t *sdt, int m, const uint8_t *codes, int cs, const int32_t *ids,
+              const double *d, int n, int cap, int32_t *out, int64_t *sym) {
+    int nk = 0;
+    for (int j = 0; j < n && nk < cap; ++j) {
+        int v = ids[j], ok = 1;
+        for (int t = 0; t < nk; ++t) {
+            if (sym) ++*sym;
+            if ((double)or_sdt_sum(sdt, codes + (size_t)out[t] * cs, codes + (size_t)v * cs, m) <
+                d[j]) {
+                ok = 0;
+                break;
+            }
+        }
+        if (ok) out[nk++] = v;
+    }
+    return nk;
+}
+
+/* ---- graph ---------------------------------------------------------------- */
+
+static int32_t *row_of(or_graph *g, int layer, int v) {
+    if (layer == 0) return g->adj0 + (int64_t)v * g->cap0;
+    return g->adjU + (g->uoff[v] + layer - 1) * g->capU;
+}
+static int32_t *cnt_of(or_graph *g, int layer, int v) {
+    if (layer == 0) return g->cnt0 + v;
+    return g->cntU + (g->uoff[v] + layer - 1);
+}
+
+typedef struct {
+    uint64_t key; /* d << 32 | id */
+    int expanded;
+} tentry;
+
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+static int cmp_tentry(const void *a, const void *b) {
+    uint64_t x = ((const tentry *)a)->key, y = ((const tentry *)b)->key;
+    return (x > y) - (x < y);
+}
+
+typedef struct {
+    uint32_t *visited; /* epoch per vertex */
+    uint32_t epoch;
+    tentry *T;
+    int *fresh;
+    int cap_scratch;
+} scratch;
+
+/* (d, id)-ordered best-first search; returns |T|, fills out (keys asc). */
+static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int layer, int entry,
+                             int entry_d, int W, uint64_t *out, or_counters *c) {
+    int cap = layer == 0 ? g->cap0 : g->capU;
+    s->epoch++;
+    if (s->epoch == 0) {
+        memset(s->visited, 0, sizeof(uint32_t) * g->n);
+        s->epoch = 1;
+    }
+    uint32_t ep = s->epoch;
+    s->visited[entry] = ep;
+    int ts = 1;
+    s->T[0].key = ((uint64_t)entry_d << 32) | (uint32_t)entry;
+    s->T[0].expanded = 0;
+    for (;;) {
+        int cur = -1;
+        for (int i = 0; i < ts; ++i)
+            if (!s->T[i].expanded) {
+                cur = i;
+                break;
+            }
+        if (cur < 0) break;
+        s->T[cur].expanded = 1;
+        int v = (int)(uint32_t)(s->T[cur].key & 0xffffffffu);
+        if (c) c->visited++;
+        int32_t *ids = row_of(g, layer, v);
+        int cnt = *cnt_of(g, layer, v);
+        if (cnt > cap) cnt = cap;
+        if (c) c->kernel_calls += (cnt + 15) >> 4;
+        int added = 0;
+        for (int j = 0; j < cnt; ++j) {
+            int u = ids[j];
+            if (u < 0 || s->visited[u] == ep) continue;
+            s->visited[u] = ep;
+            int du = adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+            if (c) c->dist_comps++;
+            s->T[ts + added].key = ((uint64_t)du << 32) | (uint32_t)u;
+            s->T[ts + added].expanded = 0;
+            added++;
+        }
+        if (added) {
+            ts += added;
+            qsort(s->T, (size_t)ts, sizeof(tentry), cmp_tentry);
+            if (ts > W) ts = W;
+        }
+    }
+    for (int i = 0; i < ts; ++i) out[i] = s->T[i].key;
+    return ts;
+}
+
+static void hill_climb_impl(or_graph *g, const uint8_t *adt, int layer, int *cur, int *curd,
+                            or_counters *c) {
+    int cap = layer == 0 ? g->cap0 : g->capU;
+    int improved = 1;
+    while (improved) {
+        improved = 0;
+        int32_t *ids = row_of(g, layer, *cur);
+        int cnt = *cnt_of(g, layer, *cur);
+        if (cnt > cap) cnt = cap;
+        if (c) c->kernel_calls += (cnt + 15) >> 4;
+        int bu = -1, bd = 0;
+        for (int j = 0; j < cnt; ++j) {
+            int u = ids[j];
+            if (u < 0) continue;
+            int du = adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+            if (c) c->dist_comps++;
+            if (bu < 0 || du < bd) {
+                bd = du;
+                bu = u;
+            }
+        }
+        if (bu >= 0 && bd < *curd) {
+            *curd = bd;
+            *cur = bu;
+            improved = 1;
+        }
+    }
+}
+
+static int scratch_init(scratch *s, int64_t n, int W, int capmax) {
+    s->visited = (uint32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(uint32_t));
+    s->T = (tentry *)malloc(sizeof(tentry) * (size_t)(W + capmax + 8));
+    s->fresh = (int *)malloc(sizeof(int) * (size_t)(capmax + 8));
+    s->epoch = 0;
+    return (s->visited && s->T && s->fresh) ? 0 : -1;
+}
+static void scratch_free(scratch *s) {
+    free(s->visited);
+    free(s->T);
+    free(s->fresh);
+}
+
+int or_layer_search(or_graph *g, const uint8_t *adt, int layer, int entry, int W, int32_t *out_ids,
+                    int32_t *out_d, or_counters *c) {
+    scratch s;
+    int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
+    if (scratch_init(&s, g->n, W, capmax)) return -1;
+    uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 1));
+    int ed = adt_sum(adt, g->codes + (size_t)entry * g->cs, g->m);
+    if (c) c->dist_comps++;
+    int ts = layer_search_impl(g, &s, adt, layer, entry, ed, W, keys, c);
+    for (int i = 0; i < ts; ++i) {
+        out_ids[i] = (int32_t)(keys[i] & 0xffffffffu);
+        out_d[i] = (int32_t)(keys[i] >> 32);
+    }
+    free(keys);
+    scratch_free(&s);
+    return ts;
+}
+
+int or_hill_climb(or_graph *g, const uint8_t *adt, int layer, int entry, int *out_d,
+                  or_counters *c) {
+    int cur = entry;
+    int curd = adt_sum(adt, g->codes + (size_t)entry * g->cs, g->m);
+    hill_climb_impl(g, adt, layer, &cur, &curd, c);
+    if (out_d) *out_d = curd;
+    return cur;
+}
+
+/* reverse_add (_core.pyx:441-477) */
+static void reverse_add(or_graph *g, const uint8_t *sdt, int y, int x, int layer, uint64_t *pairs,
+                        int32_t *cid, double *cd, int32_t *sel, or_counters *c) {
+    int cap = layer == 0 ? g->cap0 : g->capU;
+    int32_t *ids = row_of(g, layer, y);
+    int32_t *cntp = cnt_of(g, layer, y);
+    int cnt = *cntp;
+    if (cnt < cap) {
+        ids[cnt] = x;
+        *cntp = cnt + 1;
+        if (c) c->reverse_appends++;
+        return;
+    }
+    if (c) c->reverse_prunes++;
+    const uint8_t *cy = g->codes + (size_t)y * g->cs;
+    for (int j = 0; j <= cnt; ++j) {
+        int u = j < cnt ? ids[j] : x;
+        uint64_t d = (uint64_t)or_sdt_sum(sdt, cy, g->codes + (size_t)u * g->cs, g->m);
+        pairs[j] = (d << 32) | (uint32_t)u; /* (d, id) order == fa_pair_cmp */
+    }
+    if (c) c->sym_comps += cnt + 1;
+    qsort(pairs, (size_t)cnt + 1, sizeof(uint64_t), cmp_u64);
+    for (int j = 0; j <= cnt; ++j) {
+        cid[j] = (int32_t)(pairs[j] & 0xffffffffu);
+        cd[j] = (double)(pairs[j] >> 32);
+    }
+    int nk = or_select(sdt, g->m, g->codes, g->cs, cid, cd, cnt + 1, cap, sel,
+                       c ? &c->sym_comps : NULL);
+    for (int j = 0; j < cap; ++j) ids[j] = j < nk ? sel[j] : -1;
+    *cntp = nk;
+}
+
+void or_reset(or_graph *g) {
+    for (int64_t i = 0; i < g->n * g->cap0; ++i) g->adj0[i] = -1;
+    for (int64_t i = 0; i < g->nU * g->capU; ++i) g->adjU[i] = -1;
+    memset(g->cnt0, 0, sizeof(int32_t) * (size_t)g->n);
+    if (g->nU) memset(g->cntU, 0, sizeof(int32_t) * (size_t)g->nU);
+}
+
+int or_schedule(const int32_t *levels, int64_t n, int batch_max, double batch_frac, int seq_prefix,
+                int32_t *starts, int32_t *sizes) {
+    if (n <= 1) return 0;
+    int ml = levels[0], nb = 0;
+    int64_t x = 1;
+    while (x < n) {
+        int B;
+        if (levels[x] > ml) B = 1;
+        else if (x < seq_prefix) B = 1;
+        else {
+            double f = batch_frac * (double)x;
+            B = (int)f;
+            if (B > batch_max) B = batch_max;
+            if (B < 1) B = 1;
+        }
+        int size = 0;
+        starts[nb] = (int32_t)x;
+        while (size < B && x < n) {
+            int lv = levels[x];
+            if (size > 0 && lv > ml) break;
+            ++size;
+            ++x;
+            if (lv > ml) break;
+        }
+        sizes[nb] = size;
+        int last = starts[nb] + size - 1;
+        if (levels[last] > ml) ml = levels[last];
+        ++nb;
+    }
+    return nb;
+}
+
+typedef struct {
+    uint64_t key; /* row << 32 | x */
+} req_t;
+
+int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const int32_t *dims,
+             const int32_t *offs, int dmax, double dmin, double delta, const uint8_t *sdt, int C,
+             int R, int batch_max, double batch_frac, int seq_prefix, or_build_result *res) {
+    memset(res, 0, sizeof(*res));
+    res->entry_point = -1;
+    res->max_layer = -1;
+    or_reset(g);
+    if (g->n == 0) return 0;
+    int m = g->m;
+    /* codes are the fp32-tree codes (prep_qctx overwrite, _core.pyx:493-498) */
+    uint8_t *adts = NULL;
+    int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
+    for (int64_t v = 0; v < g->n; ++v)
+        or_encode_adt(proj + (size_t)v * dproj, cent, dims, offs, m, dmax, dmin, delta,
+                      g->codes + (size_t)v * g->cs, NULL);
+    int32_t *starts = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
+    int32_t *sizes = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
+    int nb = or_schedule(g->levels, g->n, batch_max, batch_frac, seq_prefix, starts, sizes);
+    int maxB = 1;
+    for (int b = 0; b < nb; ++b)
+        if (sizes[b] > maxB) maxB = sizes[b];
+    adts = (uint8_t *)malloc((size_t)m * 16);
+    scratch s;
+    if (scratch_init(&s, g->n, C, capmax)) return -1;
+    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(C + 1));
+    int32_t *cid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+    double *cd = (double *)malloc(sizeof(double) * (size_t)(C + capmax + 2));
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+    uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 2));
+    int maxlev = 0;
+    for (int64_t v = 0; v < g->n; ++v)
+        if (g->levels[v] > maxlev) maxlev = g->levels[v];
+    size_t reqcap = (size_t)maxB * (size_t)(maxlev + 1) * (size_t)R + 1;
+    uint64_t *req = (uint64_t *)malloc(sizeof(uint64_t) * reqcap);
+    int ep = 0, ml = g->levels[0];
+    or_counters *c = &res->counters;
+    for (int b = 0; b < nb; ++b) {
+        size_t nreq = 0;
+        int bep = ep, bml = ml;
+        for (int p = 0; p < sizes[b]; ++p) {
+            int x = starts[b] + p;
+            int level = g->levels[x];
+            uint8_t code_tmp[256];
+            or_encode_adt(proj + (size_t)x * dproj, cent, dims, offs, m, dmax, dmin, delta, code_tmp,
+                          adts);
+            int cur = bep;
+            int curd = adt_sum(adts, g->codes + (size_t)cur * g->cs, m);
+            c->dist_comps++;
+            for (int layer = bml; layer > level; --layer)
+                hill_climb_impl(g, adts, layer, &cur, &curd, c);
+            int top = bml < level ? bml : level;
+            for (int layer = top; layer >= 0; --layer) {
+                int ts = layer_search_impl(g, &s, adts, layer, cur, curd, C, T, c);
+                for (int j = 0; j < ts; ++j) {
+                    cid[j] = (int32_t)(T[j] & 0xffffffffu);
+                    cd[j] = (double)(T[j] >> 32);
+                }
+                int nsel = or_select(sdt, m, g->codes, g->cs, cid, cd, ts, R, sel, &c->sym_comps);
+                int cap = layer == 0 ? g->cap0 : g->capU;
+                int32_t *row = row_of(g, layer, x);
+                for (int j = 0; j < cap; ++j) row[j] = j < nsel ? sel[j] : -1;
+                *cnt_of(g, layer, x) = nsel;
+                for (int j = 0; j < nsel; ++j) {
+                    int y = sel[j];
+                    uint64_t rowg = layer == 0 ? (uint64_t)y
+                                               : (uint64_t)(g->n + g->uoff[y] + layer - 1);
+                    req[nreq++] = (rowg << 32) | (uint32_t)x;
+                }
+                cur = (int)(T[0] & 0xffffffffu);
+                curd = (int)(T[0] >> 32);
+            }
+            if (level > ml) {
+                ep = x;
+                ml = level;
+            }
+        }
+        /* reverse edges grouped by row, ascending x (the sequential order) */
+        qsort(req, nreq, sizeof(uint64_t), cmp_u64);
+        for (size_t t = 0; t < nreq; ++t) {
+            uint64_t rowg = req[t] >> 32;
+            int x = (int)(req[t] & 0xffffffffu);
+            int layer, y;
+            if ((int64_t)rowg < g->n) {
+                layer = 0;
+                y = (int)rowg;
+            } else {
+                int64_t r = (int64_t)rowg - g->n;
+                y = g->upper_owner[r];
+                layer = (int)(r - g->uoff[y]) + 1;
+            }
+            reverse_add(g, sdt, y, x, layer, pairs, cid, cd, sel, c);
+        }
+    }
+    res->entry_point = ep;
+    res->max_layer = ml;
+    res->n_batches = nb;
+    free(starts); free(sizes); free(adts); free(T); free(cid); free(cd); free(sel);
+    free(pairs); free(req);
+    scratch_free(&s);
+    return 0;
+}
+
+int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const int32_t *dims,
+              const int32_t *offs, int dmax, double dmin, double delta, int dproj, int entry,
+              int max_layer, const float *queries, const float *qproj, int nq, int ef, int k,
+              int rerank_depth, int64_t *out_ids, double *out_d, or_counters *c) {
+    int m = g->m;
+    int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
+    scratch s;
+    if (scratch_init(&s, g->n, ef, capmax)) return -1;
+    uint8_t *adt = (uint8_t *)malloc((size_t)m * 16);
+    uint8_t code[256];
+    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(ef + 1));
+    typedef struct {
+        double d;
+        int32_t id;
+    } pair;
+    pair *pr = (pair *)malloc(sizeof(pair) * (size_t)(ef + 1));
+    for (int q = 0; q < nq; ++q) {
+        or_encode_adt(qproj + (size_t)q * dproj, cent, dims, offs, m, dmax, dmin, delta, code, adt);
+        int cur = entry;
+        int curd = adt_sum(adt, g->codes + (size_t)cur * g->cs, m);
+        if (c) c->dist_comps++;
+        for (int layer = max_layer; layer > 0; --layer) hill_climb_impl(g, adt, layer, &cur, &curd, c);
+        int ts = layer_search_impl(g, &s, adt, 0, cur, curd, ef, T, c);
+        int64_t *oi = out_ids + (size_t)q * k;
+        double *od = out_d + (size_t)q * k;
+        if (rerank_depth > 0) {
+            int rr = rerank_depth < ts ? rerank_depth : ts;
+            for (int j = 0; j < rr; ++j) {
+                int id = (int)(T[j] & 0xffffffffu);
+                pr[j].d = or_l2sq_f32(queries + (size_t)q * dim, vecs + (size_t)id * dim, dim);
+                pr[j].id = id;
+            }
+            /* insertion sort by (d, id) (fa_pair_cmp) */
+            for (int a = 1; a < rr; ++a) {
+                pair t = pr[a];
+                int b = a - 1;
+                while (b >= 0 && (pr[b].d > t.d || (pr[b].d == t.d && pr[b].id > t.id))) {
+                    pr[b + 1] = pr[b];
+                    --b;
+                }
+                pr[b + 1] = t;
+            }
+            for (int j = 0; j < k; ++j) {
+                oi[j] = j < rr ? pr[j].id : -1;
+                od[j] = j < rr ? pr[j].d : INFINITY;
+            }
+        } else {
+            for (int j = 0; j < k; ++j) {
+                oi[j] = j < ts ? (int64_t)(T[j] & 0xffffffffu) : -1;
+                od[j] = j < ts ? (double)(T[j] >> 32) : INFINITY;
+            }
+        }
+    }
+    free(adt); free(T); free(pr);
+    scratch_free(&s);
+    return 0;
+}

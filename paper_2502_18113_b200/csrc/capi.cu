@@ -1,0 +1,158 @@
+// C-ABI plumbing: error strings, version, and the host-pointer drop-ins that
+// mirror the reference core's blocking Cython entry points
+// (build_graph _core.pyx:711-764, search_batch _core.pyx:817-888).
+#include <stdarg.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace fa {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// RAII device buffer for the host drop-ins.
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+    int alloc(size_t bytes) {
+        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+        if (e != cudaSuccess) {
+            set_error("cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+            return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
+        }
+        return FA_OK;
+    }
+    int upload(const void *src, size_t bytes) {
+        FA_TRY(alloc(bytes));
+        if (bytes) FA_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+        return FA_OK;
+    }
+    template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct IndexGuard {
+    fa_index *ix = nullptr;
+    ~IndexGuard() { fa_index_destroy(ix); }
+};
+
+}  // namespace fa
+
+using namespace fa;
+
+extern "C" const char *fa_last_error(void) { return g_err; }
+extern "C" int fa_version(void) { return 1; }
+
+extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dproj,
+                                   const float *proj, uint8_t *codes, int m, const float *cent,
+                                   int dmax, const int32_t *dims, const int32_t *offs,
+                                   const uint8_t *sdt, double dist_min, double delta,
+                                   const int32_t *levels, uint8_t *base_blocks, int64_t base_stride,
+                                   const int64_t *uoff, uint8_t *upper_blocks, int64_t n_upper_rows,
+                                   int64_t upper_stride, int C, int R, const fa_build_opts *opts,
+                                   fa_build_result *res) {
+    (void)vecs;
+    (void)dim;
+    FA_CHECK_ARG(n >= 0 && m >= 1 && R >= 1, "bad sizes");
+    if (n == 0) {
+        memset(res, 0, sizeof(*res));
+        res->entry_point = -1;
+        res->max_layer = -1;
+        return FA_OK;
+    }
+    DevBuf dproj_b, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper;
+    FA_TRY(dproj_b.upload(proj, sizeof(float) * n * dproj));
+    FA_TRY(dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
+    FA_TRY(ddims.upload(dims, sizeof(int32_t) * m));
+    FA_TRY(doffs.upload(offs, sizeof(int32_t) * m));
+    FA_TRY(dsdt.upload(sdt, (size_t)m * 256));
+    FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
+    FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
+    fa_index_desc d;
+    memset(&d, 0, sizeof(d));
+    d.n = n; d.m = m; d.R = R; d.dim = 0; d.dproj = dproj; d.dmax = dmax;
+    d.dist_min = dist_min; d.delta = delta;
+    d.proj = dproj_b.as<float>(); d.cent = dcent.as<float>(); d.dims = ddims.as<int32_t>();
+    d.offs = doffs.as<int32_t>(); d.sdt = dsdt.as<uint8_t>(); d.levels = dlev.as<int32_t>();
+    d.uoff = duoff.as<int64_t>(); d.n_upper_rows = n_upper_rows;
+    IndexGuard guard;
+    FA_TRY(fa_index_create(&d, &guard.ix));
+    FA_TRY(fa_index_encode(guard.ix, nullptr));
+    FA_TRY(fa_index_build(guard.ix, opts, res, nullptr));
+    // codes[x] as the compiled core leaves them (prep_qctx overwrite)
+    int cs = 0;
+    const uint8_t *dcodes = fa_index_codes(guard.ix, &cs);
+    FA_CUDA(cudaMemcpy2D(codes, m, dcodes, cs, m, n, cudaMemcpyDeviceToHost));
+    FA_TRY(dbase.alloc((size_t)n * base_stride));
+    FA_TRY(dupper.alloc((size_t)n_upper_rows * upper_stride));
+    FA_TRY(fa_index_export_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
+                                  upper_stride, nullptr));
+    FA_CUDA(cudaMemcpy(base_blocks, dbase.p, (size_t)n * base_stride, cudaMemcpyDeviceToHost));
+    if (n_upper_rows)
+        FA_CUDA(cudaMemcpy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride,
+                           cudaMemcpyDeviceToHost));
+    return FA_OK;
+}
+
+extern "C" int fa_search_batch_host(int64_t n, int dim, const float *vecs, int dproj,
+                                    const uint8_t *codes, int m, const float *cent, int dmax,
+                                    const int32_t *dims, const int32_t *offs, const uint8_t *sdt,
+                                    double dist_min, double delta, const int32_t *levels,
+                                    const uint8_t *base_blocks, int64_t base_stride,
+                                    const int64_t *uoff, const uint8_t *upper_blocks,
+                                    int64_t n_upper_rows, int64_t upper_stride, int R,
+                                    int64_t entry, int max_layer, const float *queries,
+                                    const float *qproj, int nq, int ef, int k, int rerank_depth,
+                                    int64_t *out_ids, double *out_d, int64_t *counters) {
+    if (entry < 0) {
+        set_error("cannot search an empty graph");
+        return FA_EEMPTY;
+    }
+    FA_CHECK_ARG(n > 0 && m >= 1 && R >= 1 && k >= 1, "bad sizes");
+    if (nq == 0) {
+        if (counters) memset(counters, 0, 4 * sizeof(int64_t));
+        return FA_OK;
+    }
+    DevBuf dvecs, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper, dq, dqp, dcodes, did, dd;
+    if (rerank_depth > 0) {
+        FA_TRY(dvecs.upload(vecs, sizeof(float) * n * dim));
+        FA_TRY(dq.upload(queries, sizeof(float) * (size_t)nq * dim));
+    }
+    FA_TRY(dqp.upload(qproj, sizeof(float) * (size_t)nq * dproj));
+    FA_TRY(dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
+    FA_TRY(ddims.upload(dims, sizeof(int32_t) * m));
+    FA_TRY(doffs.upload(offs, sizeof(int32_t) * m));
+    FA_TRY(dsdt.upload(sdt, (size_t)m * 256));
+    FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
+    FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
+    FA_TRY(dbase.upload(base_blocks, (size_t)n * base_stride));
+    FA_TRY(dupper.upload(upper_blocks, (size_t)n_upper_rows * upper_stride));
+    FA_TRY(dcodes.upload(codes, (size_t)n * m));
+    FA_TRY(did.alloc(sizeof(int64_t) * (size_t)nq * k));
+    FA_TRY(dd.alloc(sizeof(double) * (size_t)nq * k));
+    fa_index_desc d;
+    memset(&d, 0, sizeof(d));
+    d.n = n; d.m = m; d.R = R; d.dim = dim; d.dproj = dproj; d.dmax = dmax;
+    d.dist_min = dist_min; d.delta = delta;
+    d.vecs = dvecs.as<float>(); d.cent = dcent.as<float>(); d.dims = ddims.as<int32_t>();
+    d.offs = doffs.as<int32_t>(); d.sdt = dsdt.as<uint8_t>(); d.levels = dlev.as<int32_t>();
+    d.uoff = duoff.as<int64_t>(); d.n_upper_rows = n_upper_rows;
+    IndexGuard guard;
+    FA_TRY(fa_index_create(&d, &guard.ix));
+    FA_TRY(fa_index_set_codes(guard.ix, dcodes.as<uint8_t>(), m, nullptr));
+    FA_TRY(fa_index_import_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
+                                  upper_stride, nullptr));
+    FA_TRY(fa_index_search(guard.ix, dq.as<float>(), dqp.as<float>(), nq, ef, k, rerank_depth,
+                           entry, max_layer, did.as<int64_t>(), dd.as<double>(), counters,
+                           nullptr));
+    FA_CUDA(cudaMemcpy(out_ids, did.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToHost));
+    FA_CUDA(cudaMemcpy(out_d, dd.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToHost));
+    return FA_OK;
+}

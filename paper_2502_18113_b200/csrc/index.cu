@@ -1,0 +1,606 @@
+// Device graph runtime: allocation, the batched-insertion build loop,
+// query search, and reference-layout import/export.
+//
+// Build = reference build_graph (_core.pyx:711-764) with the OpenMP prange
+// replaced by deterministic insertion batches: every vertex of a batch
+// searches the graph as of the batch start (one warp each), then all reverse
+// edges of the batch are grouped by target row and applied in ascending x.
+// The batch schedule is a pure function of the layer draws, so the whole
+// build is enqueued without a host round trip.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.cuh"
+
+struct fa_index {
+    fa::Graph g;
+    fa_index_desc d;
+    int cap0, capU;
+    std::vector<int32_t> levels_h;
+    std::vector<int64_t> uoff_h;
+    uint8_t *codes = nullptr;
+    int32_t *adj0 = nullptr, *cnt0 = nullptr, *adjU = nullptr, *cntU = nullptr;
+    uint8_t *cons0 = nullptr, *consU = nullptr;
+    int32_t *upper_owner = nullptr;
+    int64_t entry = -1;
+    int max_layer = -1;
+};
+
+namespace fa {
+
+static int dev_alloc(void **p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        set_error("cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
+    }
+    return FA_OK;
+}
+
+__global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+static int reset_graph(fa_index *ix, cudaStream_t st) {
+    Graph &g = ix->g;
+    fill_i32<<<1184, 256, 0, st>>>(g.adj0, g.n * g.cap0p, -1);
+    if (g.nU) fill_i32<<<1184, 256, 0, st>>>(g.adjU, g.nU * g.capUp, -1);
+    FA_LAUNCH_CHECK();
+    FA_CUDA(cudaMemsetAsync(g.cnt0, 0, sizeof(int32_t) * g.n, st));
+    FA_CUDA(cudaMemsetAsync(g.cons0, 0, g.n, st));
+    if (g.nU) {
+        FA_CUDA(cudaMemsetAsync(g.cntU, 0, sizeof(int32_t) * g.nU, st));
+        FA_CUDA(cudaMemsetAsync(g.consU, 0, g.nU, st));
+    }
+    return FA_OK;
+}
+
+static int pick_hash_log2(int W, int capmax, int R, int mpad, int req) {
+    if (req > 0) return req;
+    int want = 16 * W + 2 * capmax;
+    int l = 9;
+    while ((1 << l) < want) ++l;
+    // kept ids + codes alias the hash during forward selection
+    while ((4 << l) < round_up(R * 4, 16) + R * kept_stride(mpad)) ++l;
+    return l;
+}
+
+// Export one row to the reference block layout (layout.py:1-45): count,
+// ids (-1 beyond count), subspace-major 16-slot code batches (0 beyond count).
+__global__ void export_kernel(Graph g, int64_t rows, bool upper, uint8_t *__restrict__ blocks,
+                              int64_t stride, int cap, int capp) {
+    const int lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int nb = (cap + 15) >> 4;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows;
+         r += warps) {
+        const int32_t *ids = (upper ? g.adjU : g.adj0) + r * capp;
+        const int cnt = (upper ? g.cntU : g.cnt0)[r];
+        uint8_t *b = blocks + r * stride;
+        if (lane == 0) *reinterpret_cast<int32_t *>(b) = cnt;
+        int32_t *bid = reinterpret_cast<int32_t *>(b + 4);
+        for (int j = lane; j < cap; j += 32) bid[j] = j < cnt ? ids[j] : -1;
+        uint8_t *region = b + 4 + 4 * cap;
+        const int total = nb * g.m * 16;
+        for (int t = lane; t < total; t += 32) {
+            int bt = t / (g.m * 16);
+            int rem = t % (g.m * 16);
+            int i = rem >> 4, ln = rem & 15;
+            int slot = bt * 16 + ln;
+            uint8_t c = 0;
+            if (slot < cnt) {
+                int u = ids[slot];
+                if (u >= 0) c = g.codes[(size_t)u * g.mpad + i];
+            }
+            region[t] = c;
+        }
+    }
+}
+
+__global__ void import_kernel(Graph g, int64_t rows, bool upper, const uint8_t *__restrict__ blocks,
+                              int64_t stride, int cap, int capp) {
+    const int lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows;
+         r += warps) {
+        const uint8_t *b = blocks + r * stride;
+        int cnt = *reinterpret_cast<const int32_t *>(b);
+        cnt = cnt < 0 ? 0 : (cnt > cap ? cap : cnt);
+        const int32_t *bid = reinterpret_cast<const int32_t *>(b + 4);
+        int32_t *ids = (upper ? g.adjU : g.adj0) + r * capp;
+        // live ids are compacted to a prefix (-1 slots inside the count are
+        // skipped by every reader of the reference layout, _core.pyx:308-311)
+        int w = 0;
+        for (int base = 0; base < cnt; base += 32) {
+            int j = base + lane;
+            int u = j < cnt ? bid[j] : -1;
+            unsigned bl = __ballot_sync(0xffffffffu, u >= 0);
+            if (u >= 0) ids[w + __popc(bl & ((1u << lane) - 1u))] = u;
+            w += __popc(bl);
+        }
+        for (int j = w + lane; j < capp; j += 32) ids[j] = -1;
+        if (lane == 0) {
+            (upper ? g.cntU : g.cnt0)[r] = w;
+            (upper ? g.consU : g.cons0)[r] = 0;
+        }
+    }
+}
+
+struct Batch {
+    int start, size, ep, ml;
+    int64_t nreq;
+};
+
+}  // namespace fa
+
+using namespace fa;
+
+extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
+    FA_CHECK_ARG(desc && out, "null argument");
+    FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 31) - 1, "n=%lld out of range", (long long)desc->n);
+    FA_CHECK_ARG(desc->m >= 1 && desc->m <= 128, "m=%d outside [1,128]", desc->m);
+    FA_CHECK_ARG(desc->R >= 1, "R must be >= 1");
+    FA_CHECK_ARG(2 * desc->R <= 127, "base capacity 2R=%d exceeds 127", 2 * desc->R);
+    fa_index *ix = new fa_index();
+    ix->d = *desc;
+    Graph &g = ix->g;
+    g.n = desc->n;
+    g.m = desc->m;
+    g.mpad = round_up(desc->m, 16);
+    g.cap0 = 2 * desc->R;
+    g.capU = desc->R;
+    g.cap0p = round_up(g.cap0, 32);
+    g.capUp = round_up(g.capU, 32);
+    g.nU = desc->n_upper_rows;
+    g.levels = desc->levels;
+    g.uoff = desc->uoff;
+    int rc = FA_OK;
+    auto fail = [&](int r) {
+        fa_index_destroy(ix);
+        return r;
+    };
+    if ((rc = dev_alloc((void **)&ix->codes, (size_t)g.n * g.mpad))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->adj0, sizeof(int32_t) * g.n * g.cap0p))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->cnt0, sizeof(int32_t) * g.n))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->cons0, g.n))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->adjU, sizeof(int32_t) * g.nU * g.capUp))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->cntU, sizeof(int32_t) * g.nU))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->consU, g.nU))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->upper_owner, sizeof(int32_t) * g.nU))) return fail(rc);
+    g.codes = ix->codes;
+    g.adj0 = ix->adj0; g.cnt0 = ix->cnt0; g.cons0 = ix->cons0;
+    g.adjU = ix->adjU; g.cntU = ix->cntU; g.consU = ix->consU;
+    // host copies of the layer draws drive the batch schedule
+    ix->levels_h.resize(g.n);
+    ix->uoff_h.resize(g.n);
+    if (g.n) {
+        cudaError_t e1 = cudaMemcpy(ix->levels_h.data(), desc->levels, sizeof(int32_t) * g.n,
+                                    cudaMemcpyDeviceToHost);
+        cudaError_t e2 = cudaMemcpy(ix->uoff_h.data(), desc->uoff, sizeof(int64_t) * g.n,
+                                    cudaMemcpyDeviceToHost);
+        if (e1 != cudaSuccess || e2 != cudaSuccess) {
+            set_error("copying levels/upper offsets: %s", cudaGetErrorString(e1 ? e1 : e2));
+            return fail(FA_ECUDA);
+        }
+    }
+    std::vector<int32_t> owner(g.nU > 0 ? g.nU : 1, -1);
+    for (int64_t v = 0; v < g.n; ++v) {
+        int lv = ix->levels_h[v];
+        if (lv > 0) {
+            int64_t o = ix->uoff_h[v];
+            if (o < 0 || o + lv > g.nU) {
+                set_error("upper_offsets[%lld]=%lld inconsistent with levels", (long long)v,
+                          (long long)o);
+                return fail(FA_EINVAL);
+            }
+            for (int l = 0; l < lv; ++l) owner[o + l] = (int32_t)v;
+        }
+    }
+    if (g.nU) {
+        cudaError_t e = cudaMemcpy(ix->upper_owner, owner.data(), sizeof(int32_t) * g.nU,
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            set_error("upper owner copy: %s", cudaGetErrorString(e));
+            return fail(FA_ECUDA);
+        }
+    }
+    if ((rc = reset_graph(ix, 0))) return fail(rc);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        set_error("index init: %s", cudaGetErrorString(e));
+        return fail(FA_ECUDA);
+    }
+    *out = ix;
+    return FA_OK;
+}
+
+extern "C" int fa_index_destroy(fa_index *ix) {
+    if (!ix) return FA_OK;
+    cudaFree(ix->codes);
+    cudaFree(ix->adj0); cudaFree(ix->cnt0); cudaFree(ix->cons0);
+    cudaFree(ix->adjU); cudaFree(ix->cntU); cudaFree(ix->consU);
+    cudaFree(ix->upper_owner);
+    delete ix;
+    return FA_OK;
+}
+
+extern "C" int fa_index_encode(fa_index *ix, void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    FA_CHECK_ARG(ix->d.proj, "index has no projected vectors to encode");
+    cudaStream_t st = as_stream(stream);
+    FA_CUDA(cudaMemsetAsync(ix->codes, 0, (size_t)ix->g.n * ix->g.mpad, st));
+    return launch_encode_adt(ix->d.proj, ix->g.n, ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs,
+                             ix->g.m, ix->d.dmax, ix->d.dist_min, ix->d.delta, ix->codes,
+                             ix->g.mpad, nullptr, 0, st);
+}
+
+extern "C" int fa_index_set_codes(fa_index *ix, const uint8_t *codes, int code_stride,
+                                  void *stream) {
+    FA_CHECK_ARG(ix && codes, "null argument");
+    FA_CHECK_ARG(code_stride >= ix->g.m, "code_stride < m");
+    cudaStream_t st = as_stream(stream);
+    FA_CUDA(cudaMemsetAsync(ix->codes, 0, (size_t)ix->g.n * ix->g.mpad, st));
+    if (ix->g.n)
+        FA_CUDA(cudaMemcpy2DAsync(ix->codes, ix->g.mpad, codes, code_stride, ix->g.m, ix->g.n,
+                                  cudaMemcpyDeviceToDevice, st));
+    return FA_OK;
+}
+
+extern "C" const uint8_t *fa_index_codes(fa_index *ix, int *code_stride) {
+    if (!ix) return nullptr;
+    if (code_stride) *code_stride = ix->g.mpad;
+    return ix->codes;
+}
+
+extern "C" int fa_index_adjacency(fa_index *ix, int layer_kind, const int32_t **ids,
+                                  const int32_t **cnt, int *cap, int64_t *rows) {
+    FA_CHECK_ARG(ix, "null index");
+    if (layer_kind == 0) {
+        *ids = ix->adj0; *cnt = ix->cnt0; *cap = ix->g.cap0p; *rows = ix->g.n;
+    } else {
+        *ids = ix->adjU; *cnt = ix->cntU; *cap = ix->g.capUp; *rows = ix->g.nU;
+    }
+    return FA_OK;
+}
+
+extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_result *res,
+                              void *stream) {
+    FA_CHECK_ARG(ix && opts && res, "null argument");
+    Graph &g = ix->g;
+    const int C = opts->C;
+    const int R = ix->d.R;
+    FA_CHECK_ARG(C >= 1 && C <= 2048, "C=%d outside [1,2048]", C);
+    FA_CHECK_ARG(ix->d.sdt, "index has no SDT");
+    cudaStream_t st = as_stream(stream);
+    memset(res, 0, sizeof(*res));
+    res->entry_point = -1;
+    res->max_layer = -1;
+    FA_TRY(reset_graph(ix, st));
+    if (g.n == 0) {
+        ix->entry = -1;
+        ix->max_layer = -1;
+        return FA_OK;
+    }
+    FA_CHECK_ARG(ix->d.proj, "build needs the projected vectors (per-insertion tables)");
+    const int Bmax = opts->batch_max > 0 ? opts->batch_max : 4096;
+    const double frac = opts->batch_frac > 0 ? opts->batch_frac : 0.02;
+    const int prefix = opts->seq_prefix >= 0 ? opts->seq_prefix : 256;
+
+    // ---- schedule (pure function of the layer draws) ----
+    std::vector<Batch> batches;
+    std::vector<int64_t> req_off(g.n, 0);
+    int ep = 0, ml = ix->levels_h[0];
+    int64_t maxreq = 0;
+    int maxB = 1;
+    int64_t x = 1;
+    while (x < g.n) {
+        Batch b;
+        b.start = (int)x;
+        b.ep = ep;
+        b.ml = ml;
+        int B;
+        if (ix->levels_h[x] > ml) B = 1;
+        else if (x < prefix) B = 1;
+        else B = std::max(1, std::min(Bmax, (int)(frac * (double)x)));
+        int64_t off = 0;
+        int size = 0;
+        while (size < B && x < g.n) {
+            int lv = ix->levels_h[x];
+            if (size > 0 && lv > ml) break;
+            req_off[x] = off;
+            off += (int64_t)(std::min(ml, lv) + 1) * R;
+            ++size;
+            ++x;
+            if (lv > ml) break;  // a new top layer goes alone
+        }
+        b.size = size;
+        b.nreq = off;
+        batches.push_back(b);
+        maxreq = std::max(maxreq, off);
+        maxB = std::max(maxB, size);
+        int last = b.start + size - 1;
+        if (ix->levels_h[last] > ml) {
+            ep = last;
+            ml = ix->levels_h[last];
+        }
+    }
+
+    // ---- scratch ----
+    const int capmax = std::max(g.cap0, g.capU);
+    WarpLayout L;
+    L.init(g.mpad, C, capmax, pick_hash_log2(C, capmax, R, g.mpad, opts->hash_log2));
+    const size_t sdt_bytes = round_up(g.m * 256, 128);
+    const size_t smem_search = sdt_bytes + (size_t)kSearchWarps * L.total;
+    FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
+                 smem_search);
+    FA_CUDA(cudaFuncSetAttribute(build_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_search));
+    ReverseLayout RL;
+    RL.init(capmax, g.mpad);
+    const size_t smem_rev = 2 * sdt_bytes + (size_t)kReverseWarps * RL.total;
+    FA_CUDA(cudaFuncSetAttribute(reverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_rev));
+
+    uint8_t *adt_batch = nullptr;
+    unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
+    int64_t *req_off_d = nullptr;
+    int *err = nullptr;
+    void *cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    int rc = FA_OK;
+    auto cleanup = [&]() {
+        cudaFree(adt_batch); cudaFree(req); cudaFree(req_sorted); cudaFree(ctr);
+        cudaFree(req_off_d); cudaFree(err); cudaFree(cub_tmp);
+    };
+    int end_bit = 32;
+    {
+        int64_t rows = g.n + g.nU;
+        int b = 0;
+        while ((1ll << b) <= rows) ++b;
+        end_bit = 32 + b;
+        if (end_bit > 64) end_bit = 64;
+    }
+    if ((rc = dev_alloc((void **)&adt_batch, (size_t)maxB * g.mpad * 16)) ||
+        (rc = dev_alloc((void **)&req, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
+        (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
+        (rc = dev_alloc((void **)&ctr, sizeof(unsigned long long) * 8)) ||
+        (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
+        (rc = dev_alloc((void **)&err, sizeof(int)))) {
+        cleanup();
+        return rc;
+    }
+    cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, req, req_sorted, (int)std::max<int64_t>(maxreq, 1),
+                                   0, end_bit, st);
+    if ((rc = dev_alloc(&cub_tmp, cub_bytes))) {
+        cleanup();
+        return rc;
+    }
+#define FA_BUILD_CUDA(call)                                                              \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+            cleanup();                                                                   \
+            return FA_ECUDA;                                                             \
+        }                                                                                \
+    } while (0)
+    FA_BUILD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 8, st));
+    FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+    FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
+                                  cudaMemcpyHostToDevice, st));
+    for (const Batch &b : batches) {
+        rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size, ix->d.dproj,
+                               ix->d.cent, ix->d.dims, ix->d.offs, g.m, ix->d.dmax,
+                               ix->d.dist_min, ix->d.delta, nullptr, g.mpad, adt_batch, g.mpad, st);
+        if (rc) {
+            cleanup();
+            return rc;
+        }
+        int grid = (b.size + kSearchWarps - 1) / kSearchWarps;
+        build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
+            g, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+            req, ctr, err);
+        FA_BUILD_CUDA(cudaGetLastError());
+        size_t tb = cub_bytes;
+        FA_BUILD_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, req, req_sorted, (int)b.nreq, 0,
+                                                     end_bit, st));
+        int64_t chunks = (b.nreq + 31) / 32;
+        int rgrid = (int)((chunks + kReverseWarps - 1) / kReverseWarps);
+        reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
+            g, ix->d.sdt, req_sorted, b.nreq, ix->upper_owner, RL, ctr);
+        FA_BUILD_CUDA(cudaGetLastError());
+    }
+    unsigned long long hc[8];
+    int herr = 0;
+    FA_BUILD_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    FA_BUILD_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FA_BUILD_CUDA(cudaStreamSynchronize(st));
+#undef FA_BUILD_CUDA
+    cleanup();
+    if (herr) {
+        set_error("visited hash overflow (2^%d entries per warp): raise hash_log2", L.hash_log2);
+        return FA_EOVERFLOW;
+    }
+    ix->entry = ep;
+    ix->max_layer = ml;
+    res->entry_point = ep;
+    res->max_layer = ml;
+    res->n_batches = (int32_t)batches.size();
+    res->dist_comps = (int64_t)hc[0];
+    res->sym_comps = (int64_t)hc[1];
+    res->kernel_calls = (int64_t)hc[2];
+    res->visited = (int64_t)hc[3];
+    res->reverse_prunes = (int64_t)hc[4];
+    res->reverse_appends = (int64_t)hc[5];
+    return FA_OK;
+}
+
+static int run_query_encode(fa_index *ix, const float *qproj, int nq, uint8_t **adt_q,
+                            cudaStream_t st) {
+    FA_TRY(dev_alloc((void **)adt_q, (size_t)std::max(nq, 1) * ix->g.mpad * 16));
+    int rc = launch_encode_adt(qproj, nq, ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs, ix->g.m,
+                               ix->d.dmax, ix->d.dist_min, ix->d.delta, nullptr, ix->g.mpad, *adt_q,
+                               ix->g.mpad, st);
+    if (rc) {
+        cudaFree(*adt_q);
+        *adt_q = nullptr;
+    }
+    return rc;
+}
+
+extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *qproj, int nq,
+                               int ef, int k, int rerank_depth, int64_t entry, int max_layer,
+                               int64_t *out_ids, double *out_d, int64_t *counters, void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    if (entry < 0) {
+        set_error("cannot search an empty graph");
+        return FA_EEMPTY;
+    }
+    FA_CHECK_ARG(entry < ix->g.n, "entry point out of range");
+    FA_CHECK_ARG(ef >= 1 && ef <= 4096 && k >= 1, "need 1 <= k, 1 <= ef <= 4096");
+    FA_CHECK_ARG(rerank_depth == 0 || (ix->d.vecs && queries), "rerank needs vectors and queries");
+    cudaStream_t st = as_stream(stream);
+    if (counters) memset(counters, 0, 4 * sizeof(int64_t));
+    if (nq == 0) return FA_OK;
+    const int capmax = std::max(ix->g.cap0, ix->g.capU);
+    WarpLayout L;
+    L.init(ix->g.mpad, ef, capmax, pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0));
+    size_t smem = (size_t)kSearchWarps * L.total;
+    FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
+    FA_CUDA(cudaFuncSetAttribute(query_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    uint8_t *adt_q = nullptr;
+    FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
+    unsigned long long *ctr = nullptr;
+    int *err = nullptr;
+    int rc = dev_alloc((void **)&ctr, 8 * sizeof(unsigned long long));
+    if (!rc) rc = dev_alloc((void **)&err, sizeof(int));
+    unsigned long long hc[8] = {0};
+    int herr = 0;
+    if (!rc) {
+        cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
+        cudaMemsetAsync(err, 0, sizeof(int), st);
+        int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        query_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
+            ix->g, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
+            queries, L, out_ids, out_d, ctr, err);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            set_error("query search: %s", cudaGetErrorString(e));
+            rc = FA_ECUDA;
+        }
+    }
+    cudaFree(adt_q);
+    cudaFree(ctr);
+    cudaFree(err);
+    if (rc) return rc;
+    if (herr) {
+        set_error("visited hash overflow in query search (ef=%d)", ef);
+        return FA_EOVERFLOW;
+    }
+    if (counters)
+        for (int i = 0; i < 4; ++i) counters[i] = (int64_t)hc[i];
+    return FA_OK;
+}
+
+extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
+                                     const int64_t *entries, int width, int layer,
+                                     int32_t *out_ids, double *out_d, int32_t *out_n,
+                                     int64_t *counters, void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    FA_CHECK_ARG(width >= 1 && width <= 4096, "width=%d outside [1,4096]", width);
+    FA_CHECK_ARG(layer >= 0, "layer < 0");
+    cudaStream_t st = as_stream(stream);
+    if (counters) memset(counters, 0, 4 * sizeof(int64_t));
+    if (nq == 0) return FA_OK;
+    const int capmax = std::max(ix->g.cap0, ix->g.capU);
+    WarpLayout L;
+    L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0));
+    size_t smem = (size_t)kSearchWarps * L.total;
+    FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
+    FA_CUDA(cudaFuncSetAttribute(layer_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    uint8_t *adt_q = nullptr;
+    FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
+    unsigned long long *ctr = nullptr;
+    int *err = nullptr;
+    int rc = dev_alloc((void **)&ctr, 8 * sizeof(unsigned long long));
+    if (!rc) rc = dev_alloc((void **)&err, sizeof(int));
+    unsigned long long hc[8] = {0};
+    int herr = 0;
+    if (!rc) {
+        cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
+        cudaMemsetAsync(err, 0, sizeof(int), st);
+        int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        layer_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
+            ix->g, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            set_error("layer search: %s", cudaGetErrorString(e));
+            rc = FA_ECUDA;
+        }
+    }
+    cudaFree(adt_q);
+    cudaFree(ctr);
+    cudaFree(err);
+    if (rc) return rc;
+    if (herr) {
+        set_error("visited hash overflow in layer search (width=%d)", width);
+        return FA_EOVERFLOW;
+    }
+    if (counters)
+        for (int i = 0; i < 4; ++i) counters[i] = (int64_t)hc[i];
+    return FA_OK;
+}
+
+extern "C" int fa_index_export_blocks(fa_index *ix, uint8_t *base_blocks, int64_t base_stride,
+                                      uint8_t *upper_blocks, int64_t upper_stride, void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    const Graph &g = ix->g;
+    const int nb0 = (g.cap0 + 15) / 16, nbU = (g.capU + 15) / 16;
+    FA_CHECK_ARG(base_stride >= 4 + 4 * g.cap0 + nb0 * g.m * 16, "base stride too small");
+    cudaStream_t st = as_stream(stream);
+    if (g.n) {
+        export_kernel<<<1184, 256, 0, st>>>(g, g.n, false, base_blocks, base_stride, g.cap0, g.cap0p);
+        FA_LAUNCH_CHECK();
+    }
+    if (g.nU) {
+        FA_CHECK_ARG(upper_blocks && upper_stride >= 4 + 4 * g.capU + nbU * g.m * 16,
+                     "upper stride too small");
+        export_kernel<<<1184, 256, 0, st>>>(g, g.nU, true, upper_blocks, upper_stride, g.capU,
+                                            g.capUp);
+        FA_LAUNCH_CHECK();
+    }
+    return FA_OK;
+}
+
+extern "C" int fa_index_import_blocks(fa_index *ix, const uint8_t *base_blocks, int64_t base_stride,
+                                      const uint8_t *upper_blocks, int64_t upper_stride,
+                                      void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    const Graph &g = ix->g;
+    FA_CHECK_ARG(base_stride >= 4 + 4 * g.cap0, "base stride too small");
+    cudaStream_t st = as_stream(stream);
+    if (g.n) {
+        import_kernel<<<1184, 256, 0, st>>>(g, g.n, false, base_blocks, base_stride, g.cap0, g.cap0p);
+        FA_LAUNCH_CHECK();
+    }
+    if (g.nU) {
+        FA_CHECK_ARG(upper_blocks && upper_stride >= 4 + 4 * g.capU, "upper stride too small");
+        import_kernel<<<1184, 256, 0, st>>>(g, g.nU, true, upper_blocks, upper_stride, g.capU,
+                                            g.capUp);
+        FA_LAUNCH_CHECK();
+    }
+    return FA_OK;
+}

@@ -1,0 +1,149 @@
+// K1 entry points: parity hooks (flash_batch_distance_many / _blocks) and the
+// standalone HBM-bound block scan.
+#include "scan.cuh"
+
+namespace fa {
+
+// One warp per case: the case's own table + one 16-slot batch.
+template <int NR>
+__global__ void __launch_bounds__(256) scan_cases_kernel(const uint8_t *__restrict__ adts,
+                                                         const uint8_t *__restrict__ codes, int m,
+                                                         int64_t ncases, uint8_t *__restrict__ out) {
+    const int lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < ncases;
+         c += warps) {
+        WarpTable<NR> tab;
+        tab.load(adts + c * m * 16, m, lane);
+        uint32_t v = scan_batch<NR>(tab, codes + c * m * 16, m, lane);
+        if ((lane & 2) == 0) out[c * 16 + slot_of_lane(lane)] = (uint8_t)v;
+    }
+}
+
+// One warp per batch of a block.
+template <int NR>
+__global__ void scan_blocks_kernel(const uint8_t *__restrict__ adt, const uint8_t *__restrict__ codes,
+                                   int m, int nb, uint8_t *__restrict__ out) {
+    const int lane = lane_id();
+    const int b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (b >= nb) return;
+    WarpTable<NR> tab;
+    tab.load(adt, m, lane);
+    uint32_t v = scan_batch<NR>(tab, codes + (size_t)b * m * 16, m, lane);
+    if ((lane & 2) == 0) out[b * 16 + slot_of_lane(lane)] = (uint8_t)v;
+}
+
+// Standalone scan: warp per (query, slice of its block list).  Each block is
+// [int32 count | pad | int32 ids[cap] | codes nb x m x 16] in the padded
+// device layout.  out[q] = min over live slots of (d << 32 | id); several
+// warps of one query combine with atomicMin.
+template <int NR>
+__global__ void __launch_bounds__(256) scan_select_kernel(
+    const uint8_t *__restrict__ adt, int nq, const uint8_t *__restrict__ blocks,
+    int64_t block_stride, int64_t codes_off, int cap, int m, const int32_t *__restrict__ sel,
+    int nsel, int slices, unsigned long long *__restrict__ out) {
+    const int lane = lane_id();
+    const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int q = gw / slices;
+    const int slice = gw % slices;
+    if (q >= nq) return;
+    WarpTable<NR> tab;
+    tab.load(adt + (size_t)q * m * 16, m, lane);
+    const int nb = (cap + 15) >> 4;
+    const int per = (nsel + slices - 1) / slices;
+    const int lo = slice * per;
+    const int hi = min(nsel, lo + per);
+    unsigned long long best = ~0ull;
+    const int32_t *qsel = sel + (size_t)q * nsel;
+    for (int s = lo; s < hi; ++s) {
+        const uint8_t *blk = blocks + (int64_t)__ldg(qsel + s) * block_stride;
+        int cnt = __ldg(reinterpret_cast<const int32_t *>(blk));
+        cnt = min(cnt, cap);
+        const int32_t *ids = reinterpret_cast<const int32_t *>(blk + 16);
+        const uint8_t *cod = blk + codes_off;
+        for (int b = 0; b < nb; ++b) {
+            uint32_t v = scan_batch<NR>(tab, cod + (size_t)b * m * 16, m, lane);
+            int slot = b * 16 + slot_of_lane(lane);
+            if ((lane & 2) == 0 && slot < cnt) {
+                int id = __ldg(ids + slot);
+                if (id >= 0) {
+                    unsigned long long key = ((unsigned long long)v << 32) | (uint32_t)id;
+                    best = key < best ? key : best;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other < best ? other : best;
+    }
+    if (lane == 0 && best != ~0ull) atomicMin(out + q, best);
+}
+
+}  // namespace fa
+
+using namespace fa;
+
+extern "C" int fa_scan_cases_dev(const uint8_t *adts, const uint8_t *codes, int m, int64_t ncases,
+                                 uint8_t *out, void *stream) {
+    FA_CHECK_ARG(m >= 1 && m <= 128, "m=%d outside [1,128]", m);
+    FA_CHECK_ARG(ncases >= 0, "ncases < 0");
+    if (ncases == 0) return FA_OK;
+    cudaStream_t st = as_stream(stream);
+    int64_t blocks = (ncases + 7) / 8;
+    int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
+    if (m <= 32) scan_cases_kernel<1><<<grid, 256, 0, st>>>(adts, codes, m, ncases, out);
+    else if (m <= 64) scan_cases_kernel<2><<<grid, 256, 0, st>>>(adts, codes, m, ncases, out);
+    else if (m <= 96) scan_cases_kernel<3><<<grid, 256, 0, st>>>(adts, codes, m, ncases, out);
+    else scan_cases_kernel<4><<<grid, 256, 0, st>>>(adts, codes, m, ncases, out);
+    FA_LAUNCH_CHECK();
+    return FA_OK;
+}
+
+extern "C" int fa_scan_blocks_dev(const uint8_t *adt, const uint8_t *codes, int m, int nb,
+                                  uint8_t *out, void *stream) {
+    FA_CHECK_ARG(m >= 1 && m <= 128, "m=%d outside [1,128]", m);
+    FA_CHECK_ARG(nb >= 0, "nb < 0");
+    if (nb == 0) return FA_OK;
+    cudaStream_t st = as_stream(stream);
+    int grid = (nb + 3) / 4;
+    if (m <= 32) scan_blocks_kernel<1><<<grid, 128, 0, st>>>(adt, codes, m, nb, out);
+    else if (m <= 64) scan_blocks_kernel<2><<<grid, 128, 0, st>>>(adt, codes, m, nb, out);
+    else if (m <= 96) scan_blocks_kernel<3><<<grid, 128, 0, st>>>(adt, codes, m, nb, out);
+    else scan_blocks_kernel<4><<<grid, 128, 0, st>>>(adt, codes, m, nb, out);
+    FA_LAUNCH_CHECK();
+    return FA_OK;
+}
+
+extern "C" int fa_scan_select_dev(const uint8_t *adt, int nq, const uint8_t *blocks,
+                                  int64_t nblocks, int64_t block_stride, int64_t codes_off, int cap,
+                                  int m, const int32_t *sel, int nsel, uint64_t *out_u64,
+                                  void *stream) {
+    FA_CHECK_ARG(m >= 1 && m <= 128, "m=%d outside [1,128]", m);
+    FA_CHECK_ARG(codes_off % 16 == 0 && block_stride % 16 == 0, "block layout must be 16B aligned");
+    FA_CHECK_ARG(nq >= 0 && nsel >= 0 && nblocks >= 0, "negative sizes");
+    if (nq == 0) return FA_OK;
+    cudaStream_t st = as_stream(stream);
+    unsigned long long *out = reinterpret_cast<unsigned long long *>(out_u64);
+    FA_CUDA(cudaMemsetAsync(out, 0xff, sizeof(unsigned long long) * nq, st));
+    // enough warps to keep >= 32 KB of block bytes in flight per SM
+    int slices = 1;
+    while ((int64_t)nq * slices < 148 * 48 && slices * 8 <= nsel) slices *= 2;
+    int64_t warps = (int64_t)nq * slices;
+    int grid = (int)((warps + 7) / 8);
+    if (m <= 32)
+        scan_select_kernel<1><<<grid, 256, 0, st>>>(adt, nq, blocks, block_stride, codes_off, cap,
+                                                    m, sel, nsel, slices, out);
+    else if (m <= 64)
+        scan_select_kernel<2><<<grid, 256, 0, st>>>(adt, nq, blocks, block_stride, codes_off, cap,
+                                                    m, sel, nsel, slices, out);
+    else if (m <= 96)
+        scan_select_kernel<3><<<grid, 256, 0, st>>>(adt, nq, blocks, block_stride, codes_off, cap,
+                                                    m, sel, nsel, slices, out);
+    else
+        scan_select_kernel<4><<<grid, 256, 0, st>>>(adt, nq, blocks, block_stride, codes_off, cap,
+                                                    m, sel, nsel, slices, out);
+    FA_LAUNCH_CHECK();
+    return FA_OK;
+}

@@ -1,0 +1,264 @@
+// Search kernels: batched-insertion search (build), query search with exact
+// rerank (search_batch), and the single-layer hook (greedy_search_layer).
+#include "kernels.cuh"
+
+namespace fa {
+
+__device__ __forceinline__ int64_t row_global(const Graph &g, int layer, int y) {
+    return layer == 0 ? (int64_t)y : g.n + __ldg(g.uoff + y) + layer - 1;
+}
+
+// Per-warp workspace pointers.
+struct WarpWS {
+    uint8_t *adt;
+    unsigned long long *T, *X, *S;
+    int32_t *fresh;
+    uint32_t *fdist;
+    uint32_t *H;
+    __device__ WarpWS(uint8_t *base, const WarpLayout &L) {
+        adt = base + L.adt;
+        T = reinterpret_cast<unsigned long long *>(base + L.T);
+        X = reinterpret_cast<unsigned long long *>(base + L.X);
+        S = reinterpret_cast<unsigned long long *>(base + L.S);
+        fresh = reinterpret_cast<int32_t *>(base + L.fresh);
+        fdist = reinterpret_cast<uint32_t *>(base + L.fdist);
+        H = reinterpret_cast<uint32_t *>(base + L.hash);
+    }
+};
+
+__device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned long long *ctr,
+                                               int lane) {
+    if (lane == 0) {
+        atomicAdd(ctr + 0, c.dist);
+        atomicAdd(ctr + 1, c.sym);
+        atomicAdd(ctr + 2, c.kcalls);
+        atomicAdd(ctr + 3, c.visited);
+    }
+}
+
+// One warp inserts one vertex of the batch: descent, per-layer beam search of
+// width C, forward selection (cap R), forward row write, reverse requests.
+// Mirrors insert_one (_core.pyx:501-536) against the graph as of batch start.
+__global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
+    Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ adt_batch, int start,
+    int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
+    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int sdt_bytes = round_up(g.m * 256, 128);
+    uint8_t *sdtT = smem;
+    stage_sdt_T(sdt, g.m, sdtT, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    const int p = blockIdx.x * kSearchWarps + wid;
+    if (p >= size) return;
+    WarpWS ws(smem + sdt_bytes + wid * L.total, L);
+    const int x = start + p;
+    load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
+    __syncwarp();
+    SearchCounters cnt = {0, 0, 0, 0};
+    const int level = __ldg(g.levels + x);
+    int cur = ep;
+    uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
+    cnt.dist += 1;
+    for (int layer = ml; layer > level; --layer)
+        hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+    const int top = min(ml, level);
+    unsigned long long *myreq = req + __ldg(req_off + p);
+    int32_t *kept = reinterpret_cast<int32_t *>(ws.H);
+    uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
+    for (int layer = top; layer >= 0; --layer) {
+        int ts = 0;
+        bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.X, ws.S, ws.fresh,
+                               ws.fdist, ws.H, L.hash_log2, cnt, lane);
+        if (!ok) {
+            if (lane == 0) atomicExch(err, 1);
+            for (int l = layer; l >= 0; --l)
+                for (int j = lane; j < R; j += 32) myreq[(size_t)(top - l) * R + j] = KEY_MAX;
+            flush_counters(cnt, ctr, lane);
+            return;
+        }
+        unsigned long long sym = 0;
+        const unsigned long long *T = ws.T;
+        int nsel = warp_select_heur(
+            sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
+            [&](int j, int &v, double &dv) {
+                unsigned long long k = T[j];
+                v = key_id(k);
+                dv = (double)key_d(k);
+            },
+            kept, kcodes, lane, &sym);
+        cnt.sym += sym;
+        // forward row of x (write_forward, _core.pyx:424-438); rows past the
+        // live count keep -1 so readers need only the id row
+        int32_t *row = const_cast<int32_t *>(row_ids(g, layer, x));
+        const int cap = layer_cap(g, layer);
+        for (int j = lane; j < cap; j += 32) row[j] = j < nsel ? kept[j] : -1;
+        if (lane == 0) {
+            if (layer == 0) {
+                g.cnt0[x] = nsel;
+                g.cons0[x] = 0;
+            } else {
+                int64_t r = __ldg(g.uoff + x) + layer - 1;
+                g.cntU[r] = nsel;
+                g.consU[r] = 0;
+            }
+        }
+        unsigned long long *lreq = myreq + (size_t)(top - layer) * R;
+        for (int j = lane; j < R; j += 32)
+            lreq[j] = j < nsel ? ((unsigned long long)row_global(g, layer, kept[j]) << 32) |
+                                     (uint32_t)x
+                               : KEY_MAX;
+        cur = key_id(ws.T[0]);
+        curd = key_d(ws.T[0]);
+        __syncwarp();
+    }
+    flush_counters(cnt, ctr, lane);
+}
+
+// Warp-cooperative fp32 L2 (fa_l2sq_f32 tree, common.cuh l2_tree) of four
+// (query, vector) pairs at once: lane group g = lane/8 handles pair g and lane
+// k = lane%8 owns accumulator k of the 8-wide main loop.
+__device__ __forceinline__ float warp_l2_group(const float *q, const float *v, int d, int lane) {
+    const int k = lane & 7;
+    int nfull = d >= 8 ? d / 8 : 0;
+    float acc = 0.f;
+    if (q && v)
+        for (int c = 0; c < nfull; ++c) {
+            float e = __fsub_rn(__ldg(q + 8 * c + k), __ldg(v + 8 * c + k));
+            acc = __fadd_rn(acc, __fmul_rn(e, e));
+        }
+    const unsigned full = 0xffffffffu;
+    float hi = __shfl_down_sync(full, acc, 4);
+    float vk = (k < 4) ? __fadd_rn(acc, hi) : 0.f;  // v[k] = acc[k] + acc[k+4]
+    int i = 8 * nfull;
+    bool four = (d - i) >= 4;
+    float wk = vk;
+    if (four && k < 4 && q && v) {
+        float e = __fsub_rn(__ldg(q + i + k), __ldg(v + i + k));
+        wk = __fmaf_rn(e, e, vk);
+    }
+    float w2 = __shfl_down_sync(full, wk, 2);
+    float t = __fadd_rn(wk, w2);  // lane0: w0+w2, lane1: w1+w3
+    float t1 = __shfl_down_sync(full, t, 1);
+    float s = __fadd_rn(t, t1);   // lane k==0: (w0+w2)+(w1+w3)
+    if (!four && nfull == 0) s = 0.f;
+    if (four) i += 4;
+    if (k == 0 && q && v)
+        for (; i < d; ++i) {
+            float e = __fsub_rn(__ldg(q + i), __ldg(v + i));
+            s = __fmaf_rn(e, e, s);
+        }
+    return s;  // valid in lane k == 0 of the group
+}
+
+// search_one (_core.pyx:784-814): descent on layers ml..1, layer-0 search of
+// width ef, optional exact rerank of the first rerank_depth results with
+// (d, id) ordering (fa_sort_pairs), then the first k.
+__global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
+    Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep, int ml, int ef, int k,
+    int rerank_depth, const float *__restrict__ vecs, int dim, const float *__restrict__ queries,
+    WarpLayout L, int64_t *__restrict__ out_ids, double *__restrict__ out_d,
+    unsigned long long *__restrict__ ctr, int *err) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    const int q = blockIdx.x * kSearchWarps + wid;
+    if (q >= nq) return;
+    WarpWS ws(smem + wid * L.total, L);
+    load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
+    __syncwarp();
+    SearchCounters cnt = {0, 0, 0, 0};
+    int cur = ep;
+    uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
+    cnt.dist += 1;
+    for (int layer = ml; layer > 0; --layer)
+        hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+    int ts = 0;
+    bool ok = layer_search(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.X, ws.S, ws.fresh, ws.fdist,
+                           ws.H, L.hash_log2, cnt, lane);
+    int64_t *oid = out_ids + (size_t)q * k;
+    double *od = out_d + (size_t)q * k;
+    if (!ok) {
+        if (lane == 0) atomicExch(err, 1);
+        flush_counters(cnt, ctr, lane);
+        return;
+    }
+    if (rerank_depth > 0) {
+        const int rr = min(rerank_depth, ts);
+        // exact distances into X (as double bits), ids into S-adjacent fresh? use X/T
+        double *dd = reinterpret_cast<double *>(ws.X);
+        const float *qv = queries + (size_t)q * dim;
+        for (int base = 0; base < rr; base += 4) {
+            int j = base + (lane >> 3);
+            const float *vv = j < rr ? vecs + (size_t)key_id(ws.T[j]) * dim : nullptr;
+            float s = warp_l2_group(j < rr ? qv : nullptr, vv, dim, lane);
+            if ((lane & 7) == 0 && j < rr) dd[j] = (double)s;
+        }
+        __syncwarp();
+        // rank sort by (d, id) (fa_pair_cmp, _simd.h:237-243)
+        for (int j = lane; j < rr; j += 32) {
+            double dj = dd[j];
+            int idj = key_id(ws.T[j]);
+            int rank = 0;
+            for (int t = 0; t < rr; ++t) {
+                double dt = dd[t];
+                int idt = key_id(ws.T[t]);
+                rank += (dt < dj) || (dt == dj && idt < idj);
+            }
+            if (rank < k) {
+                oid[rank] = idj;
+                od[rank] = dj;
+            }
+        }
+        for (int j = rr + lane; j < k; j += 32) {
+            oid[j] = -1;
+            od[j] = __longlong_as_double(0x7ff0000000000000ll);
+        }
+    } else {
+        for (int j = lane; j < k; j += 32) {
+            if (j < ts) {
+                oid[j] = key_id(ws.T[j]);
+                od[j] = (double)key_d(ws.T[j]);
+            } else {
+                oid[j] = -1;
+                od[j] = __longlong_as_double(0x7ff0000000000000ll);
+            }
+        }
+    }
+    flush_counters(cnt, ctr, lane);
+}
+
+// greedy_search_layer (_core.pyx:891-939): one layer from a given entry.
+__global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
+    Graph g, const uint8_t *__restrict__ adt_q, int nq, const int64_t *__restrict__ entries,
+    int width, int layer, WarpLayout L, int32_t *__restrict__ out_ids, double *__restrict__ out_d,
+    int32_t *__restrict__ out_n, unsigned long long *__restrict__ ctr, int *err) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    const int q = blockIdx.x * kSearchWarps + wid;
+    if (q >= nq) return;
+    WarpWS ws(smem + wid * L.total, L);
+    load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
+    __syncwarp();
+    SearchCounters cnt = {0, 0, 0, 0};
+    const int entry = (int)entries[q];
+    uint32_t d0 = adt_one(ws.adt, g.codes + (size_t)entry * g.mpad, g.mpad, lane);
+    cnt.dist += 1;
+    int ts = 0;
+    bool ok = layer_search(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.X, ws.S, ws.fresh,
+                           ws.fdist, ws.H, L.hash_log2, cnt, lane);
+    if (!ok) {
+        if (lane == 0) atomicExch(err, 1);
+        ts = 0;
+    }
+    for (int j = lane; j < width; j += 32) {
+        out_ids[(size_t)q * width + j] = j < ts ? key_id(ws.T[j]) : -1;
+        out_d[(size_t)q * width + j] = j < ts ? (double)key_d(ws.T[j]) : 0.0;
+    }
+    if (lane == 0) out_n[q] = ts;
+    flush_counters(cnt, ctr, lane);
+}
+
+}  // namespace fa

@@ -1,0 +1,339 @@
+// K4/K7: warp-per-point best-first layer search with (d, id) total order,
+// greedy upper-layer descent, and the shared per-warp workspace.
+//
+// Reference semantics restated with a strict total order:
+//   search_layer (_core.pyx:278-342)  -> layer_search below
+//   hill_climb   (_core.pyx:345-385)  -> hill_climb below
+// key(u) = (d(u) << 32) | (u << 1) | expanded, d = min(sum ADT, 255).
+//
+// Device graph layout (B200-first, SoA instead of the reference's inlined
+// blocks, layout.py:1-45): per layer, ids rows of `capp` int32 (cap rounded to
+// 32 -> 128-byte aligned rows, -1 beyond the live count) + a count array, and
+// one flat code table n x mpad bytes (mpad = m rounded to 16, zero padded).
+// A visited neighbour costs only its 4-byte id; fresh neighbours gather their
+// m code bytes from the L2-resident code table.
+#pragma once
+
+#include "select.cuh"
+
+namespace fa {
+
+struct Graph {
+    int64_t n;
+    int m, mpad;
+    int cap0, capU;    // live capacity per layer kind (2R, R)
+    int cap0p, capUp;  // row stride in int32
+    int32_t *adj0, *cnt0;
+    int32_t *adjU, *cntU;
+    uint8_t *cons0, *consU;  // row holds exactly a prune result, in order
+    const uint8_t *codes;    // n x mpad
+    const int32_t *levels;
+    const int64_t *uoff;
+    int64_t nU;
+};
+
+__device__ __forceinline__ const int32_t *row_ids(const Graph &g, int layer, int v) {
+    if (layer == 0) return g.adj0 + (int64_t)v * g.cap0p;
+    return g.adjU + (__ldg(g.uoff + v) + layer - 1) * g.capUp;
+}
+__device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
+    return layer == 0 ? g.cap0 : g.capU;
+}
+
+// ---- per-warp workspace ----------------------------------------------------
+struct WarpLayout {
+    int adt, T, X, S, fresh, fdist, hash, total;
+    int hash_log2;
+    __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
+    __host__ __device__ void init(int mpad, int W, int capmax, int hlog2) {
+        hash_log2 = hlog2;
+        int o = 0;
+        adt = o; o += round_up(adt_bytes(mpad), 16);
+        T = o; o += round_up(W, 32) * 8;
+        X = o; o += round_up(W, 32) * 8;
+        S = o; o += 32 * 8;
+        fresh = o; o += round_up(capmax, 32) * 4;
+        fdist = o; o += round_up(capmax, 32) * 4;
+        hash = o; o += (4 << hlog2);
+        total = round_up(o, 128);
+    }
+};
+
+// Skewed ADT rows: row r at ((r + r/16) * 16) so the 16-subspace chunks read by
+// different lane groups fall in different banks.
+__device__ __forceinline__ int adt_row_off(int r) { return (r + (r >> 4)) << 4; }
+
+__device__ __forceinline__ void load_adt_smem(uint8_t *adt_s, const uint8_t *adt, int mpad,
+                                              int lane) {
+    for (int r = lane; r < mpad; r += 32)
+        *reinterpret_cast<uint4 *>(adt_s + adt_row_off(r)) =
+            __ldg(reinterpret_cast<const uint4 *>(adt + (size_t)r * 16));
+}
+
+// Saturated ADT distance of one code row (single vertex: entry point).
+__device__ __forceinline__ uint32_t adt_one(const uint8_t *adt_s, const uint8_t *code, int mpad,
+                                            int lane) {
+    uint32_t s = 0;
+    for (int r = lane; r < mpad; r += 32) s += adt_s[adt_row_off(r) + __ldg(code + r)];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s > 255u ? 255u : s;
+}
+
+// Distances of the nf ids in ids_s[] (shared) into out_s[] (shared).  G lanes per
+// id, each summing one 16-subspace chunk gathered with a 16-byte load.
+template <int G>
+__device__ __forceinline__ void gather_dists(const uint8_t *adt_s, const uint8_t *__restrict__ codes,
+                                             int mpad, const int32_t *ids_s, int nf,
+                                             uint32_t *out_s, int lane) {
+    constexpr int PER = 32 / G;
+    const int gi = lane / G, c = lane % G;
+    for (int base = 0; base < nf; base += PER) {
+        const int f = base + gi;
+        uint32_t sum = 0;
+        if (f < nf && c * 16 < mpad) {
+            const int id = ids_s[f];
+            uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
+            const uint8_t *rowbase = adt_s + adt_row_off(c * 16);
+            uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    int r = q * 4 + b;  // row within chunk; chunk rows are contiguous
+                    sum += rowbase[r * 16 + ((ww[q] >> (8 * b)) & 0xffu)];
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (c == 0 && f < nf) out_s[f] = sum > 255u ? 255u : sum;
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void gather_dists_dispatch(const uint8_t *adt_s, const uint8_t *codes,
+                                                      int mpad, const int32_t *ids_s, int nf,
+                                                      uint32_t *out_s, int lane) {
+    gather_dists<G>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
+}
+
+__device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *codes, int mpad,
+                                          const int32_t *ids_s, int nf, uint32_t *out_s, int lane) {
+    const int chunks = mpad >> 4;
+    if (chunks <= 1) gather_dists<1>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
+    else if (chunks <= 2) gather_dists<2>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
+    else if (chunks <= 4) gather_dists<4>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
+    else gather_dists<8>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
+    __syncwarp();
+}
+
+// ---- visited hash (exact, open addressing in shared memory) ---------------
+__device__ __forceinline__ void hash_clear(uint32_t *H, int hlog2, int lane) {
+    uint4 z = make_uint4(0, 0, 0, 0);
+    const int n4 = (1 << hlog2) >> 2;
+    for (int i = lane; i < n4; i += 32) reinterpret_cast<uint4 *>(H)[i] = z;
+}
+// true iff id was absent (and is now present)
+__device__ __forceinline__ bool hash_insert(uint32_t *H, int hlog2, int id) {
+    const uint32_t key = (uint32_t)id + 1u;
+    const uint32_t mask = (1u << hlog2) - 1u;
+    uint32_t h = (key * 2654435761u) >> (32 - hlog2);
+    while (true) {
+        uint32_t old = atomicCAS(H + h, 0u, key);
+        if (old == 0u) return true;
+        if (old == key) return false;
+        h = (h + 1u) & mask;
+    }
+}
+
+// ---- sorted top-W buffer ---------------------------------------------------
+constexpr unsigned long long KEY_MAX = ~0ull;
+
+__device__ __forceinline__ unsigned long long make_key(uint32_t d, int id) {
+    return ((unsigned long long)d << 32) | ((unsigned long long)(uint32_t)id << 1);
+}
+__device__ __forceinline__ int key_id(unsigned long long k) { return (int)((k >> 1) & 0x7fffffffu); }
+__device__ __forceinline__ uint32_t key_d(unsigned long long k) { return (uint32_t)(k >> 32); }
+
+// Bitonic sort of 32 keys, one per lane, ascending by lane.
+__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
+            bool up = ((lane & k) == 0);
+            bool lower = ((lane & j) == 0);
+            bool take_min = (lower == up);
+            unsigned long long mn = x < y ? x : y, mx = x < y ? y : x;
+            x = take_min ? mn : mx;
+        }
+    }
+    return x;
+}
+
+// number of entries of sorted a[0..n) strictly less than x
+__device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, unsigned long long x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Merge `ns` sorted keys (lane l holds s for l < ns, KEY_MAX beyond) into the
+// sorted buffer T[0..ts), keeping the W smallest.  Returns the lowest position
+// that changed (W if nothing entered).  X, S are scratch.
+__device__ __forceinline__ int merge_into(unsigned long long *T, int &ts, int W,
+                                          unsigned long long *X, unsigned long long *S,
+                                          unsigned long long s, int ns, int lane) {
+    if (ns == 0) return W;
+    if (lane < ns) S[lane] = s;
+    __syncwarp();
+    int p = lane < ns ? lane + lower_rank(T, ts, s) : W;
+    const int p0 = __shfl_sync(0xffffffffu, p, 0);
+    const int newts = min(W, ts + ns);
+    if (p0 >= newts) return W;
+    for (int i = p0 + lane; i < ts; i += 32) {
+        unsigned long long t = T[i];
+        int np = i + lower_rank(S, ns, t);
+        if (np < newts) X[np - p0] = t;
+    }
+    if (lane < ns && p < newts) X[p - p0] = s;
+    __syncwarp();
+    for (int i = p0 + lane; i < newts; i += 32) T[i] = X[i - p0];
+    __syncwarp();
+    ts = newts;
+    return p0;
+}
+
+struct SearchCounters {
+    unsigned long long dist, kcalls, visited, sym;
+};
+
+// Warp-cooperative best-first search on one layer.
+// On return T[0..ts) holds the result ascending by (d, id).
+// Returns false on visited-hash overflow.
+__device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
+                             const uint8_t *adt_s, unsigned long long *T, int &ts,
+                             unsigned long long *X, unsigned long long *S, int32_t *fresh,
+                             uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
+                             int lane) {
+    const int cap = layer_cap(g, layer);
+    const int hlimit = (1 << hlog2) - (1 << hlog2) / 8;
+    hash_clear(H, hlog2, lane);
+    __syncwarp();
+    if (lane == 0) {
+        hash_insert(H, hlog2, entry);
+        T[0] = make_key(entry_d, entry);
+    }
+    int nvis = 1;
+    ts = 1;
+    int cur = 0;
+    __syncwarp();
+    while (true) {
+        // next unexpanded member (all of T[0..cur) are expanded)
+        int found = -1;
+        while (cur < ts) {
+            int idx = cur + lane;
+            bool f = idx < ts && ((T[idx] & 1ull) == 0ull);
+            unsigned b = __ballot_sync(0xffffffffu, f);
+            if (b) {
+                found = cur + __ffs(b) - 1;
+                break;
+            }
+            cur += 32;
+        }
+        if (found < 0) break;
+        cur = found;
+        const int v = key_id(T[cur]);
+        __syncwarp();
+        if (lane == 0) T[cur] |= 1ull;
+        cnt.visited++;
+        const int32_t *ids = row_ids(g, layer, v);
+        if (nvis + cap > hlimit) return false;
+        // visited filter over the row, compacted in slot order
+        int nf = 0, nlive = 0;
+        for (int base = 0; base < cap; base += 32) {
+            int j = base + lane;
+            int u = j < cap ? __ldg(ids + j) : -1;
+            bool live = u >= 0;
+            bool fr = live && hash_insert(H, hlog2, u);
+            unsigned bl = __ballot_sync(0xffffffffu, live);
+            unsigned bf = __ballot_sync(0xffffffffu, fr);
+            if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = u;
+            nf += __popc(bf);
+            nlive += __popc(bl);
+        }
+        nvis += nf;
+        cnt.kcalls += (nlive + 15) >> 4;
+        cnt.dist += nf;
+        __syncwarp();
+        if (nf == 0) continue;
+        dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
+        int lowest = W;
+        for (int base = 0; base < nf; base += 32) {
+            const int f = base + lane;
+            unsigned long long k = f < nf ? make_key(fdist[f], fresh[f]) : KEY_MAX;
+            const unsigned long long worst = ts < W ? KEY_MAX : T[W - 1];
+            bool keep = k < worst;
+            unsigned bk = __ballot_sync(0xffffffffu, keep);
+            int ns = __popc(bk);
+            if (ns == 0) continue;
+            k = keep ? k : KEY_MAX;
+            k = warp_sort32(k, lane);
+            int p0 = merge_into(T, ts, W, X, S, k, ns, lane);
+            lowest = min(lowest, p0);
+        }
+        if (lowest < cur) cur = lowest;
+    }
+    return true;
+}
+
+// Width-1 greedy descent (hill_climb, _core.pyx:345-385): move to the first
+// slot holding the minimum distance while it is strictly better.
+__device__ inline void hill_climb(const Graph &g, int layer, int &cur, uint32_t &curd,
+                           const uint8_t *adt_s, int32_t *ids_s, uint32_t *d_s,
+                           SearchCounters &cnt, int lane) {
+    const int cap = layer_cap(g, layer);
+    while (true) {
+        const int32_t *ids = row_ids(g, layer, cur);
+        int nlive = 0;
+        for (int base = 0; base < cap; base += 32) {
+            int j = base + lane;
+            int u = j < cap ? __ldg(ids + j) : -1;
+            if (j < cap) ids_s[j] = u;
+            nlive += __popc(__ballot_sync(0xffffffffu, u >= 0));
+        }
+        __syncwarp();
+        // live ids form a prefix (rows keep -1 beyond the count)
+        cnt.kcalls += (nlive + 15) >> 4;
+        cnt.dist += nlive;
+        if (nlive == 0) break;
+        dists_for(adt_s, g.codes, g.mpad, ids_s, nlive, d_s, lane);
+        unsigned long long best = KEY_MAX;
+        for (int j = lane; j < nlive; j += 32) {
+            unsigned long long k = ((unsigned long long)d_s[j] << 32) | (uint32_t)j;
+            best = k < best ? k : best;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+            best = y < best ? y : best;
+        }
+        uint32_t dmin = (uint32_t)(best >> 32);
+        int slot = (int)(best & 0xffffffffu);
+        if (dmin < curd) {
+            curd = dmin;
+            cur = ids_s[slot];
+            __syncwarp();
+        } else {
+            break;
+        }
+    }
+}
+
+}  // namespace fa

@@ -1,0 +1,89 @@
+// K5: warp-cooperative neighbour selection (select_heur, _core.pyx:388-408)
+// with Flash symmetric-table distances (sym_one -> fa_sdt_sum_sat,
+// _core.pyx:179-191, _simd.h:87-95).
+//
+// Candidates are scanned in the given order; v is kept iff no already-kept u
+// has sdt(u, v) < d_v; the scan stops once `cap` are kept.  The decision for v
+// is an OR over the kept set, so evaluating the kept set in parallel (lane t
+// takes kept[t], kept[t+32], ...) gives exactly the reference's decisions.
+//
+// Shared-memory layout: the SDT is stored transposed, sdtT[i][b][a] =
+// sdt[i][a][b], where b is the CANDIDATE's code.  All lanes test the same
+// candidate, so for subspace i every lane reads inside one 16-byte row
+// (4 banks): conflict-free.  Kept codes sit in rows of kstride = mpad + 4 bytes
+// (an odd number of words) so lane t's word reads land in distinct banks.
+#pragma once
+
+#include "common.cuh"
+
+namespace fa {
+
+__host__ __device__ inline int kept_stride(int mpad) { return mpad + 4; }
+
+// Stage sdt (m x 16 x 16, global) transposed into shared memory.
+__device__ __forceinline__ void stage_sdt_T(const uint8_t *__restrict__ sdt, int m, uint8_t *sdtT,
+                                            int tid, int nthreads) {
+    for (int t = tid; t < m * 256; t += nthreads) {
+        int i = t >> 8, a = (t >> 4) & 15, b = t & 15;
+        sdtT[(i << 8) + (b << 4) + a] = sdt[t];
+    }
+}
+
+// min(sum_i sdt[i][cu_i][cv_i], 255) with cu from shared (word-aligned row)
+// and cv from global/shared (uniform across the warp).
+__device__ __forceinline__ uint32_t sdt_sum_rows(const uint8_t *sdtT, int m, const uint8_t *cu,
+                                                 const uint8_t *cv) {
+    uint32_t acc = 0;
+    int i = 0;
+    for (; i + 4 <= m; i += 4) {
+        uint32_t wu = *reinterpret_cast<const uint32_t *>(cu + i);
+        uint32_t wv = *reinterpret_cast<const uint32_t *>(cv + i);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            uint32_t a_ = (wu >> (8 * b)) & 0xffu, b_ = (wv >> (8 * b)) & 0xffu;
+            acc += sdtT[((i + b) << 8) + (b_ << 4) + a_];
+        }
+    }
+    for (; i < m; ++i) acc += sdtT[(i << 8) + (cv[i] << 4) + cu[i]];
+    return acc > 255u ? 255u : acc;
+}
+
+// Generic warp selection.  get(j, &v, &dv_less) must return the candidate id
+// and a functor-like comparison: we pass the candidate distance as a double
+// (exact for the reference's integer-valued Flash distances and for arbitrary
+// hook inputs).  Candidate code rows are read from `codes` (global, row
+// stride cs bytes, 4-byte aligned, zero padded to mpad).  Returns the number
+// kept; kept ids in kept_ids[0..nk), their codes in kept_codes rows.
+template <class Get>
+__device__ int warp_select_heur(const uint8_t *sdtT, int m, int mpad,
+                                const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
+                                Get get, int32_t *kept_ids, uint8_t *kept_codes, int lane,
+                                unsigned long long *sym_count) {
+    const int ks = kept_stride(mpad);
+    int nk = 0;
+    unsigned long long sym = 0;
+    for (int j = 0; j < ncand && nk < cap; ++j) {
+        int v;
+        double dv;
+        get(j, v, dv);
+        const uint8_t *cv = codes + (size_t)v * cs;
+        bool bad = false;
+        for (int t = lane; t < nk; t += 32) {
+            uint32_t s = sdt_sum_rows(sdtT, m, kept_codes + t * ks, cv);
+            bad |= ((double)s < dv);
+        }
+        sym += nk;
+        if (!__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) kept_ids[nk] = v;
+            for (int i = lane * 4; i < mpad; i += 128)
+                *reinterpret_cast<uint32_t *>(kept_codes + nk * ks + i) =
+                    *reinterpret_cast<const uint32_t *>(cv + i);
+            ++nk;
+            __syncwarp();
+        }
+    }
+    if (sym_count && lane == 0) *sym_count += sym;
+    return nk;
+}
+
+}  // namespace fa
