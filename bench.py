@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark: Flash HNSW build throughput on one B200 (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 1,000,000 x 128 float32 (256-component
+mixture, rounded and clipped to 0..255; seeded synthetic), m = 64 subspaces x
+4-bit, uint8 tables, M = 32 (R), efConstruction = 200 (C).
+
+A "step" is one pass of the hot path over the whole input: project + encode
+every vector and insert all of them with the batched GPU build (the
+reference's graph_seconds: attach + build_graph).  The coder is trained once
+on the GPU before the timed region (reported as coding_seconds).  Inputs are
+resident in HBM when the timed region starts; the working set (vectors
+0.5 GB, adjacency 0.3 GB, codes 64 MB, visits spread over all of it) exceeds
+the 126 MB L2, so no flush is needed between steps.
+
+value  = vectors inserted per second (all ranks) — device time, CUDA events.
+e2e    = the same metric through the reference-facing host-array drop-in
+         (sm100.build_graph: numpy in, reference-layout blocks out), H2D/D2H
+         inside the timed region.
+roofline (dominant kernel = the build's search kernel) and a standalone block
+scan (K1) at the config's block shape, each against MEASURED_PEAKS.json.
+cpu_baseline: the reference's own compiled core (oracle/_ref, OpenMP on all
+host cores) building a bounded prefix of the same data.
+
+N > 1 (torchrun): "replicas only" — each rank builds its own full index; no
+collective on the data path; value = total vectors / max time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG = 2
+METRIC = "HNSW build vectors/sec and code-distance evals/sec (% HBM roofline), 1 B200"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(f"/tmp/fa_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4)
+                          if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ref_cpu_build(prov_full, levels_fn, n_sub, C, R, threads):
+    """The reference's compiled build_graph on the first n_sub vectors.
+    Returns (seconds, vec/s)."""
+    from oracle import refpkg
+    from paper_2502_18113_b200 import layout
+
+    core = refpkg.load_ref_core()
+    if core is None:
+        return None
+    m = prov_full["cent"].shape[0]
+    prov = dict(prov_full)
+    prov["proj"] = np.ascontiguousarray(prov_full["proj"][:n_sub])
+    prov["vecs"] = np.ascontiguousarray(prov_full["vecs"][:n_sub])
+    prov["codes"] = np.ascontiguousarray(prov_full["codes"][:n_sub]).copy()
+    levels = levels_fn(n_sub)
+    lv64 = levels.astype(np.int64)
+    uoff = np.where(lv64 > 0, np.cumsum(lv64) - lv64, -1)
+    base = layout.empty_rows(n_sub, 2 * R, m)
+    upper = layout.empty_rows(int(lv64.sum()), R, m)
+    t0 = time.perf_counter()
+    core.build_graph(4, prov, levels, base, uoff, upper, C, R, threads=threads,
+                     kernel=len(core.available_kernels()) - 1)
+    dt = time.perf_counter() - t0
+    return dt, n_sub / dt
+
+
+def cpu_prov(data, model):
+    """Reference-shaped prov dict from a trained model (host arrays)."""
+    proj = model["proj_fn"](data)
+    return {"vecs": data, "dim": data.shape[1], "proj": proj,
+            "codes": np.zeros((data.shape[0], model["cent"].shape[0]), np.uint8),
+            "cent": model["cent"], "dims": model["dims"], "offs": model["offs"],
+            "sdt": model["sdt"], "dist_min": model["dist_min"],
+            "delta": model["dist_max"] - model["dist_min"]}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU build on bounded samples."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import refpkg, train_np
+    from paper_2502_18113_b200 import dataset, graph
+
+    c = dataset.CONFIGS[CFG]
+    threads = os.cpu_count() or 1
+    if refpkg.load_ref_core() is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref not built (make -C oracle ref needs /root/reference)"}))
+        return
+    data, _ = dataset.baseline_config(CFG, n=args.ref_max, nq=0)
+    model = train_np.train(train_np.training_sample(data, 100_000, 0), c["d_f"], c["m_f"], 0, 10)
+    prov = cpu_prov(data, model)
+    lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
+    # size each step so the whole run stays within ~3 minutes
+    _, rate = ref_cpu_build(prov, lvf, 4000, c["efC"], c["M"], threads)
+    steps = args.steps + args.warmup
+    n_sub = int(min(args.ref_max, max(4000, rate * 150.0 / steps)))
+    for _ in range(args.warmup):
+        ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)
+    times = [ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)[0]
+             for _ in range(args.steps)]
+    ms = 1000.0 * float(np.mean(times))
+    value = n_sub / (ms / 1000.0)
+    sample = (f"first {n_sub} of {c['n']} config-2 vectors (prefix; CPU throughput falls "
+              f"with n, so this favours the CPU), build_graph threads={threads}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "vectors/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": {"workload": f"config{CFG}", "n": n_sub, "dim": c["dim"],
+                                        "M": c["M"], "efConstruction": c["efC"], "m": c["m_f"]},
+        "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def scan_benchmark(lib, torch, m, cap, peak, reps=5):
+    """Standalone K1 block scan over a > L2 padded block array."""
+    from paper_2502_18113_b200._lib import check
+
+    nb = (cap + 15) // 16
+    codes_off = 16 + 4 * cap
+    codes_off = (codes_off + 15) // 16 * 16
+    stride = (codes_off + nb * m * 16 + 127) // 128 * 128
+    nblocks = 1_000_000
+    g = torch.Generator(device="cuda").manual_seed(1)
+    blocks = torch.randint(0, 16, (nblocks, stride), dtype=torch.uint8, device="cuda",
+                           generator=g)
+    v = blocks[:, :16].view(torch.int32)
+    v[:, 0] = cap  # full blocks
+    ids = blocks[:, 16: 16 + 4 * cap].view(torch.int32)
+    ids.copy_(torch.randint(0, nblocks, ids.shape, dtype=torch.int32, device="cuda",
+                            generator=g))
+    nq, ns = 4096, 256
+    adt = torch.randint(0, 8, (nq, m, 16), dtype=torch.uint8, device="cuda", generator=g)
+    sel = torch.randint(0, nblocks, (nq, ns), dtype=torch.int32, device="cuda", generator=g)
+    out = torch.empty(nq, dtype=torch.int64, device="cuda")
+    call = lambda: check(lib.fa_scan_select_dev(  # noqa: E731
+        adt.data_ptr(), nq, blocks.data_ptr(), nblocks, stride, codes_off, cap, m,
+        sel.data_ptr(), ns, out.data_ptr(), None))
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    lanes = nq * ns * nb * 16
+    alg_bytes = nq * ns * (4 + nb * 16 * (m + 4))  # count + per batch: ids + codes
+    gbs = alg_bytes / (ms * 1e-3) / 1e9
+    del blocks
+    return {"kernel": "scan_select_kernel (K1)", "evals_per_s": lanes / (ms * 1e-3),
+            "ms_per_launch": ms, "bytes_per_launch": alg_bytes, "achieved": gbs,
+            "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "shape": f"m={m} cap={cap}, {nq} queries x {ns} random blocks of {nblocks}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override vector count")
+    ap.add_argument("--ref-max", type=int, default=200_000)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2502_18113_b200 import _lib, builder, dataset, flash, graph, layout, sm100
+
+    lib = _lib.load()
+    c = dataset.CONFIGS[CFG]
+    n = args.n or c["n"]
+    peak, peak_kind = load_peaks()
+    data, _ = dataset.baseline_config(CFG, n=n, nq=0)
+    x_dev = torch.from_numpy(data).cuda()
+
+    # coder training on the GPU (coding_seconds)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sample = builder.training_sample(data, builder.DEFAULT_SAMPLE, 0)
+    model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=10)
+    torch.cuda.synchronize()
+    coding_s = time.perf_counter() - t0
+
+    params = graph.BuildParams(C=c["efC"], R=c["M"], seed=0)
+    levels = graph.assign_layers(n, 0, c["M"])
+    provider = flash.FlashProvider(model)
+    provider.attach(data, vecs_dev=x_dev)
+    g = graph.GraphIndex(n, data.shape[1], params, "flash", model.m, levels)
+    g.create_device(provider)
+
+    def step(profile=0):
+        provider.reproject()  # project + encode every vector (device, in place)
+        _lib.check(lib.fa_index_set_codes(g.handle, provider.dev["codes"].data_ptr(),
+                                          provider.dev["codes"].shape[1], None))
+        return builder.build_device(g, provider, params, profile=profile)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        ctrs = [step() for _ in range(args.steps)]
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = n * world / (ms / 1000.0)
+
+    # per-kernel device times (one extra profiled step, outside the timed region)
+    prof = step(profile=1)
+    kernel_ms = {"encode": prof["ms_encode"], "search": prof["ms_search"],
+                 "sort": prof["ms_sort"], "reverse": prof["ms_reverse"]}
+    cap0, mpad = 2 * c["M"], (c["m_f"] + 15) // 16 * 16
+    # algorithmic bytes of the search kernel: one id row per expansion + the
+    # code row of every evaluated vertex
+    search_bytes = prof["visited"] * cap0 * 4 + prof["dist_comps"] * c["m_f"]
+    search_gbs = search_bytes / (prof["ms_search"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "build_search_kernel (K4+K5)",
+                "achieved": search_gbs, "peak": peak, "unit": "GB/s",
+                "frac": search_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_build": search_bytes,
+                "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}
+
+    out = {"metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (seeded config-2 mixture, no dataset download)",
+           "config": {"workload": f"config{CFG}", "n": n, "dim": c["dim"], "M": c["M"],
+                      "efConstruction": c["efC"], "m": c["m_f"], "subspace_bits": 4,
+                      "parallelism": f"replicas x{world}",
+                      "l2": "inputs larger than L2 (no flush)",
+                      "batch": {k: v for k, v in sm100.BUILD_OPTIONS.items() if k != "profile"}},
+           "coding_seconds": coding_s, "kernel_ms_per_build": kernel_ms,
+           "counters": {k: ctrs[-1][k] for k in ("dist_comps", "sym_comps", "visited",
+                                                  "kernel_calls", "reverse_prunes",
+                                                  "reverse_appends", "n_batches")},
+           "gpu_launches": int(ctrs[-1]["launches"] + 1) * args.steps,
+           "roofline": roofline, "clocks": clk.summary()}
+
+    if rank == 0:
+        out["scan"] = scan_benchmark(lib, torch, c["m_f"], cap0, peak)
+        if not args.no_e2e:
+            prov = provider.core_arrays()
+            prov = dict(prov, codes=prov["codes"].copy())
+            base = layout.empty_rows(n, cap0, model.m)
+            upper = layout.empty_rows(g.n_upper_rows, c["M"], model.m)
+            h2d = prov["proj"].nbytes + prov["codes"].nbytes + levels.nbytes + \
+                g.upper_offsets.nbytes + model.cent.nbytes + model.sdt.nbytes
+            d2h = prov["codes"].nbytes + base.nbytes + upper.nbytes
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            sm100.build_graph(4, prov, levels, base, g.upper_offsets, upper, c["efC"], c["M"])
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t1
+            out["e2e"] = {"value": n / e2e_s, "unit": "vectors/s", "h2d_bytes_per_step": h2d,
+                          "d2h_bytes_per_step": d2h, "seconds": e2e_s,
+                          "api": "sm100.build_graph (host numpy arrays, reference layout)"}
+        if not args.no_cpu_baseline:
+            from oracle import train_np
+
+            threads = os.cpu_count() or 1
+            pm = {"proj_fn": None, "cent": model.cent, "dims": model.dims, "offs": model.offs,
+                  "sdt": model.sdt, "dist_min": model.dist_min, "dist_max": model.dist_max}
+            cprov = provider.core_arrays()
+            lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
+            cal = ref_cpu_build(cprov, lvf, 4000, c["efC"], c["M"], threads)
+            if cal is None:
+                out["cpu_baseline"] = None
+            else:
+                n_cpu = int(min(n, max(4000, cal[1] * args.cpu_seconds)))
+                dt, rate = ref_cpu_build(cprov, lvf, n_cpu, c["efC"], c["M"], threads)
+                out["cpu_baseline"] = {
+                    "value": rate, "unit": "vectors/s", "cores": threads, "kind": "reference",
+                    "sample": f"first {n_cpu} of {n} vectors (prefix, same model), reference "
+                              f"compiled build_graph, OpenMP threads={threads}, {dt:.1f} s"}
+            del pm, train_np
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

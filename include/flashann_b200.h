@@ -94,6 +94,34 @@ int fa_select_dev(const uint8_t *sdt, int m, const uint8_t *codes, int code_stri
                   const int32_t *cand_ids, const double *cand_d, int ncand, int cap,
                   int32_t *out, int32_t *nout, void *stream);
 
+/* ---- coder training (flashann/kmeans.py, flashann/flash.py:63-107) ------- */
+
+/* State of numpy's PCG64 bit generator (Generator.bit_generator.state). */
+typedef struct {
+    unsigned long long s_hi, s_lo, inc_hi, inc_lo;
+    unsigned int has_uint32, uinteger;
+} fa_pcg64_state;
+
+/* Scratch bytes needed by fa_kmeans_subspaces_dev.                           */
+size_t fa_kmeans_scratch_bytes(int m, int nsub);
+
+/* kmeans(sub_i, 16, iters, seed+i) for every subspace i at once (one CTA per
+ * subspace; kmeans.py:35-76).  xs: ns x ld f32 projected sample; sel: m x nsub
+ * subsample rows (NULL = all rows, nsub = ns); states[i]: the PCG64 state of
+ * default_rng(seed+i) after the host-drawn permutation.  cent_out m x 16 x
+ * dmax f32 (zero padded), hist_out m x (iters+1) f64 inertia history.        */
+int fa_kmeans_subspaces_dev(const float *xs, int64_t ns, int ld, const int32_t *dims,
+                            const int32_t *offs, int m, const int32_t *sel, int nsub,
+                            const void *states, int iters, float *cent_out, int dmax,
+                            double *hist_out, void *scratch, void *stream);
+
+/* Range statistics of flash_train (flash.py:86-98): raw_sdt m x 16 x 16 f64
+ * (direct differences), range_out[0] = dist_min, range_out[1] = dist_max
+ * (sum of per-subspace maxima).  scratch: >= 3*m*8 bytes.                    */
+int fa_flash_range_dev(const float *xs, int64_t ns, int ld, const int32_t *dims,
+                       const int32_t *offs, int m, const float *cent, int dmax, double *raw_sdt,
+                       double *range_out, void *scratch, void *stream);
+
 /* ---- graph index (build + search) --------------------------------------- */
 
 typedef struct fa_index fa_index; /* opaque, device resident */
@@ -124,6 +152,7 @@ typedef struct {
     double batch_frac;    /* batch <= frac * |inserted| (0 = default)            */
     int seq_prefix;       /* first vertices inserted one per batch (-1 default)  */
     int hash_log2;        /* visited-hash size per warp = 2^hash_log2 (0 = auto) */
+    int profile;          /* 1: time every kernel class with CUDA events        */
 } fa_build_opts;
 
 typedef struct {
@@ -132,6 +161,8 @@ typedef struct {
     int32_t n_batches;
     int64_t dist_comps, sym_comps, kernel_calls, visited; /* _core.pyx:695-704 */
     int64_t reverse_prunes, reverse_appends;
+    int64_t launches;     /* kernels of this library launched by the build      */
+    double ms_encode, ms_search, ms_sort, ms_reverse; /* profile = 1 only       */
 } fa_build_result;
 
 /* Allocate the device graph (adjacency rows, counts, code table) for desc.   */

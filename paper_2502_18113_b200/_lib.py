@@ -34,13 +34,15 @@ class IndexDesc(C.Structure):
 
 class BuildOpts(C.Structure):
     _fields_ = [("C", C.c_int), ("batch_max", C.c_int), ("batch_frac", f64),
-                ("seq_prefix", C.c_int), ("hash_log2", C.c_int)]
+                ("seq_prefix", C.c_int), ("hash_log2", C.c_int), ("profile", C.c_int)]
 
 
 class BuildResult(C.Structure):
     _fields_ = [("entry_point", i64), ("max_layer", i32), ("n_batches", i32),
                 ("dist_comps", i64), ("sym_comps", i64), ("kernel_calls", i64),
-                ("visited", i64), ("reverse_prunes", i64), ("reverse_appends", i64)]
+                ("visited", i64), ("reverse_prunes", i64), ("reverse_appends", i64),
+                ("launches", i64), ("ms_encode", f64), ("ms_search", f64), ("ms_sort", f64),
+                ("ms_reverse", f64)]
 
     def counters(self) -> dict:
         return {"dist_comps": int(self.dist_comps), "sym_comps": int(self.sym_comps),
@@ -60,6 +62,11 @@ _SIGS = {
                                     C.c_int, vp, C.c_int, vp]),
     "fa_sdt_sum_dev": (C.c_int, [vp, C.c_int, vp, i64, vp, i64, i64, vp, vp]),
     "fa_select_dev": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
+    "fa_kmeans_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "fa_kmeans_subspaces_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp,
+                                          C.c_int, vp, C.c_int, vp, vp, vp]),
+    "fa_flash_range_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp, vp,
+                                     vp, vp]),
     "fa_index_create": (C.c_int, [C.POINTER(IndexDesc), C.POINTER(vp)]),
     "fa_index_destroy": (C.c_int, [vp]),
     "fa_index_encode": (C.c_int, [vp, vp]),

@@ -393,7 +393,17 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
                                   cudaMemcpyHostToDevice, st));
-    for (const Batch &b : batches) {
+    // optional per-kernel-class timing: 5 events per batch on the build stream
+    const bool prof = opts->profile != 0;
+    std::vector<cudaEvent_t> ev;
+    if (prof) {
+        ev.resize(batches.size() * 5);
+        for (auto &e : ev) FA_BUILD_CUDA(cudaEventCreate(&e));
+    }
+    int64_t launches = 2;  // the two row resets of reset_graph
+    for (size_t bi = 0; bi < batches.size(); ++bi) {
+        const Batch &b = batches[bi];
+        if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 0], st));
         rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size, ix->d.dproj,
                                ix->d.cent, ix->d.dims, ix->d.offs, g.m, ix->d.dmax,
                                ix->d.dist_min, ix->d.delta, nullptr, g.mpad, adt_batch, g.mpad, st);
@@ -401,25 +411,45 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             cleanup();
             return rc;
         }
+        if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
         int grid = (b.size + kSearchWarps - 1) / kSearchWarps;
         build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
             g, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
             req, ctr, err);
         FA_BUILD_CUDA(cudaGetLastError());
+        if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         size_t tb = cub_bytes;
         FA_BUILD_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, req, req_sorted, (int)b.nreq, 0,
                                                      end_bit, st));
+        if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 3], st));
         int64_t chunks = (b.nreq + 31) / 32;
         int rgrid = (int)((chunks + kReverseWarps - 1) / kReverseWarps);
         reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
             g, ix->d.sdt, req_sorted, b.nreq, ix->upper_owner, RL, ctr);
         FA_BUILD_CUDA(cudaGetLastError());
+        if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
+        launches += 3;
     }
     unsigned long long hc[8];
     int herr = 0;
     FA_BUILD_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     FA_BUILD_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
     FA_BUILD_CUDA(cudaStreamSynchronize(st));
+    if (prof) {
+        double acc[4] = {0, 0, 0, 0};
+        for (size_t bi = 0; bi < batches.size(); ++bi)
+            for (int k = 0; k < 4; ++k) {
+                float ms = 0.f;
+                FA_BUILD_CUDA(cudaEventElapsedTime(&ms, ev[bi * 5 + k], ev[bi * 5 + k + 1]));
+                acc[k] += ms;
+            }
+        for (auto &e : ev) cudaEventDestroy(e);
+        res->ms_encode = acc[0];
+        res->ms_search = acc[1];
+        res->ms_sort = acc[2];
+        res->ms_reverse = acc[3];
+    }
+    res->launches = launches;
 #undef FA_BUILD_CUDA
     cleanup();
     if (herr) {

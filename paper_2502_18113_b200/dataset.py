@@ -1,0 +1,153 @@
+"""Datasets, the BASELINE synthetic workloads, and exact k-NN ground truth.
+
+VectorDataset / GroundTruth mirror flashann/dataset.py:19-51.  brute_force_knn
+(:126-161: float64 ||q||^2 + ||b||^2 - 2 q.b, clamped, ties by ascending id)
+runs on the GPU.  `baseline_config` draws the five BASELINE.json workloads
+from seeded generators (no public dataset is named; distributions the
+BASELINE text leaves open are the builder's choices documented in DESIGN.md).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigError
+
+
+@dataclass
+class VectorDataset:
+    data: np.ndarray  # (n, dim) float32
+
+    def __post_init__(self):
+        if not hasattr(self.data, "device"):
+            self.data = np.ascontiguousarray(self.data, dtype=np.float32)
+        if self.data.ndim != 2:
+            raise ConfigError("dataset must be a 2-D array")
+
+    @property
+    def n(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.data.shape[1]
+
+    def __len__(self) -> int:
+        return self.n
+
+
+@dataclass
+class GroundTruth:
+    k: int
+    ids: np.ndarray  # (nq, k) int32
+    dists: np.ndarray  # (nq, k) float64
+
+
+def brute_force_knn(base, queries, k: int, block: int = 256) -> GroundTruth:
+    """Exact top-k by squared L2 on the GPU (float64), ties by ascending id."""
+    import torch
+
+    b = getattr(base, "data", base)
+    q = getattr(queries, "data", queries)
+    if b.shape[1] != q.shape[1]:
+        raise ConfigError(f"dimension mismatch: base {b.shape[1]} vs queries {q.shape[1]}")
+    n = b.shape[0]
+    if k > n:
+        raise ConfigError(f"k={k} exceeds dataset size {n}")
+    bd = torch.as_tensor(np.asarray(b) if not hasattr(b, "device") else b, device="cuda").double()
+    bsq = (bd * bd).sum(1)
+    nq = q.shape[0]
+    ids = np.empty((nq, k), np.int32)
+    dists = np.empty((nq, k), np.float64)
+    qd_all = torch.as_tensor(np.asarray(q) if not hasattr(q, "device") else q, device="cuda")
+    win = min(n, k + 32)
+    ar = torch.arange(n, device="cuda")
+    for lo in range(0, nq, block):
+        qd = qd_all[lo: lo + block].double()
+        d2 = (qd * qd).sum(1)[:, None] + bsq[None, :] - 2.0 * (qd @ bd.T)
+        d2.clamp_(min=0.0)
+        vals, idx = torch.topk(d2, win, dim=1, largest=False, sorted=True)
+        # (d, id) order inside the window: stable sort by id, then by distance
+        o = torch.argsort(idx, dim=1, stable=True)
+        vals, idx = vals.gather(1, o), idx.gather(1, o)
+        o = torch.argsort(vals, dim=1, stable=True)
+        vals, idx = vals.gather(1, o), idx.gather(1, o)
+        # ties that spill past the window: redo those rows with a full sort
+        spill = (vals[:, k - 1] == vals[:, -1]) & (win < n)
+        for r in torch.nonzero(spill).flatten().tolist():
+            row = d2[r]
+            o1 = torch.argsort(ar, stable=True)
+            o2 = torch.argsort(row[o1], stable=True)
+            idx[r, :] = o1[o2][:win]
+            vals[r, :] = row[idx[r]]
+        ids[lo: lo + qd.shape[0]] = idx[:, :k].cpu().numpy()
+        dists[lo: lo + qd.shape[0]] = vals[:, :k].cpu().numpy()
+    return GroundTruth(k=k, ids=ids, dists=dists)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json workloads (seeded synthetic stand-ins)
+
+CONFIGS = {
+    1: dict(n=20_000, nq=200, dim=128, M=16, efC=100, m_f=32, d_f=128, ef=64),
+    2: dict(n=1_000_000, nq=10_000, dim=128, M=32, efC=200, m_f=64, d_f=128, ef=64),
+    3: dict(n=10_000_000, nq=10_000, dim=96, M=32, efC=200, m_f=48, d_f=96, ef=64),
+    4: dict(n=1_000_000, nq=5_000, dim=960, M=32, efC=300, m_f=64, d_f=256, ef=64),
+    5: dict(n=5_000_000, nq=10_000, dim=768, M=48, efC=256, m_f=96, d_f=768, ef=64),
+}
+
+
+def baseline_config(cfg: int, n: int | None = None, nq: int | None = None, seed: int = 0):
+    """(base (n, dim) f32, queries (nq, dim) f32) for BASELINE config `cfg`.
+
+    Queries are fresh draws from the same distribution (same mixture
+    centres).  `n` may select a prefix-sized sample of the same law."""
+    c = CONFIGS[cfg]
+    n = c["n"] if n is None else n
+    nq = c["nq"] if nq is None else nq
+    rng = np.random.default_rng(seed)
+    tot = n + nq
+    if cfg == 1:
+        # 64-component isotropic mixture, centres ~ N(0,1), sigma 0.3
+        centres = rng.normal(0.0, 1.0, (64, c["dim"]))
+        a = rng.integers(0, 64, tot)
+        x = centres[a] + rng.normal(0.0, 0.3, (tot, c["dim"]))
+    elif cfg == 2:
+        # 256-component mixture, centres ~ U(0,255), sigma 20, rounded, clipped
+        centres = rng.uniform(0.0, 255.0, (256, c["dim"]))
+        a = rng.integers(0, 256, tot)
+        x = np.clip(np.rint(centres[a] + rng.normal(0.0, 20.0, (tot, c["dim"]))), 0, 255)
+    elif cfg == 3:
+        centres = rng.normal(0.0, 1.0, (1024, c["dim"]))
+        a = rng.integers(0, 1024, tot)
+        x = centres[a] + rng.normal(0.0, 0.3, (tot, c["dim"]))
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+    elif cfg == 4:
+        # 512 components, covariance spectrum i^-1.2 in one random rotation
+        d = c["dim"]
+        q, _ = np.linalg.qr(rng.normal(size=(d, d)))
+        scale = np.arange(1, d + 1, dtype=np.float64) ** -0.6
+        centres = rng.normal(0.0, 1.0, (512, d))
+        a = rng.integers(0, 512, tot)
+        x = centres[a] + (rng.normal(size=(tot, d)) * scale) @ q.T
+    elif cfg == 5:
+        # rank-64 signal + isotropic noise at SNR 3 (power ratio), unit norm, bf16
+        d = c["dim"]
+        basis = rng.normal(size=(64, d)) / np.sqrt(d)
+        sig = rng.normal(size=(tot, 64)) @ basis
+        noise = rng.normal(size=(tot, d)) * np.sqrt((sig ** 2).mean() / 3.0)
+        x = sig + noise
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        x = _round_bf16(x.astype(np.float32))
+    else:
+        raise ConfigError(f"unknown config {cfg}")
+    x = x.astype(np.float32)
+    return x[:n], x[n:]
+
+
+def _round_bf16(x: np.ndarray) -> np.ndarray:
+    u = x.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32)

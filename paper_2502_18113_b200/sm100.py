@@ -42,6 +42,7 @@ BUILD_OPTIONS = {
     "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.02")),
     "seq_prefix": int(os.environ.get("FLASHANN_B200_SEQ_PREFIX", "256")),
     "hash_log2": int(os.environ.get("FLASHANN_B200_HASH_LOG2", "0")),
+    "profile": 0,
 }
 
 
@@ -76,7 +77,8 @@ def _require_flash(kind: int) -> None:
 def build_options(C_: int) -> _lib.BuildOpts:
     o = BUILD_OPTIONS
     return _lib.BuildOpts(C=C_, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
-                          seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"])
+                          seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
+                          profile=o.get("profile", 0))
 
 
 def _prov_arrays(prov: dict):

@@ -1,0 +1,108 @@
+"""GPU coder training (K3 + PCA) against the reference's golden models.
+
+Given the same projected sample, codebooks must match within 1e-4 relative
+(north-star tolerance; the device replays numpy's PCG64 draws, so they are
+normally bit-identical) and the SDT/range must match exactly.  The GPU PCA
+basis is compared up to per-component sign where eigen-gaps are resolvable.
+"""
+
+import numpy as np
+import pytest
+
+import golden_inputs as gi
+from oracle import train_np
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def flash(cuda):
+    from paper_2502_18113_b200 import flash
+
+    return flash
+
+
+@pytest.mark.parametrize("name", list(gi.MODELS))
+def test_codebooks_given_reference_projection(flash, golden, name):
+    spec = gi.MODELS[name]
+    p = f"model_{name}_"
+    data = gi.model_data(spec)
+    red = train_np.project(golden[p + "mean"], golden[p + "basis"], spec["d_f"], data)
+    dims, offs = golden[p + "dims"], golden[p + "offs"]
+    cent, sdt, dmin, dmax, hist = flash.train_codebooks(red, dims, offs, spec["seed"],
+                                                        spec["iters"])
+    ref = golden[p + "cent"]
+    scale = np.abs(ref).max()
+    assert np.abs(cent - ref).max() <= TOL * scale
+    assert np.array_equal(sdt, golden[p + "sdt"])
+    assert np.allclose([dmin, dmax], golden[p + "range"], rtol=1e-12, atol=0)
+    assert (np.diff(hist, axis=1) <= 1e-9 * hist[:, :1]).all()  # inertia non-increasing
+
+
+def test_codebooks_bit_exact_on_reference_projection(flash, golden):
+    """The PCG64 replay + numpy summation order give the reference's bytes."""
+    exact = 0
+    for name, spec in gi.MODELS.items():
+        p = f"model_{name}_"
+        red = train_np.project(golden[p + "mean"], golden[p + "basis"], spec["d_f"],
+                               gi.model_data(spec))
+        cent, *_ = flash.train_codebooks(red, golden[p + "dims"], golden[p + "offs"],
+                                         spec["seed"], spec["iters"])
+        exact += np.array_equal(cent, golden[p + "cent"])
+    assert exact >= len(gi.MODELS) - 1, exact
+
+
+def test_subsampled_kmeans_matches_restatement(flash):
+    """> 4096 training rows exercise the host-drawn permutation + device draws."""
+    rng = np.random.default_rng(9)
+    red = (rng.normal(size=(20_000, 8)) * 3 + rng.integers(0, 5, (20_000, 1))).astype(np.float32)
+    dims, offs = np.array([4, 4], np.int32), np.array([0, 4], np.int32)
+    cent, *_ = flash.train_codebooks(red, dims, offs, seed=5, kmeans_iters=7)
+    for i in range(2):
+        c, _ = train_np.kmeans(red[:, offs[i]: offs[i] + 4], 7, 5 + i)
+        assert np.abs(cent[i, :, :4] - c).max() <= TOL * np.abs(c).max()
+
+
+@pytest.mark.parametrize("name", ["t3", "c1s", "d8"])
+def test_gpu_pca_basis_up_to_sign(golden, name, cuda):
+    from paper_2502_18113_b200 import pca
+
+    spec = gi.MODELS[name]
+    data = gi.model_data(spec)
+    model = pca.pca_train(data, d=spec["d_f"])
+    ref_b = golden[f"model_{name}_basis"]
+    ref = train_np.pca(data, spec["d_f"])
+    eig = ref[2]
+    assert np.allclose(model.eigvals, eig, rtol=1e-6, atol=1e-9 * eig[0])
+    for j in range(spec["d_f"]):
+        gap = min(abs(eig[j] - eig[j - 1]) if j else np.inf,
+                  abs(eig[j] - eig[j + 1]) if j + 1 < len(eig) else np.inf)
+        if gap < 1e-3 * eig[0]:
+            continue  # eigenvector not resolvable at fp32 covariance precision
+        s = np.sign(model.basis[:, j] @ ref_b[:, j])
+        assert np.abs(s * model.basis[:, j] - ref_b[:, j]).max() < 1e-4
+
+
+def test_flash_train_end_to_end_codes(golden, cuda):
+    """Full GPU flash_train: codes of the training data agree with the
+    reference model's codes (PCA sign/rotation invariant check)."""
+    from oracle import native
+    from paper_2502_18113_b200 import flash
+
+    spec = gi.MODELS["c1s"]
+    data = gi.model_data(spec)
+    model = flash.flash_train(data, spec["d_f"], spec["m_f"], spec["seed"], spec["iters"])
+    assert model.dist_min == 0.0
+    assert model.sdt.shape == (spec["m_f"], 16, 16)
+    assert np.array_equal(model.sdt, model.sdt.transpose(0, 2, 1))
+    # the symmetric table stays well inside the 8-bit range (test_flash.py:72-76)
+    assert model.sdt.max() < 255
+    prov = flash.FlashProvider(model)
+    prov.attach(data)
+    codes = prov.core_arrays()["codes"]
+    red = prov.core_arrays()["proj"]
+    c2, _ = native.encode_adt(red[:200], model.cent, model.dims, model.offs, model.dist_min,
+                              model.delta)
+    assert np.array_equal(codes[:200], c2)
