@@ -18,6 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib, graph, layout
+from ._arrays import rows_of
 from ._lib import check
 from .errors import ConfigError
 from .flash import FlashProvider, flash_train
@@ -52,7 +53,7 @@ class BuildResult:
 
 def training_sample(dataset, sample_size: int, seed: int):
     """<= sample_size rows drawn without replacement, sorted (builder.py:60-65)."""
-    data = getattr(dataset, "data", dataset)
+    data = rows_of(dataset)
     n = data.shape[0]
     if n <= sample_size:
         return data
@@ -106,7 +107,7 @@ def build(dataset, strategy: str, params: graph.BuildParams, sp: StrategyParams 
           sample_size: int = DEFAULT_SAMPLE, kernel: str | None = None,
           core_impl=None) -> BuildResult:
     """Train, encode, and insert the whole dataset."""
-    data = getattr(dataset, "data", dataset)
+    data = rows_of(dataset)
     n = data.shape[0]
     if n < 1:
         raise ConfigError("cannot build an index over an empty dataset")

@@ -13,6 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._arrays import is_tensor, rows_of
 from .errors import ConfigError
 
 
@@ -21,7 +22,7 @@ class VectorDataset:
     data: np.ndarray  # (n, dim) float32
 
     def __post_init__(self):
-        if not hasattr(self.data, "device"):
+        if not is_tensor(self.data):
             self.data = np.ascontiguousarray(self.data, dtype=np.float32)
         if self.data.ndim != 2:
             raise ConfigError("dataset must be a 2-D array")
@@ -49,19 +50,19 @@ def brute_force_knn(base, queries, k: int, block: int = 256) -> GroundTruth:
     """Exact top-k by squared L2 on the GPU (float64), ties by ascending id."""
     import torch
 
-    b = getattr(base, "data", base)
-    q = getattr(queries, "data", queries)
+    b = rows_of(base)
+    q = rows_of(queries)
     if b.shape[1] != q.shape[1]:
         raise ConfigError(f"dimension mismatch: base {b.shape[1]} vs queries {q.shape[1]}")
     n = b.shape[0]
     if k > n:
         raise ConfigError(f"k={k} exceeds dataset size {n}")
-    bd = torch.as_tensor(np.asarray(b) if not hasattr(b, "device") else b, device="cuda").double()
+    bd = torch.as_tensor(b if is_tensor(b) else np.asarray(b), device="cuda").double()
     bsq = (bd * bd).sum(1)
     nq = q.shape[0]
     ids = np.empty((nq, k), np.int32)
     dists = np.empty((nq, k), np.float64)
-    qd_all = torch.as_tensor(np.asarray(q) if not hasattr(q, "device") else q, device="cuda")
+    qd_all = torch.as_tensor(q if is_tensor(q) else np.asarray(q), device="cuda")
     win = min(n, k + 32)
     ar = torch.arange(n, device="cuda")
     for lo in range(0, nq, block):

@@ -18,6 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._arrays import rows_of
 from ._lib import check
 from .errors import ConfigError
 from .pca import PCAModel, as_device_f32, pca_project, pca_project_all_dev, pca_train
@@ -148,7 +149,7 @@ def train_codebooks(reduced, dims, offs, seed: int = 0, kmeans_iters: int = 25):
 def flash_train(sample, d_f: int, m_f: int, seed: int = 0, kmeans_iters: int = 25) -> FlashModel:
     """Fit rotation, codebooks, quantization range and the symmetric table
     (flash.py:63-107) on the GPU."""
-    data = getattr(sample, "data", sample)
+    data = rows_of(sample)
     n, dim = data.shape
     if n < 10 * K:
         raise ConfigError(f"need at least {10 * K} training vectors, got {n}")
@@ -234,7 +235,7 @@ class FlashProvider:
 
     def attach(self, dataset, vecs_dev=None) -> None:
         """Project + encode every row on the device."""
-        data = getattr(dataset, "data", dataset)
+        data = rows_of(dataset)
         if data.shape[1] != self.model.pca.mean.shape[0]:
             raise ConfigError("dataset dimension does not match the trained model")
         self.dataset = dataset
@@ -268,7 +269,7 @@ class FlashProvider:
         if not self.dev:
             raise ConfigError("provider not attached to a dataset")
         if self._prov is None:
-            data = getattr(self.dataset, "data", None)
+            data = rows_of(self.dataset)
             self._prov = {
                 "vecs": data if isinstance(data, np.ndarray) else self.dev["vecs"].cpu().numpy(),
                 "dim": int(self.dev["vecs"].shape[1]),

@@ -16,6 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._arrays import is_tensor, rows_of
 from .errors import ConfigError
 
 
@@ -40,7 +41,7 @@ def _torch():
 
 def as_device_f32(data):
     torch = _torch()
-    if hasattr(data, "device"):
+    if is_tensor(data):
         return data.to(device="cuda", dtype=torch.float32).contiguous()
     return torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).cuda()
 
@@ -48,7 +49,7 @@ def as_device_f32(data):
 def pca_train(sample, alpha: float | None = 0.9, d: int | None = None) -> PCAModel:
     """Fit the rotation on the device; keep d components (or the smallest d
     reaching the variance fraction alpha)."""
-    data = getattr(sample, "data", sample)
+    data = rows_of(sample)
     n = data.shape[0]
     if n < 2:
         raise ConfigError("need at least 2 vectors to fit a covariance")
