@@ -75,7 +75,8 @@ def test_gpu_pca_basis_up_to_sign(golden, name, cuda):
     ref_b = golden[f"model_{name}_basis"]
     ref = train_np.pca(data, spec["d_f"])
     eig = ref[2]
-    assert np.allclose(model.eigvals, eig, rtol=1e-6, atol=1e-9 * eig[0])
+    # fp32 covariance GEMM (as in the reference): absolute error ~1e-7 x top eigenvalue
+    assert np.allclose(model.eigvals, eig, rtol=1e-6, atol=1e-6 * eig[0])
     for j in range(spec["d_f"]):
         gap = min(abs(eig[j] - eig[j - 1]) if j else np.inf,
                   abs(eig[j] - eig[j + 1]) if j + 1 < len(eig) else np.inf)
