@@ -42,7 +42,7 @@ __device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
 
 // ---- per-warp workspace ----------------------------------------------------
 struct WarpLayout {
-    int adt, T, X, S, fresh, fdist, hash, total;
+    int adt, T, S, fresh, fdist, hash, total;
     int hash_log2;
     __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
     __host__ __device__ void init(int mpad, int W, int capmax, int hlog2) {
@@ -50,7 +50,6 @@ struct WarpLayout {
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
         T = o; o += round_up(W, 32) * 8;
-        X = o; o += round_up(W, 32) * 8;
         S = o; o += 32 * 8;
         fresh = o; o += round_up(capmax, 32) * 4;
         fdist = o; o += round_up(capmax, 32) * 4;
@@ -156,23 +155,6 @@ __device__ __forceinline__ unsigned long long make_key(uint32_t d, int id) {
 __device__ __forceinline__ int key_id(unsigned long long k) { return (int)((k >> 1) & 0x7fffffffu); }
 __device__ __forceinline__ uint32_t key_d(unsigned long long k) { return (uint32_t)(k >> 32); }
 
-// Bitonic sort of 32 keys, one per lane, ascending by lane.
-__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x, int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
-            bool up = ((lane & k) == 0);
-            bool lower = ((lane & j) == 0);
-            bool take_min = (lower == up);
-            unsigned long long mn = x < y ? x : y, mx = x < y ? y : x;
-            x = take_min ? mn : mx;
-        }
-    }
-    return x;
-}
-
 // number of entries of sorted a[0..n) strictly less than x
 __device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, unsigned long long x) {
     int lo = 0, hi = n;
@@ -184,27 +166,47 @@ __device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, un
     return lo;
 }
 
-// Merge `ns` sorted keys (lane l holds s for l < ns, KEY_MAX beyond) into the
-// sorted buffer T[0..ts), keeping the W smallest.  Returns the lowest position
-// that changed (W if nothing entered).  X, S are scratch.
-__device__ __forceinline__ int merge_into(unsigned long long *T, int &ts, int W,
-                                          unsigned long long *X, unsigned long long *S,
-                                          unsigned long long s, int ns, int lane) {
+// number of entries of the unsorted (small) a[0..n) strictly less than x;
+// every lane reads the same word: shared-memory broadcast
+__device__ __forceinline__ int count_less(const unsigned long long *a, int n, unsigned long long x) {
+    int c = 0;
+    for (int j = 0; j < n; ++j) c += a[j] < x;
+    return c;
+}
+
+// Merge the candidates held by the lanes with keep == true (unsorted, distinct
+// keys) into the sorted buffer T[0..ts), keeping the W smallest — without
+// sorting them first: a candidate's final position is its rank in T plus its
+// rank among the candidates; T's tail moves right in place, highest 32-entry
+// chunk first, so no element is overwritten before it is read.
+// Returns the lowest position that changed (W if nothing entered).
+__device__ __forceinline__ int merge_unsorted(unsigned long long *T, int &ts, int W,
+                                              unsigned long long *S, unsigned long long s,
+                                              bool keep, int lane) {
+    const unsigned bk = __ballot_sync(0xffffffffu, keep);
+    const int ns = __popc(bk);
     if (ns == 0) return W;
-    if (lane < ns) S[lane] = s;
+    if (keep) S[__popc(bk & ((1u << lane) - 1u))] = s;
     __syncwarp();
-    int p = lane < ns ? lane + lower_rank(T, ts, s) : W;
-    const int p0 = __shfl_sync(0xffffffffu, p, 0);
+    const int p = keep ? lower_rank(T, ts, s) + count_less(S, ns, s) : W;
+    const int p0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)p);
     const int newts = min(W, ts + ns);
     if (p0 >= newts) return W;
-    for (int i = p0 + lane; i < ts; i += 32) {
-        unsigned long long t = T[i];
-        int np = i + lower_rank(S, ns, t);
-        if (np < newts) X[np - p0] = t;
+    if (ts > p0) {
+        for (int base = p0 + ((ts - 1 - p0) & ~31); base >= p0; base -= 32) {
+            const int i = base + lane;
+            unsigned long long t = 0;
+            int np = W;
+            if (i < ts) {
+                t = T[i];
+                np = i + count_less(S, ns, t);
+            }
+            __syncwarp();
+            if (np < newts) T[np] = t;
+            __syncwarp();
+        }
     }
-    if (lane < ns && p < newts) X[p - p0] = s;
-    __syncwarp();
-    for (int i = p0 + lane; i < newts; i += 32) T[i] = X[i - p0];
+    if (keep && p < newts) T[p] = s;
     __syncwarp();
     ts = newts;
     return p0;
@@ -217,11 +219,33 @@ struct SearchCounters {
 // Warp-cooperative best-first search on one layer.
 // On return T[0..ts) holds the result ascending by (d, id).
 // Returns false on visited-hash overflow.
+constexpr int kRowChunks = 4;  // id rows up to 128 slots (cap = 2R <= 127)
+
+// First unexpanded member of T at or after `from` (-1 if none).
+__device__ __forceinline__ int next_unexpanded(const unsigned long long *T, int ts, int from,
+                                               int lane) {
+    for (int c = from; c < ts; c += 32) {
+        int idx = c + lane;
+        bool f = idx < ts && ((T[idx] & 1ull) == 0ull);
+        unsigned b = __ballot_sync(0xffffffffu, f);
+        if (b) return c + __ffs(b) - 1;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane,
+                                         int (&u)[kRowChunks]) {
+#pragma unroll
+    for (int k = 0; k < kRowChunks; ++k) {
+        int j = k * 32 + lane;
+        u[k] = j < cap ? __ldg(ids + j) : -1;
+    }
+}
+
 __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
-                             const uint8_t *adt_s, unsigned long long *T, int &ts,
-                             unsigned long long *X, unsigned long long *S, int32_t *fresh,
-                             uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
-                             int lane) {
+                                    const uint8_t *adt_s, unsigned long long *T, int &ts,
+                                    unsigned long long *S, int32_t *fresh, uint32_t *fdist,
+                                    uint32_t *H, int hlog2, SearchCounters &cnt, int lane) {
     const int cap = layer_cap(g, layer);
     const int hlimit = (1 << hlog2) - (1 << hlog2) / 8;
     hash_clear(H, hlog2, lane);
@@ -233,38 +257,40 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     int nvis = 1;
     ts = 1;
     int cur = 0;
+    // speculative id row of the most likely next expansion (the next
+    // unexpanded member before this step's merge)
+    int pre_v = -1;
+    int pre[kRowChunks];
     __syncwarp();
     while (true) {
-        // next unexpanded member (all of T[0..cur) are expanded)
-        int found = -1;
-        while (cur < ts) {
-            int idx = cur + lane;
-            bool f = idx < ts && ((T[idx] & 1ull) == 0ull);
-            unsigned b = __ballot_sync(0xffffffffu, f);
-            if (b) {
-                found = cur + __ffs(b) - 1;
-                break;
-            }
-            cur += 32;
-        }
-        if (found < 0) break;
-        cur = found;
+        cur = next_unexpanded(T, ts, cur, lane);
+        if (cur < 0) break;
         const int v = key_id(T[cur]);
+        int u[kRowChunks];
+        if (v == pre_v) {
+#pragma unroll
+            for (int k = 0; k < kRowChunks; ++k) u[k] = pre[k];
+        } else {
+            load_row(row_ids(g, layer, v), cap, lane, u);
+        }
+        const int nxt = next_unexpanded(T, ts, cur + 1, lane);
+        pre_v = nxt >= 0 ? key_id(T[nxt]) : -1;
+        if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         __syncwarp();
         if (lane == 0) T[cur] |= 1ull;
         cnt.visited++;
-        const int32_t *ids = row_ids(g, layer, v);
         if (nvis + cap > hlimit) return false;
         // visited filter over the row, compacted in slot order
         int nf = 0, nlive = 0;
-        for (int base = 0; base < cap; base += 32) {
-            int j = base + lane;
-            int u = j < cap ? __ldg(ids + j) : -1;
-            bool live = u >= 0;
-            bool fr = live && hash_insert(H, hlog2, u);
+#pragma unroll
+        for (int k = 0; k < kRowChunks; ++k) {
+            if (k * 32 >= cap) break;
+            const int x = u[k];
+            bool live = x >= 0;
+            bool fr = live && hash_insert(H, hlog2, x);
             unsigned bl = __ballot_sync(0xffffffffu, live);
             unsigned bf = __ballot_sync(0xffffffffu, fr);
-            if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = u;
+            if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
             nf += __popc(bf);
             nlive += __popc(bl);
         }
@@ -279,13 +305,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             const int f = base + lane;
             unsigned long long k = f < nf ? make_key(fdist[f], fresh[f]) : KEY_MAX;
             const unsigned long long worst = ts < W ? KEY_MAX : T[W - 1];
-            bool keep = k < worst;
-            unsigned bk = __ballot_sync(0xffffffffu, keep);
-            int ns = __popc(bk);
-            if (ns == 0) continue;
-            k = keep ? k : KEY_MAX;
-            k = warp_sort32(k, lane);
-            int p0 = merge_into(T, ts, W, X, S, k, ns, lane);
+            int p0 = merge_unsorted(T, ts, W, S, k, k < worst, lane);
             lowest = min(lowest, p0);
         }
         if (lowest < cur) cur = lowest;
