@@ -161,6 +161,7 @@ typedef struct {
     int32_t n_batches;
     int64_t dist_comps, sym_comps, kernel_calls, visited; /* _core.pyx:695-704 */
     int64_t reverse_prunes, reverse_appends;
+    int64_t reverse_full_prunes; /* prunes that could not take the fast path    */
     int64_t launches;     /* kernels of this library launched by the build      */
     double ms_encode, ms_search, ms_sort, ms_reverse; /* profile = 1 only       */
 } fa_build_result;

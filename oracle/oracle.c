@@ -15,8 +15,8 @@
  *   or_batch_lanes   _kernels/_simd.h:111-121 (scalar semantic definition)
  *   or_sdt_sum       _kernels/_simd.h:87-95
  *   or_select        _kernels/_core.pyx:388-408
- *   or_layer_search  _kernels/_core.pyx:278-342 with the (d, id) total order
- *                    of SURVEY §8(c) (T-only stop rule)
+ *   or_layer_search  _pycore.py:246-283, the reference's semantic core for
+ *                    _core.pyx:278-342 (ties by vertex id via tuple order)
  *   or_hill_climb    _kernels/_core.pyx:345-385
  *   or_reverse_add   _kernels/_core.pyx:441-477 (+ fa_sort_pairs :232-247)
  *   or_build         _kernels/_core.pyx:501-536 / :711-764 under the
@@ -160,29 +160,75 @@ static int32_t *cnt_of(or_graph *g, int layer, int v) {
     return g->cntU + (g->uoff[v] + layer - 1);
 }
 
-typedef struct {
-    uint64_t key; /* d << 32 | id */
-    int expanded;
-} tentry;
-
 static int cmp_u64(const void *a, const void *b) {
     uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
-    return (x > y) - (x < y);
-}
-static int cmp_tentry(const void *a, const void *b) {
-    uint64_t x = ((const tentry *)a)->key, y = ((const tentry *)b)->key;
     return (x > y) - (x < y);
 }
 
 typedef struct {
     uint32_t *visited; /* epoch per vertex */
     uint32_t epoch;
-    tentry *T;
-    int *fresh;
-    int cap_scratch;
+    uint64_t *fr;      /* frontier min-heap, key (d << 32 | u)                  */
+    uint64_t *rs;      /* result max-heap, key (d << 32 | ~u): top = max d, min u */
+    uint64_t *fresh;   /* (d << 32 | u) of one expansion                         */
+    size_t fr_cap;
 } scratch;
 
-/* (d, id)-ordered best-first search; returns |T|, fills out (keys asc). */
+static void heap_push_min(uint64_t *h, int *n, uint64_t k) {
+    int i = (*n)++;
+    h[i] = k;
+    while (i > 0) {
+        int p = (i - 1) >> 1;
+        if (h[p] <= h[i]) break;
+        uint64_t t = h[p]; h[p] = h[i]; h[i] = t;
+        i = p;
+    }
+}
+static uint64_t heap_pop_min(uint64_t *h, int *n) {
+    uint64_t top = h[0];
+    int m = --(*n), i = 0;
+    h[0] = h[m];
+    for (;;) {
+        int c = 2 * i + 1;
+        if (c >= m) break;
+        if (c + 1 < m && h[c + 1] < h[c]) ++c;
+        if (h[i] <= h[c]) break;
+        uint64_t t = h[i]; h[i] = h[c]; h[c] = t;
+        i = c;
+    }
+    return top;
+}
+static void heap_push_max(uint64_t *h, int *n, uint64_t k) {
+    int i = (*n)++;
+    h[i] = k;
+    while (i > 0) {
+        int p = (i - 1) >> 1;
+        if (h[p] >= h[i]) break;
+        uint64_t t = h[p]; h[p] = h[i]; h[i] = t;
+        i = p;
+    }
+}
+static void heap_pop_max(uint64_t *h, int *n) {
+    int m = --(*n), i = 0;
+    h[0] = h[m];
+    for (;;) {
+        int c = 2 * i + 1;
+        if (c >= m) break;
+        if (c + 1 < m && h[c + 1] > h[c]) ++c;
+        if (h[i] >= h[c]) break;
+        uint64_t t = h[i]; h[i] = h[c]; h[c] = t;
+        i = c;
+    }
+}
+static uint64_t rkey(uint64_t d, uint32_t u) { return (d << 32) | (uint32_t)~u; }
+
+/* Best-first layer search with the semantics of the reference's semantic
+ * core (flashann/_pycore.py:246-283): frontier popped in (d, id) order; stop
+ * once the result set is full and the popped distance exceeds its worst
+ * distance; a block's fresh neighbours are processed in ascending (d, id);
+ * accept while the set is not full or d < worst distance (strict), evicting
+ * the worst (largest d, smallest id on ties).  Returns |R|; out holds
+ * (d << 32 | id) ascending. */
 static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int layer, int entry,
                              int entry_d, int W, uint64_t *out, or_counters *c) {
     int cap = layer == 0 ? g->cap0 : g->capU;
@@ -193,43 +239,50 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
     }
     uint32_t ep = s->epoch;
     s->visited[entry] = ep;
-    int ts = 1;
-    s->T[0].key = ((uint64_t)entry_d << 32) | (uint32_t)entry;
-    s->T[0].expanded = 0;
-    for (;;) {
-        int cur = -1;
-        for (int i = 0; i < ts; ++i)
-            if (!s->T[i].expanded) {
-                cur = i;
-                break;
-            }
-        if (cur < 0) break;
-        s->T[cur].expanded = 1;
-        int v = (int)(uint32_t)(s->T[cur].key & 0xffffffffu);
+    int nf = 0, nr = 0;
+    heap_push_min(s->fr, &nf, ((uint64_t)entry_d << 32) | (uint32_t)entry);
+    heap_push_max(s->rs, &nr, rkey((uint64_t)entry_d, (uint32_t)entry));
+    while (nf > 0) {
+        uint64_t top = heap_pop_min(s->fr, &nf);
+        uint64_t d = top >> 32;
+        int v = (int)(uint32_t)top;
+        if (nr >= W && d > (s->rs[0] >> 32)) break;
         if (c) c->visited++;
         int32_t *ids = row_of(g, layer, v);
         int cnt = *cnt_of(g, layer, v);
         if (cnt > cap) cnt = cap;
         if (c) c->kernel_calls += (cnt + 15) >> 4;
-        int added = 0;
+        int nfresh = 0;
         for (int j = 0; j < cnt; ++j) {
             int u = ids[j];
             if (u < 0 || s->visited[u] == ep) continue;
             s->visited[u] = ep;
-            int du = adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
-            if (c) c->dist_comps++;
-            s->T[ts + added].key = ((uint64_t)du << 32) | (uint32_t)u;
-            s->T[ts + added].expanded = 0;
-            added++;
+            uint64_t du = (uint64_t)adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+            s->fresh[nfresh++] = (du << 32) | (uint32_t)u;
         }
-        if (added) {
-            ts += added;
-            qsort(s->T, (size_t)ts, sizeof(tentry), cmp_tentry);
-            if (ts > W) ts = W;
+        if (c) c->dist_comps += nfresh;
+        qsort(s->fresh, (size_t)nfresh, sizeof(uint64_t), cmp_u64);
+        for (int j = 0; j < nfresh; ++j) {
+            uint64_t du = s->fresh[j] >> 32;
+            uint32_t u = (uint32_t)s->fresh[j];
+            if (nr < W) {
+                heap_push_max(s->rs, &nr, rkey(du, u));
+            } else if (du < (s->rs[0] >> 32)) {
+                heap_pop_max(s->rs, &nr);
+                heap_push_max(s->rs, &nr, rkey(du, u));
+            } else {
+                break;  /* sorted: every later candidate is rejected too */
+            }
+            if ((size_t)nf >= s->fr_cap) return -1;
+            heap_push_min(s->fr, &nf, s->fresh[j]);
         }
     }
-    for (int i = 0; i < ts; ++i) out[i] = s->T[i].key;
-    return ts;
+    for (int i = 0; i < nr; ++i) {
+        uint64_t k = s->rs[i];
+        out[i] = (k & 0xffffffff00000000ull) | (uint32_t)~(uint32_t)k;
+    }
+    qsort(out, (size_t)nr, sizeof(uint64_t), cmp_u64);
+    return nr;
 }
 
 static void hill_climb_impl(or_graph *g, const uint8_t *adt, int layer, int *cur, int *curd,
@@ -263,14 +316,17 @@ static void hill_climb_impl(or_graph *g, const uint8_t *adt, int layer, int *cur
 
 static int scratch_init(scratch *s, int64_t n, int W, int capmax) {
     s->visited = (uint32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(uint32_t));
-    s->T = (tentry *)malloc(sizeof(tentry) * (size_t)(W + capmax + 8));
-    s->fresh = (int *)malloc(sizeof(int) * (size_t)(capmax + 8));
+    s->fr_cap = (size_t)(n > 0 ? n : 1) + 2;  /* each vertex is pushed at most once */
+    s->fr = (uint64_t *)malloc(sizeof(uint64_t) * s->fr_cap);
+    s->rs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 2));
+    s->fresh = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 8));
     s->epoch = 0;
-    return (s->visited && s->T && s->fresh) ? 0 : -1;
+    return (s->visited && s->fr && s->rs && s->fresh) ? 0 : -1;
 }
 static void scratch_free(scratch *s) {
     free(s->visited);
-    free(s->T);
+    free(s->fr);
+    free(s->rs);
     free(s->fresh);
 }
 

@@ -41,7 +41,7 @@ class BuildResult(C.Structure):
     _fields_ = [("entry_point", i64), ("max_layer", i32), ("n_batches", i32),
                 ("dist_comps", i64), ("sym_comps", i64), ("kernel_calls", i64),
                 ("visited", i64), ("reverse_prunes", i64), ("reverse_appends", i64),
-                ("launches", i64), ("ms_encode", f64), ("ms_search", f64), ("ms_sort", f64),
+                ("reverse_full_prunes", i64), ("launches", i64), ("ms_encode", f64), ("ms_search", f64), ("ms_sort", f64),
                 ("ms_reverse", f64)]
 
     def counters(self) -> dict:

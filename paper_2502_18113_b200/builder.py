@@ -97,6 +97,7 @@ def build_device(g: graph.GraphIndex, provider: FlashProvider, params: graph.Bui
     g.max_layer = int(res.max_layer)
     g.counters = dict(res.counters(), reverse_prunes=int(res.reverse_prunes),
                       reverse_appends=int(res.reverse_appends), n_batches=int(res.n_batches),
+                      reverse_full_prunes=int(res.reverse_full_prunes),
                       launches=int(res.launches), ms_encode=res.ms_encode,
                       ms_search=res.ms_search, ms_sort=res.ms_sort, ms_reverse=res.ms_reverse)
     g.invalidate()

@@ -346,16 +346,22 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaFuncSetAttribute(reverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));
 
+    int rev_per_sm = 0;
+    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, reverse_kernel,
+                                                          kReverseWarps * 32, smem_rev));
+    const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * kNumSMs;
+
     uint8_t *adt_batch = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
-    int64_t *req_off_d = nullptr;
-    int *err = nullptr;
+    int64_t *req_off_d = nullptr, *heads = nullptr;
+    int *err = nullptr, *nheads = nullptr, *next_seg = nullptr;
     void *cub_tmp = nullptr;
     size_t cub_bytes = 0;
     int rc = FA_OK;
     auto cleanup = [&]() {
         cudaFree(adt_batch); cudaFree(req); cudaFree(req_sorted); cudaFree(ctr);
-        cudaFree(req_off_d); cudaFree(err); cudaFree(cub_tmp);
+        cudaFree(req_off_d); cudaFree(err); cudaFree(cub_tmp); cudaFree(heads);
+        cudaFree(nheads); cudaFree(next_seg);
     };
     int end_bit = 32;
     {
@@ -370,6 +376,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&ctr, sizeof(unsigned long long) * 8)) ||
         (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
+        (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
+        (rc = dev_alloc((void **)&nheads, sizeof(int))) ||
+        (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
         (rc = dev_alloc((void **)&err, sizeof(int)))) {
         cleanup();
         return rc;
@@ -422,13 +431,18 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         FA_BUILD_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, req, req_sorted, (int)b.nreq, 0,
                                                      end_bit, st));
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 3], st));
-        int64_t chunks = (b.nreq + 31) / 32;
-        int rgrid = (int)((chunks + kReverseWarps - 1) / kReverseWarps);
+        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, sizeof(int), st));
+        reverse_heads_kernel<<<(int)((b.nreq + 255) / 256), 256, 0, st>>>(req_sorted, b.nreq,
+                                                                         heads, nheads, next_seg);
+        FA_BUILD_CUDA(cudaGetLastError());
+        // persistent warps pull row segments; never more warps than requests
+        int rgrid = (int)std::min<int64_t>(rev_ctas, (b.nreq + 32 * kReverseWarps - 1) /
+                                                          (32 * kReverseWarps) + 1);
         reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
-            g, ix->d.sdt, req_sorted, b.nreq, ix->upper_owner, RL, ctr);
+            g, ix->d.sdt, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
-        launches += 3;
+        launches += 4;
     }
     unsigned long long hc[8];
     int herr = 0;
@@ -467,6 +481,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     res->visited = (int64_t)hc[3];
     res->reverse_prunes = (int64_t)hc[4];
     res->reverse_appends = (int64_t)hc[5];
+    res->reverse_full_prunes = (int64_t)hc[6];
     return FA_OK;
 }
 

@@ -40,10 +40,15 @@ struct ReverseLayout {
     }
 };
 
+__global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys, int64_t N,
+                                     int64_t *__restrict__ heads, int *__restrict__ nheads,
+                                     int *__restrict__ next);
+
 __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                const unsigned long long *__restrict__ keys, int64_t N,
-                               const int32_t *__restrict__ upper_owner, ReverseLayout L,
-                               unsigned long long *__restrict__ ctr);
+                               const int64_t *__restrict__ heads, const int *__restrict__ nheads,
+                               int *__restrict__ next, const int32_t *__restrict__ upper_owner,
+                               ReverseLayout L, unsigned long long *__restrict__ ctr);
 
 int launch_encode_adt(const float *red, int64_t n, int64_t red_stride, const float *cent,
                       const int32_t *dims, const int32_t *offs, int m, int dmax, double dmin,

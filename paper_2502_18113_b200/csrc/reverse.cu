@@ -2,15 +2,16 @@
 //
 // The batch's forward selections emit requests (row(y, layer) << 32 | x);
 // after a radix sort each row's incoming x arrive ascending, which is the
-// order the sequential reference applies them in.  One warp owns a row and
-// replays the reference's per-edge rule exactly:
+// order the sequential reference applies them in.  reverse_heads_kernel lists
+// the row segments; reverse_kernel's warps pull segments dynamically and
+// replay the reference's per-edge rule exactly:
 //   count < cap : append x (write_code_slot + id, count+1)
 //   count == cap: d(y,u) = sdt-sum for all cap+1 candidates, sort by (d, id)
 //                 (fa_sort_pairs), select_heur(cap), rewrite the row.
 // Fast path: a row whose content is exactly the previous prune's output (kept
-// order = ascending (d, id), pairwise non-dominated) stays kept except for
-// candidates x itself dominates, so the prune of L + {x} needs only the
-// sums against x — decision-identical to the full scan.
+// order = ascending (d, id), pairwise non-dominated) keeps every member that x
+// does not dominate, so the prune of L + {x} needs only the sums against x and
+// no sort — decision-identical to the full scan.
 #include "kernels.cuh"
 
 namespace fa {
@@ -33,29 +34,28 @@ __device__ __forceinline__ uint32_t sdt_sum_u_uniform(const uint8_t *sdtN, int m
     return acc > 255u ? 255u : acc;
 }
 
-// Bitonic sort of np (power of two <= 128) keys in shared memory, ascending.
-__device__ __forceinline__ void warp_bitonic_smem(unsigned long long *a, int np, int lane) {
-    for (int k = 2; k <= np; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = lane; i < np; i += 32) {
-                int l = i ^ j;
-                if (l > i) {
-                    unsigned long long x = a[i], y = a[l];
-                    bool up = (i & k) == 0;
-                    if ((x > y) == up) {
-                        a[i] = y;
-                        a[l] = x;
-                    }
-                }
-            }
-            __syncwarp();
-        }
+// Segment heads of the sorted request keys (first key of every row).
+__global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys, int64_t N,
+                                     int64_t *__restrict__ heads, int *__restrict__ nheads,
+                                     int *__restrict__ next) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i == 0) *next = 0;
+    bool h = false;
+    if (i < N) {
+        unsigned long long k = keys[i];
+        h = k != KEY_MAX && (i == 0 || (keys[i - 1] >> 32) != (k >> 32));
     }
+    const unsigned b = __ballot_sync(0xffffffffu, h);
+    int base = 0;
+    if ((threadIdx.x & 31) == 0 && b) base = atomicAdd(nheads, __popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (h) heads[base + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = i;
 }
 
 __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
     Graph g, const uint8_t *__restrict__ sdt, const unsigned long long *__restrict__ keys,
-    int64_t N, const int32_t *__restrict__ upper_owner, ReverseLayout L,
+    int64_t N, const int64_t *__restrict__ heads, const int *__restrict__ nheads,
+    int *__restrict__ next, const int32_t *__restrict__ upper_owner, ReverseLayout L,
     unsigned long long *__restrict__ ctr) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tb = round_up(g.m * 256, 128);
@@ -71,16 +71,14 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
     unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
     int32_t *kept = reinterpret_cast<int32_t *>(base + L.kept);
     uint8_t *kcodes = base + L.kcodes;
-    const int64_t chunk = (int64_t)blockIdx.x * kReverseWarps + wid;
-    const int64_t i = chunk * 32 + lane;
-    unsigned long long key = i < N ? keys[i] : KEY_MAX;
-    unsigned long long prev = (i > 0 && i < N) ? keys[i - 1] : KEY_MAX;
-    bool head = key != KEY_MAX && (i == 0 || (prev >> 32) != (key >> 32));
-    unsigned heads = __ballot_sync(0xffffffffu, head);
-    unsigned long long n_prune = 0, n_app = 0, n_sym = 0;
-    while (heads) {
-        const int64_t h = chunk * 32 + __ffs(heads) - 1;
-        heads &= heads - 1;
+    const int nseg = *nheads;
+    unsigned long long n_prune = 0, n_app = 0, n_sym = 0, n_full = 0;
+    while (true) {
+        int s = 0;
+        if (lane == 0) s = atomicAdd(next, 1);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= nseg) break;
+        const int64_t h = heads[s];
         const unsigned long long hk = keys[h];
         const int64_t rowg = (int64_t)(hk >> 32);
         int64_t e = -1;
@@ -115,65 +113,90 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 continue;
             }
             ++n_prune;
-            // candidates: row + x, keys (d(y,u) << 32 | u), sorted (fa_sort_pairs)
-            int np = 32;
-            while (np < cap + 1) np <<= 1;
-            for (int j = lane; j < np; j += 32) {
-                unsigned long long k = KEY_MAX;
-                if (j <= cap) {
-                    int u = j < cap ? row_s[j] : x;
-                    uint32_t d = sdt_sum_u_uniform(sdtN, g.m, cy, g.codes + (size_t)u * g.mpad);
-                    k = ((unsigned long long)d << 32) | (uint32_t)u;
-                }
-                cand[j] = k;
-            }
-            n_sym += cap + 1;
-            __syncwarp();
-            warp_bitonic_smem(cand, np, lane);
-            int nk;
             const uint8_t *cx = g.codes + (size_t)x * g.mpad;
+            const uint32_t dx = sdt_sum_u_uniform(sdtN, g.m, cy, cx);
+            const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
+            int nk = 0;
             if (cons) {
-                // position of x in the sorted candidates
-                int p = -1;
-                for (int j = lane; j <= cap; j += 32)
-                    if ((int)(cand[j] & 0xffffffffu) == x) p = j;
+                // L = row_s is sorted by (d, id) and pairwise non-dominated.
+                // p = position of x among the candidates; x survives iff no
+                // L_j (j < p) dominates it; L_j (j >= p) drops iff x survives
+                // and dominates it.
+                int p = 0;
+                unsigned long long kj[kRowChunks];
+                bool domx = false;
 #pragma unroll
-                for (int o = 16; o; o >>= 1) p = max(p, __shfl_xor_sync(0xffffffffu, p, o));
-                const uint32_t dx = (uint32_t)(cand[p] >> 32);
-                bool dom = false;  // some earlier (kept) candidate dominates x
-                for (int j = lane; j < p; j += 32) {
-                    const uint8_t *cu = g.codes + (size_t)(uint32_t)(cand[j] & 0xffffffffu) * g.mpad;
-                    dom |= sdt_sum_rows(sdtT, g.m, cu, cx) < dx;
-                }
-                const bool xkept = !__any_sync(0xffffffffu, dom);
-                n_sym += p;
-                // survivors in order; L_j (j > p) drops iff x kept and x dominates it
-                nk = 0;
-                for (int base2 = 0; base2 <= cap; base2 += 32) {
-                    int j = base2 + lane;
-                    bool keep = false;
-                    int u = -1;
-                    if (j <= cap) {
-                        u = (int)(cand[j] & 0xffffffffu);
-                        if (j < p) keep = true;
-                        else if (j == p) keep = xkept;
-                        else {
-                            keep = true;
-                            if (xkept) {
-                                uint32_t dj = (uint32_t)(cand[j] >> 32);
-                                keep = sdt_sum_u_uniform(sdtN, g.m, cx,
-                                                         g.codes + (size_t)u * g.mpad) >= dj;
-                            }
-                        }
+                for (int c = 0; c < kRowChunks; ++c) {
+                    const int j = c * 32 + lane;
+                    kj[c] = KEY_MAX;
+                    if (j < cap) {
+                        const int uj = row_s[j];
+                        const uint8_t *cu = g.codes + (size_t)uj * g.mpad;
+                        const uint32_t dj = sdt_sum_u_uniform(sdtN, g.m, cy, cu);
+                        kj[c] = ((unsigned long long)dj << 32) | (uint32_t)uj;
+                        if (kj[c] < kx) domx |= sdt_sum_rows(sdtT, g.m, cu, cx) < dx;
                     }
-                    unsigned bk = __ballot_sync(0xffffffffu, keep);
-                    int pos = nk + __popc(bk & ((1u << lane) - 1u));
-                    if (keep && pos < cap) kept[pos] = u;
+                    p += __popc(__ballot_sync(0xffffffffu, kj[c] < kx));
+                }
+                const bool xkept = !__any_sync(0xffffffffu, domx);
+                n_sym += cap + 1 + p;
+                if (xkept) n_sym += cap - p;
+                // survivors in candidate order: L_0..L_{p-1}, x, L_p..
+#pragma unroll
+                for (int c = 0; c < kRowChunks; ++c) {
+                    const int j = c * 32 + lane;
+                    bool keep = false;
+                    int uj = -1;
+                    if (j < cap) {
+                        uj = (int)(kj[c] & 0xffffffffu);
+                        keep = true;
+                        if (j >= p && xkept)
+                            keep = sdt_sum_u_uniform(sdtN, g.m, cx, g.codes + (size_t)uj * g.mpad) >=
+                                   (uint32_t)(kj[c] >> 32);
+                    }
+                    const unsigned bk = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        int pos = nk + __popc(bk & ((1u << lane) - 1u));
+                        if (j >= p && xkept) ++pos;  // x sits at position p
+                        if (pos < cap) kept[pos] = uj;
+                    }
                     nk += __popc(bk);
                 }
-                if (xkept) n_sym += cap - p;
+                if (xkept) {
+                    if (lane == 0 && p < cap) kept[p] = x;
+                    ++nk;
+                }
                 nk = min(nk, cap);
             } else {
+                ++n_full;
+                // candidates row + x with (d, id) keys, sorted by rank
+                for (int j = lane; j <= cap; j += 32) {
+                    if (j < cap) {
+                        const int uj = row_s[j];
+                        const uint32_t dj =
+                            sdt_sum_u_uniform(sdtN, g.m, cy, g.codes + (size_t)uj * g.mpad);
+                        cand[j] = ((unsigned long long)dj << 32) | (uint32_t)uj;
+                    } else {
+                        cand[j] = kx;
+                    }
+                }
+                __syncwarp();
+                unsigned long long mine[kRowChunks + 1];
+                int rk[kRowChunks + 1];
+#pragma unroll
+                for (int c = 0; c <= kRowChunks; ++c) {
+                    const int j = c * 32 + lane;
+                    rk[c] = -1;
+                    if (j <= cap) {
+                        mine[c] = cand[j];
+                        rk[c] = count_less(cand, cap + 1, mine[c]);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c <= kRowChunks; ++c)
+                    if (rk[c] >= 0) cand[rk[c]] = mine[c];
+                __syncwarp();
                 unsigned long long sym = 0;
                 nk = warp_select_heur(
                     sdtT, g.m, g.mpad, g.codes, g.mpad, cap + 1, cap,
@@ -183,7 +206,7 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                         dv = (double)(uint32_t)(k >> 32);
                     },
                     kept, kcodes, lane, &sym);
-                n_sym += sym;
+                n_sym += cap + 1 + sym;
             }
             __syncwarp();
             for (int j = lane; j < cap; j += 32) row_s[j] = j < nk ? kept[j] : -1;
@@ -202,6 +225,7 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
         atomicAdd(ctr + 1, n_sym);
         atomicAdd(ctr + 4, n_prune);
         atomicAdd(ctr + 5, n_app);
+        atomicAdd(ctr + 6, n_full);
     }
 }
 

@@ -12,6 +12,7 @@ __device__ __forceinline__ int64_t row_global(const Graph &g, int layer, int y) 
 struct WarpWS {
     uint8_t *adt;
     unsigned long long *T, *S;
+    int32_t *TQ;
     int32_t *fresh;
     uint32_t *fdist;
     uint32_t *H;
@@ -19,6 +20,7 @@ struct WarpWS {
         adt = base + L.adt;
         T = reinterpret_cast<unsigned long long *>(base + L.T);
         S = reinterpret_cast<unsigned long long *>(base + L.S);
+        TQ = reinterpret_cast<int32_t *>(base + L.TQ);
         fresh = reinterpret_cast<int32_t *>(base + L.fresh);
         fdist = reinterpret_cast<uint32_t *>(base + L.fdist);
         H = reinterpret_cast<uint32_t *>(base + L.hash);
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
     for (int layer = top; layer >= 0; --layer) {
         int ts = 0;
-        bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.fresh,
+        bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                                ws.fdist, ws.H, L.hash_log2, cnt, lane);
         if (!ok) {
             if (lane == 0) atomicExch(err, 1);
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     for (int layer = ml; layer > 0; --layer)
         hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
     int ts = 0;
-    bool ok = layer_search(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.fresh, ws.fdist,
+    bool ok = layer_search(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh, ws.fdist,
                            ws.H, L.hash_log2, cnt, lane);
     int64_t *oid = out_ids + (size_t)q * k;
     double *od = out_d + (size_t)q * k;
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     uint32_t d0 = adt_one(ws.adt, g.codes + (size_t)entry * g.mpad, g.mpad, lane);
     cnt.dist += 1;
     int ts = 0;
-    bool ok = layer_search(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.fresh,
+    bool ok = layer_search(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                            ws.fdist, ws.H, L.hash_log2, cnt, lane);
     if (!ok) {
         if (lane == 0) atomicExch(err, 1);

@@ -42,7 +42,7 @@ __device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
 
 // ---- per-warp workspace ----------------------------------------------------
 struct WarpLayout {
-    int adt, T, S, fresh, fdist, hash, total;
+    int adt, T, S, TQ, fresh, fdist, hash, total;
     int hash_log2;
     __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
     __host__ __device__ void init(int mpad, int W, int capmax, int hlog2) {
@@ -50,7 +50,8 @@ struct WarpLayout {
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
         T = o; o += round_up(W, 32) * 8;
-        S = o; o += 32 * 8;
+        S = o; o += 256 * 8;  // two 128-key candidate buffers
+        TQ = o; o += round_up(W, 32) * 4;
         fresh = o; o += round_up(capmax, 32) * 4;
         fdist = o; o += round_up(capmax, 32) * 4;
         hash = o; o += (4 << hlog2);
@@ -174,42 +175,18 @@ __device__ __forceinline__ int count_less(const unsigned long long *a, int n, un
     return c;
 }
 
-// Merge the candidates held by the lanes with keep == true (unsorted, distinct
-// keys) into the sorted buffer T[0..ts), keeping the W smallest — without
-// sorting them first: a candidate's final position is its rank in T plus its
-// rank among the candidates; T's tail moves right in place, highest 32-entry
-// chunk first, so no element is overwritten before it is read.
-// Returns the lowest position that changed (W if nothing entered).
-__device__ __forceinline__ int merge_unsorted(unsigned long long *T, int &ts, int W,
-                                              unsigned long long *S, unsigned long long s,
-                                              bool keep, int lane) {
-    const unsigned bk = __ballot_sync(0xffffffffu, keep);
-    const int ns = __popc(bk);
-    if (ns == 0) return W;
-    if (keep) S[__popc(bk & ((1u << lane) - 1u))] = s;
-    __syncwarp();
-    const int p = keep ? lower_rank(T, ts, s) + count_less(S, ns, s) : W;
-    const int p0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)p);
-    const int newts = min(W, ts + ns);
-    if (p0 >= newts) return W;
-    if (ts > p0) {
-        for (int base = p0 + ((ts - 1 - p0) & ~31); base >= p0; base -= 32) {
-            const int i = base + lane;
-            unsigned long long t = 0;
-            int np = W;
-            if (i < ts) {
-                t = T[i];
-                np = i + count_less(S, ns, t);
-            }
-            __syncwarp();
-            if (np < newts) T[np] = t;
-            __syncwarp();
-        }
+// Move T[lo..hi) one slot right (T[hi] is overwritten), highest 32-entry chunk
+// first, so no entry is overwritten before it is read.
+__device__ __forceinline__ void shift_right1(unsigned long long *T, int lo, int hi, int lane) {
+    if (hi <= lo) return;
+    for (int base = lo + ((hi - 1 - lo) & ~31); base >= lo; base -= 32) {
+        const int i = base + lane;
+        unsigned long long t = 0;
+        if (i < hi) t = T[i];
+        __syncwarp();
+        if (i < hi) T[i + 1] = t;
+        __syncwarp();
     }
-    if (keep && p < newts) T[p] = s;
-    __syncwarp();
-    ts = newts;
-    return p0;
 }
 
 struct SearchCounters {
@@ -242,10 +219,26 @@ __device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane,
     }
 }
 
+// Best-first search on one layer with the reference's semantic-core rules
+// (flashann/_pycore.py:246-283; ties by vertex id through tuple order):
+//   * the frontier pops in (d, id) order; the search stops once the result set
+//     is full and the popped distance exceeds the worst kept distance;
+//   * an expansion's fresh neighbours are offered in ascending (d, id); one is
+//     accepted while the set is not full or its distance is strictly below the
+//     worst, evicting the worst (largest d, smallest id on ties).
+// Representation: the result set T[0..ts) sorted by (d, id) with an
+// "expanded" bit (bit 0) — its unexpanded members are exactly the frontier
+// entries that can still be popped — plus the tie queue TQ of unexpanded
+// entries evicted at the current worst distance (a popped frontier entry with
+// d > worst stops the search, so nothing else in the frontier can matter).
+// Evictions at one worst distance remove members of the last distance group,
+// so TQ holds < W ids, ascending, and empties when the worst distance drops.
+// On return T[0..ts) is the result ascending by (d, id).  false = hash overflow.
 __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
                                     const uint8_t *adt_s, unsigned long long *T, int &ts,
-                                    unsigned long long *S, int32_t *fresh, uint32_t *fdist,
-                                    uint32_t *H, int hlog2, SearchCounters &cnt, int lane) {
+                                    unsigned long long *S, int32_t *TQ, int32_t *fresh,
+                                    uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
+                                    int lane) {
     const int cap = layer_cap(g, layer);
     const int hlimit = (1 << hlog2) - (1 << hlog2) / 8;
     hash_clear(H, hlog2, lane);
@@ -256,16 +249,22 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     }
     int nvis = 1;
     ts = 1;
-    int cur = 0;
-    // speculative id row of the most likely next expansion (the next
-    // unexpanded member before this step's merge)
+    int cur = 0;          // T[0..cur) are expanded
+    int tq_h = 0, tq_t = 0;  // tie queue TQ[tq_h..tq_t), distance == worst
+    // speculative id row of the most likely next pop
     int pre_v = -1;
     int pre[kRowChunks];
     __syncwarp();
     while (true) {
-        cur = next_unexpanded(T, ts, cur, lane);
-        if (cur < 0) break;
-        const int v = key_id(T[cur]);
+        // ---- pop the frontier minimum: first unexpanded of T vs tie queue head
+        const int c0 = next_unexpanded(T, ts, cur, lane);
+        cur = c0 >= 0 ? c0 : ts;
+        const unsigned long long kT = c0 >= 0 ? (T[c0] & ~1ull) : KEY_MAX;
+        const uint32_t wd = ts >= W ? key_d(T[W - 1]) : 0xffffffffu;
+        const unsigned long long kQ = tq_h < tq_t ? make_key(wd, TQ[tq_h]) : KEY_MAX;
+        if (kT == KEY_MAX && kQ == KEY_MAX) break;
+        const bool fromT = kT < kQ;
+        const int v = key_id(fromT ? kT : kQ);
         int u[kRowChunks];
         if (v == pre_v) {
 #pragma unroll
@@ -273,11 +272,21 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         } else {
             load_row(row_ids(g, layer, v), cap, lane, u);
         }
-        const int nxt = next_unexpanded(T, ts, cur + 1, lane);
-        pre_v = nxt >= 0 ? key_id(T[nxt]) : -1;
-        if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
+        {  // predict the next pop assuming nothing new enters
+            const int nt = fromT ? next_unexpanded(T, ts, cur + 1, lane) : c0;
+            const unsigned long long k1 = nt >= 0 ? (T[nt] & ~1ull) : KEY_MAX;
+            const int qh = fromT ? tq_h : tq_h + 1;
+            const unsigned long long k2 = qh < tq_t ? make_key(wd, TQ[qh]) : KEY_MAX;
+            const unsigned long long kn = k1 < k2 ? k1 : k2;
+            pre_v = kn != KEY_MAX ? key_id(kn) : -1;
+            if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
+        }
         __syncwarp();
-        if (lane == 0) T[cur] |= 1ull;
+        if (fromT) {
+            if (lane == 0) T[cur] |= 1ull;
+        } else {
+            ++tq_h;
+        }
         cnt.visited++;
         if (nvis + cap > hlimit) return false;
         // visited filter over the row, compacted in slot order
@@ -300,15 +309,52 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         __syncwarp();
         if (nf == 0) continue;
         dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
-        int lowest = W;
+        // candidates that can possibly enter: all while T is not full, else
+        // d < worst; sorted ascending by (d, id) through their ranks
+        unsigned long long *Sa = S, *Sb = S + 128;
+        const uint32_t wd0 = ts >= W ? key_d(T[W - 1]) : 0xffffffffu;
+        int ns = 0;
         for (int base = 0; base < nf; base += 32) {
             const int f = base + lane;
-            unsigned long long k = f < nf ? make_key(fdist[f], fresh[f]) : KEY_MAX;
-            const unsigned long long worst = ts < W ? KEY_MAX : T[W - 1];
-            int p0 = merge_unsorted(T, ts, W, S, k, k < worst, lane);
-            lowest = min(lowest, p0);
+            const bool ok = f < nf && fdist[f] < wd0;
+            const unsigned b = __ballot_sync(0xffffffffu, ok);
+            if (ok) Sa[ns + __popc(b & ((1u << lane) - 1u))] = make_key(fdist[f], fresh[f]);
+            ns += __popc(b);
         }
-        if (lowest < cur) cur = lowest;
+        __syncwarp();
+        if (ns == 0) continue;
+        for (int j = lane; j < ns; j += 32) {
+            const unsigned long long k = Sa[j];
+            Sb[count_less(Sa, ns, k)] = k;
+        }
+        __syncwarp();
+        // offer them in order; the accepted ones form a prefix
+        for (int j = 0; j < ns; ++j) {
+            const unsigned long long s = Sb[j];
+            if (ts < W) {
+                const int pos = lower_rank(T, ts, s);
+                shift_right1(T, pos, ts, lane);
+                if (lane == 0) T[pos] = s;
+                ++ts;
+                cur = min(cur, pos);
+            } else {
+                const uint32_t wd = key_d(T[W - 1]);
+                if (key_d(s) >= wd) break;
+                // evict the first member of the last distance group
+                const int e = lower_rank(T, ts, (unsigned long long)wd << 32);
+                const unsigned long long ev = T[e];
+                const int pos = lower_rank(T, e, s);  // s < ev, so pos <= e
+                __syncwarp();
+                if (lane == 0 && !(ev & 1ull)) TQ[tq_t] = key_id(ev);
+                if (!(ev & 1ull)) ++tq_t;
+                shift_right1(T, pos, e, lane);  // T[e] (the evicted) is overwritten
+                if (lane == 0) T[pos] = s;
+                __syncwarp();
+                cur = min(cur, pos);
+                if (key_d(T[W - 1]) < wd) tq_h = tq_t = 0;  // worst dropped: ties are gone
+            }
+            __syncwarp();
+        }
     }
     return true;
 }

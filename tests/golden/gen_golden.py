@@ -134,6 +134,50 @@ def main() -> None:
         recalls.append(fa.evaluation.recall_at_k(ids, gt))
     out["g_ref_recall"] = np.array(recalls)
 
+    # the reference's semantic core (_pycore, ties by vertex id) on that graph:
+    # greedy_search_layer results, with the compiled core's fp32 query tables
+    hb, hu = out["g_base"], out["g_upper"]
+    w = fa._pycore.GraphWriter(4, pv, out["g_levels"], hb, out["g_uoff"], hu, g["C"], g["R"])
+    rng = np.random.default_rng(77)
+    ents = rng.integers(0, hb.shape[0], size=out["g_qproj"].shape[0])
+    rows = []
+    for width in gi.PY_WIDTHS:
+        for q in range(out["g_qproj"].shape[0]):
+            _, adt = EXT.flash_encode_adt(pv["cent"], pv["dims"], pv["offs"], pv["dist_min"],
+                                          pv["delta"], out["g_qproj"][q])
+            res_q = w.greedy_search_layer({"adt": adt}, int(ents[q]), width, 0)
+            rows.append(np.array([u for u, _ in res_q] + [-1] * (width - len(res_q)), np.int32))
+    out["py_entries"] = ents
+    out["py_search_ids"] = np.concatenate(rows)
+
+    # a full sequential build by the semantic core (fp32 encoder patched in)
+    real_enc = fa._pycore.flash_encode_adt
+    fa._pycore.flash_encode_adt = lambda c, d, o, a, b, r: EXT.flash_encode_adt(
+        c, d, o, a, b, np.asarray(r, np.float32))
+    try:
+        pb = gi.PY_BUILD
+        data = gi.mixture(pb["n"], pb["dim"], pb["clusters"], 900, sigma=0.4, spread=1.0)
+        model = fa.flash_train(fa.VectorDataset(data), d_f=pb["d_f"], m_f=pb["m_f"], seed=0,
+                               kmeans_iters=5)
+        prov = fa.FlashProvider(model)
+        prov.attach(fa.VectorDataset(data))
+        p2 = prov.core_arrays()
+        levels = fa.assign_layers(pb["n"], pb["seed"], pb["R"])
+        gi_ = fa.GraphIndex(pb["n"], pb["dim"], fa.BuildParams(C=pb["C"], R=pb["R"]), "flash",
+                            model.m, levels)
+        o2 = fa._pycore.build_graph(4, p2, levels, gi_.base_blocks, gi_.upper_offsets,
+                                    gi_.upper_blocks, pb["C"], pb["R"])
+    finally:
+        fa._pycore.flash_encode_adt = real_enc
+    for k in ("proj", "codes", "cent", "dims", "offs", "sdt"):
+        out["pb_" + k] = p2[k]
+    out["pb_range"] = np.array([p2["dist_min"], p2["delta"]])
+    out["pb_levels"] = levels
+    out["pb_uoff"] = gi_.upper_offsets
+    out["pb_base"] = gi_.base_blocks
+    out["pb_upper"] = gi_.upper_blocks
+    out["pb_state"] = np.array([o2["entry_point"], o2["max_layer"]])
+
     np.savez_compressed(OUT / "reference_golden.npz", **out)
     print("wrote", OUT / "reference_golden.npz", "recall", recalls)
 

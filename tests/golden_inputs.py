@@ -23,6 +23,9 @@ MODELS = {
 
 GRAPH = {"n": 2000, "nq": 100, "dim": 32, "clusters": 24, "sigma": 0.3, "d_f": 32, "m_f": 16,
          "R": 8, "C": 48, "seed": 0, "iters": 10, "ef": 32}
+PY_WIDTHS = (4, 16, 48)
+# sequential build by the reference's semantic core (_pycore), ~1 min on CPU
+PY_BUILD = {"n": 600, "dim": 24, "clusters": 6, "d_f": 24, "m_f": 8, "R": 4, "C": 24, "seed": 5}
 
 
 def l2_inputs(d: int, count: int = 64):

@@ -131,6 +131,55 @@ def test_batched_build_matches_oracle(core, golden, sched):
         assert res["counters"][k] == oc[k], k
 
 
+def test_layer_search_matches_semantic_core(core, golden):
+    """Bit-exact against the reference's semantic core (_pycore
+    greedy_search_layer) on the reference-built graph (golden)."""
+    prov = _prov(golden)
+    ix = core.DeviceIndex(prov, golden["g_levels"], golden["g_base"], golden["g_uoff"],
+                          golden["g_upper"], gi.GRAPH["R"])
+    qp = golden["g_qproj"]
+    expect = golden["py_search_ids"]
+    off = 0
+    for width in gi.PY_WIDTHS:
+        ids, _, ns, _ = ix.search_layer(qp, golden["py_entries"], width, 0)
+        for q in range(qp.shape[0]):
+            row = expect[off: off + width]
+            off += width
+            assert list(ids[q, : ns[q]]) == [int(x) for x in row if x >= 0], (width, q)
+    ix.close()
+
+
+def test_sequential_build_matches_semantic_core(core, golden):
+    """Batch size 1 = the reference's sequential build: every row equals the
+    graph _pycore.build_graph built (golden, same encoder outputs)."""
+    from paper_2502_18113_b200 import layout
+
+    pb = gi.PY_BUILD
+    dmin, delta = golden["pb_range"]
+    prov = {"vecs": np.zeros((pb["n"], 1), np.float32), "proj": golden["pb_proj"],
+            "codes": np.zeros_like(golden["pb_codes"]), "cent": golden["pb_cent"],
+            "dims": golden["pb_dims"], "offs": golden["pb_offs"], "sdt": golden["pb_sdt"],
+            "dist_min": float(dmin), "delta": float(delta)}
+    levels, uoff = golden["pb_levels"], golden["pb_uoff"]
+    R, m = pb["R"], prov["cent"].shape[0]
+    base = layout.empty_rows(pb["n"], 2 * R, m)
+    upper = layout.empty_rows(int(levels.sum()), R, m)
+    saved = dict(core.BUILD_OPTIONS)
+    core.BUILD_OPTIONS.update(SCHEDULES["sequential"])
+    try:
+        res = core.build_graph(4, prov, levels, base, uoff, upper, pb["C"], R)
+    finally:
+        core.BUILD_OPTIONS.clear()
+        core.BUILD_OPTIONS.update(saved)
+    assert [res["entry_point"], res["max_layer"]] == list(golden["pb_state"])
+    assert np.array_equal(prov["codes"], golden["pb_codes"])
+    for v in range(pb["n"]):
+        assert np.array_equal(layout.row_ids(base, v, 2 * R),
+                              layout.row_ids(golden["pb_base"], v, 2 * R)), v
+    for r in range(upper.shape[0]):
+        assert np.array_equal(layout.row_ids(upper, r, R), layout.row_ids(golden["pb_upper"], r, R))
+
+
 def test_flash_narrated_trace(core):
     """Narrated fixture (Flash form): final set [17, 5, 3, 9] after exactly
     seven distance computations; pruning to 2 keeps [17, 5]."""

@@ -106,6 +106,37 @@ def test_oracle_search_on_reference_graph_is_order_free(golden):
         assert np.array_equal(ids, base[q][0]) and np.array_equal(ds, base[q][1])
 
 
+def test_oracle_search_matches_semantic_core_golden(golden):
+    hg = _golden_graph(golden)
+    cent, dims, offs = golden["g_cent"], golden["g_dims"], golden["g_offs"]
+    dmin, delta = golden["g_range"]
+    _, adts = native.encode_adt(golden["g_qproj"], cent, dims, offs, dmin, delta)
+    expect = golden["py_search_ids"]
+    off = 0
+    for width in gi.PY_WIDTHS:
+        for q in range(adts.shape[0]):
+            ids, _, _ = hg.layer_search(adts[q], 0, int(golden["py_entries"][q]), width)
+            row = expect[off: off + width]
+            off += width
+            assert list(ids) == [int(x) for x in row if x >= 0], (width, q)
+
+
+def test_oracle_sequential_build_matches_semantic_core_golden(golden):
+    from paper_2502_18113_b200 import layout
+
+    pb = gi.PY_BUILD
+    dmin, delta = golden["pb_range"]
+    hg = native.HostGraph(golden["pb_levels"], golden["pb_uoff"], pb["R"],
+                          golden["pb_cent"].shape[0])
+    res = hg.build(golden["pb_proj"], golden["pb_cent"], golden["pb_dims"], golden["pb_offs"],
+                   dmin, delta, golden["pb_sdt"], pb["C"], batch_max=1, batch_frac=1.0,
+                   seq_prefix=1 << 30)
+    assert [res["entry_point"], res["max_layer"]] == list(golden["pb_state"])
+    assert np.array_equal(hg.codes, golden["pb_codes"])
+    for v in range(pb["n"]):
+        assert list(hg.neighbors(v, 0)) == list(layout.row_ids(golden["pb_base"], v, 2 * pb["R"]))
+
+
 def test_schedule_properties():
     levels = np.zeros(5000, np.int32)
     levels[[0, 10, 300, 2000]] = [1, 2, 3, 1]
