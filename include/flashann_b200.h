@@ -153,6 +153,10 @@ typedef struct {
     int seq_prefix;       /* first vertices inserted one per batch (-1 default)  */
     int hash_log2;        /* visited-hash size per warp = 2^hash_log2 (0 = auto) */
     int profile;          /* 1: time every kernel class with CUDA events        */
+    int tie;              /* order among equal distances in the searches:
+                             0 vertex id (reference semantic core, _pycore.py),
+                             1 fixed id scramble, 2 scramble salted per
+                             inserted vertex (default of the Python layer)     */
 } fa_build_opts;
 
 typedef struct {
@@ -188,6 +192,10 @@ int fa_index_build(fa_index *idx, const fa_build_opts *opts, fa_build_result *re
 int fa_index_search(fa_index *idx, const float *queries, const float *qproj, int nq, int ef,
                     int k, int rerank_depth, int64_t entry, int max_layer, int64_t *out_ids,
                     double *out_d, int64_t *counters, void *stream);
+
+/* Tie order (fa_build_opts.tie modes) used by fa_index_search and
+ * fa_index_search_layer; 0 (vertex id) by default.                            */
+int fa_index_set_search_tie(fa_index *idx, int mode);
 
 /* Single-layer candidate search from a given entry (greedy_search_layer,
  * _core.pyx:891-939) for nq queries; out_ids/out_d nq x width, out_n nq.     */

@@ -172,6 +172,7 @@ typedef struct {
     uint64_t *rs;      /* result max-heap, key (d << 32 | ~u): top = max d, min u */
     uint64_t *fresh;   /* (d << 32 | u) of one expansion                         */
     size_t fr_cap;
+    uint32_t salt;     /* tie-order salt of the current search                   */
 } scratch;
 
 static void heap_push_min(uint64_t *h, int *n, uint64_t k) {
@@ -222,6 +223,28 @@ static void heap_pop_max(uint64_t *h, int *n) {
 }
 static uint64_t rkey(uint64_t d, uint32_t u) { return (d << 32) | (uint32_t)~u; }
 
+/* Tie order among equal distances: vertex id (tie = 0, the reference's
+ * semantic core) or a fixed bijective scramble of the id (tie = 1; a
+ * deterministic stand-in for the compiled core's heap-order tie breaks). */
+#define TIE_MUL 0x2545F491u
+static uint32_t tie_inv(void) {
+    uint32_t x = TIE_MUL; /* Newton iteration for the inverse mod 2^32 */
+    for (int i = 0; i < 5; ++i) x *= 2u - TIE_MUL * x;
+    return x;
+}
+/* tie = 2 salts the scramble per search (salt = hash of the inserted vertex
+ * or query), so different insertions break ties differently, as the compiled
+ * core's history-dependent heap order does. */
+static uint32_t tie_salt(int tie, uint32_t who) {
+    return tie == 2 ? ((who + 1u) * 0x9E3779B1u) & 0x7fffffffu : 0u;
+}
+static uint32_t tie_fwd(int tie, uint32_t salt, uint32_t u) {
+    return tie ? ((u ^ salt) * TIE_MUL) & 0x7fffffffu : u;
+}
+static uint32_t tie_back(int tie, uint32_t salt, uint32_t t) {
+    return tie ? ((t * tie_inv()) & 0x7fffffffu) ^ salt : t;
+}
+
 /* Best-first layer search with the semantics of the reference's semantic
  * core (flashann/_pycore.py:246-283): frontier popped in (d, id) order; stop
  * once the result set is full and the popped distance exceeds its worst
@@ -238,14 +261,15 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
         s->epoch = 1;
     }
     uint32_t ep = s->epoch;
+    const int tie = g->tie;
     s->visited[entry] = ep;
     int nf = 0, nr = 0;
-    heap_push_min(s->fr, &nf, ((uint64_t)entry_d << 32) | (uint32_t)entry);
-    heap_push_max(s->rs, &nr, rkey((uint64_t)entry_d, (uint32_t)entry));
+    heap_push_min(s->fr, &nf, ((uint64_t)entry_d << 32) | tie_fwd(tie, s->salt, (uint32_t)entry));
+    heap_push_max(s->rs, &nr, rkey((uint64_t)entry_d, tie_fwd(tie, s->salt, (uint32_t)entry)));
     while (nf > 0) {
         uint64_t top = heap_pop_min(s->fr, &nf);
         uint64_t d = top >> 32;
-        int v = (int)(uint32_t)top;
+        int v = (int)tie_back(tie, s->salt, (uint32_t)top);
         if (nr >= W && d > (s->rs[0] >> 32)) break;
         if (c) c->visited++;
         int32_t *ids = row_of(g, layer, v);
@@ -258,7 +282,7 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
             if (u < 0 || s->visited[u] == ep) continue;
             s->visited[u] = ep;
             uint64_t du = (uint64_t)adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
-            s->fresh[nfresh++] = (du << 32) | (uint32_t)u;
+            s->fresh[nfresh++] = (du << 32) | tie_fwd(tie, s->salt, (uint32_t)u);
         }
         if (c) c->dist_comps += nfresh;
         qsort(s->fresh, (size_t)nfresh, sizeof(uint64_t), cmp_u64);
@@ -281,7 +305,9 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
         uint64_t k = s->rs[i];
         out[i] = (k & 0xffffffff00000000ull) | (uint32_t)~(uint32_t)k;
     }
-    qsort(out, (size_t)nr, sizeof(uint64_t), cmp_u64);
+    qsort(out, (size_t)nr, sizeof(uint64_t), cmp_u64);  /* (d, tie key) ascending */
+    for (int i = 0; i < nr; ++i)
+        out[i] = (out[i] & 0xffffffff00000000ull) | tie_back(tie, s->salt, (uint32_t)out[i]);
     return nr;
 }
 
@@ -321,6 +347,7 @@ static int scratch_init(scratch *s, int64_t n, int W, int capmax) {
     s->rs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 2));
     s->fresh = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 8));
     s->epoch = 0;
+    s->salt = 0;
     return (s->visited && s->fr && s->rs && s->fresh) ? 0 : -1;
 }
 static void scratch_free(scratch *s) {
@@ -484,6 +511,7 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
                 hill_climb_impl(g, adts, layer, &cur, &curd, c);
             int top = bml < level ? bml : level;
             for (int layer = top; layer >= 0; --layer) {
+                s.salt = tie_salt(g->tie, (uint32_t)x);
                 int ts = layer_search_impl(g, &s, adts, layer, cur, curd, C, T, c);
                 for (int j = 0; j < ts; ++j) {
                     cid[j] = (int32_t)(T[j] & 0xffffffffu);
@@ -556,6 +584,7 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
         int curd = adt_sum(adt, g->codes + (size_t)cur * g->cs, m);
         if (c) c->dist_comps++;
         for (int layer = max_layer; layer > 0; --layer) hill_climb_impl(g, adt, layer, &cur, &curd, c);
+        s.salt = tie_salt(g->tie, (uint32_t)q);
         int ts = layer_search_impl(g, &s, adt, 0, cur, curd, ef, T, c);
         int64_t *oi = out_ids + (size_t)q * k;
         double *od = out_d + (size_t)q * k;

@@ -21,6 +21,7 @@ typedef struct {
     const int32_t *levels;
     const int64_t *uoff;
     const int32_t *upper_owner; /* nU: vertex owning each upper row */
+    int tie;                    /* 0: ties by id; 1: by the scrambled id    */
 } or_graph;
 
 typedef struct {

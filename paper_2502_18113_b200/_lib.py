@@ -34,7 +34,8 @@ class IndexDesc(C.Structure):
 
 class BuildOpts(C.Structure):
     _fields_ = [("C", C.c_int), ("batch_max", C.c_int), ("batch_frac", f64),
-                ("seq_prefix", C.c_int), ("hash_log2", C.c_int), ("profile", C.c_int)]
+                ("seq_prefix", C.c_int), ("hash_log2", C.c_int), ("profile", C.c_int),
+                ("tie", C.c_int)]
 
 
 class BuildResult(C.Structure):
@@ -76,6 +77,7 @@ _SIGS = {
                                   vp, vp, vp, vp]),
     "fa_index_search_layer": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp, vp,
                                         vp]),
+    "fa_index_set_search_tie": (C.c_int, [vp, C.c_int]),
     "fa_index_export_blocks": (C.c_int, [vp, vp, i64, vp, i64, vp]),
     "fa_index_import_blocks": (C.c_int, [vp, vp, i64, vp, i64, vp]),
     "fa_index_codes": (vp, [vp, C.POINTER(C.c_int)]),

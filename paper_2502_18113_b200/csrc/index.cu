@@ -24,6 +24,8 @@ struct fa_index {
     int32_t *adj0 = nullptr, *cnt0 = nullptr, *adjU = nullptr, *cntU = nullptr;
     uint8_t *cons0 = nullptr, *consU = nullptr;
     int32_t *upper_owner = nullptr;
+    uint32_t *gvis = nullptr, *gvis_epoch = nullptr;  // global visited tier
+    int search_tie = 0;
     int64_t entry = -1;
     int max_layer = -1;
 };
@@ -60,11 +62,29 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
     return FA_OK;
 }
 
+// Global visited tier (VisitedSet): one 2^kGlobalHashLog2-entry table per
+// hardware warp slot, allocated on first use; absent for n >= 2^24 (the tier
+// packs ids into 24 bits), where the shared tier alone must suffice.
+static int ensure_gvis(fa_index *ix) {
+    if (ix->gvis || ix->g.n >= (1ll << 24) - 1) return FA_OK;
+    int dev = 0, sms = 0;
+    FA_CUDA(cudaGetDevice(&dev));
+    FA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t slots = (size_t)sms * kMaxWarpsPerSM;
+    FA_TRY(dev_alloc((void **)&ix->gvis, (slots << kGlobalHashLog2) * sizeof(uint32_t)));
+    FA_TRY(dev_alloc((void **)&ix->gvis_epoch, slots * sizeof(uint32_t)));
+    FA_CUDA(cudaMemset(ix->gvis, 0, (slots << kGlobalHashLog2) * sizeof(uint32_t)));
+    FA_CUDA(cudaMemset(ix->gvis_epoch, 0, slots * sizeof(uint32_t)));
+    ix->g.gvis = ix->gvis;
+    ix->g.gvis_epoch = ix->gvis_epoch;
+    return FA_OK;
+}
+
 static int pick_hash_log2(int W, int capmax, int R, int mpad, int req) {
     if (req > 0) return req;
-    int want = 16 * W + 2 * capmax;
+    int want = 8 * W + 2 * capmax;  // the global tier absorbs longer searches
     int l = 9;
-    while ((1 << l) < want) ++l;
+    while ((1 << l) < want && l < 12) ++l;
     // kept ids + codes alias the hash during forward selection
     while ((4 << l) < round_up(R * 4, 16) + R * kept_stride(mpad)) ++l;
     return l;
@@ -175,6 +195,9 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.codes = ix->codes;
     g.adj0 = ix->adj0; g.cnt0 = ix->cnt0; g.cons0 = ix->cons0;
     g.adjU = ix->adjU; g.cntU = ix->cntU; g.consU = ix->consU;
+    g.tie = 0;
+    g.gvis = nullptr;
+    g.gvis_epoch = nullptr;
     // host copies of the layer draws drive the batch schedule
     ix->levels_h.resize(g.n);
     ix->uoff_h.resize(g.n);
@@ -225,7 +248,15 @@ extern "C" int fa_index_destroy(fa_index *ix) {
     cudaFree(ix->adj0); cudaFree(ix->cnt0); cudaFree(ix->cons0);
     cudaFree(ix->adjU); cudaFree(ix->cntU); cudaFree(ix->consU);
     cudaFree(ix->upper_owner);
+    cudaFree(ix->gvis);
+    cudaFree(ix->gvis_epoch);
     delete ix;
+    return FA_OK;
+}
+
+extern "C" int fa_index_set_search_tie(fa_index *ix, int mode) {
+    FA_CHECK_ARG(ix && mode >= 0 && mode <= 2, "tie mode must be 0, 1 or 2");
+    ix->search_tie = mode;
     return FA_OK;
 }
 
@@ -281,6 +312,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     res->entry_point = -1;
     res->max_layer = -1;
     FA_TRY(reset_graph(ix, st));
+    FA_TRY(ensure_gvis(ix));
+    FA_CHECK_ARG(opts->tie >= 0 && opts->tie <= 2, "tie mode must be 0, 1 or 2");
+    Graph gb = g;  // the build's view: its own tie order
+    gb.tie = opts->tie;
     if (g.n == 0) {
         ix->entry = -1;
         ix->max_layer = -1;
@@ -423,7 +458,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
         int grid = (b.size + kSearchWarps - 1) / kSearchWarps;
         build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
-            g, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+            gb, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
             req, ctr, err);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
@@ -439,7 +474,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         int rgrid = (int)std::min<int64_t>(rev_ctas, (b.nreq + 32 * kReverseWarps - 1) /
                                                           (32 * kReverseWarps) + 1);
         reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
-            g, ix->d.sdt, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
+            gb, ix->d.sdt, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
         launches += 4;
@@ -512,6 +547,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     cudaStream_t st = as_stream(stream);
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
+    FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
     L.init(ix->g.mpad, ef, capmax, pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0));
@@ -531,8 +567,10 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
         cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
         cudaMemsetAsync(err, 0, sizeof(int), st);
         int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        Graph gq = ix->g;
+        gq.tie = ix->search_tie;
         query_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
-            ix->g, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
+            gq, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
             queries, L, out_ids, out_d, ctr, err);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);
@@ -566,6 +604,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     cudaStream_t st = as_stream(stream);
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
+    FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
     L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0));
@@ -585,8 +624,10 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
         cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
         cudaMemsetAsync(err, 0, sizeof(int), st);
         int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        Graph gq = ix->g;
+        gq.tie = ix->search_tie;
         layer_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
-            ix->g, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
+            gq, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     if (p >= size) return;
     WarpWS ws(smem + sdt_bytes + wid * L.total, L);
     const int x = start + p;
+    const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
     load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
     __syncwarp();
     SearchCounters cnt = {0, 0, 0, 0};
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     for (int layer = top; layer >= 0; --layer) {
         int ts = 0;
         bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
-                               ws.fdist, ws.H, L.hash_log2, cnt, lane);
+                               ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
         if (!ok) {
             if (lane == 0) atomicExch(err, 1);
             for (int l = layer; l >= 0; --l)
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
             sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
             [&](int j, int &v, double &dv) {
                 unsigned long long k = T[j];
-                v = key_id(k);
+                v = to.back((uint32_t)key_id(k));
                 dv = (double)key_d(k);
             },
             kept, kcodes, lane, &sym);
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
             lreq[j] = j < nsel ? ((unsigned long long)row_global(g, layer, kept[j]) << 32) |
                                      (uint32_t)x
                                : KEY_MAX;
-        cur = key_id(ws.T[0]);
+        cur = to.back((uint32_t)key_id(ws.T[0]));
         curd = key_d(ws.T[0]);
         __syncwarp();
     }
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     const int q = blockIdx.x * kSearchWarps + wid;
     if (q >= nq) return;
     WarpWS ws(smem + wid * L.total, L);
+    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();
     SearchCounters cnt = {0, 0, 0, 0};
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
         hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
     int ts = 0;
     bool ok = layer_search(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh, ws.fdist,
-                           ws.H, L.hash_log2, cnt, lane);
+                           ws.H, L.hash_log2, cnt, to, lane);
     int64_t *oid = out_ids + (size_t)q * k;
     double *od = out_d + (size_t)q * k;
     if (!ok) {
@@ -192,7 +194,8 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
         const float *qv = queries + (size_t)q * dim;
         for (int base = 0; base < rr; base += 4) {
             int j = base + (lane >> 3);
-            const float *vv = j < rr ? vecs + (size_t)key_id(ws.T[j]) * dim : nullptr;
+            const float *vv =
+                j < rr ? vecs + (size_t)to.back((uint32_t)key_id(ws.T[j])) * dim : nullptr;
             float s = warp_l2_group(j < rr ? qv : nullptr, vv, dim, lane);
             if ((lane & 7) == 0 && j < rr) dd[j] = (double)s;
         }
@@ -200,11 +203,11 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
         // rank sort by (d, id) (fa_pair_cmp, _simd.h:237-243)
         for (int j = lane; j < rr; j += 32) {
             double dj = dd[j];
-            int idj = key_id(ws.T[j]);
+            int idj = to.back((uint32_t)key_id(ws.T[j]));
             int rank = 0;
             for (int t = 0; t < rr; ++t) {
                 double dt = dd[t];
-                int idt = key_id(ws.T[t]);
+                int idt = to.back((uint32_t)key_id(ws.T[t]));
                 rank += (dt < dj) || (dt == dj && idt < idj);
             }
             if (rank < k) {
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     } else {
         for (int j = lane; j < k; j += 32) {
             if (j < ts) {
-                oid[j] = key_id(ws.T[j]);
+                oid[j] = to.back((uint32_t)key_id(ws.T[j]));
                 od[j] = (double)key_d(ws.T[j]);
             } else {
                 oid[j] = -1;
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     const int q = blockIdx.x * kSearchWarps + wid;
     if (q >= nq) return;
     WarpWS ws(smem + wid * L.total, L);
+    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();
     SearchCounters cnt = {0, 0, 0, 0};
@@ -249,13 +253,13 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     cnt.dist += 1;
     int ts = 0;
     bool ok = layer_search(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
-                           ws.fdist, ws.H, L.hash_log2, cnt, lane);
+                           ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
     if (!ok) {
         if (lane == 0) atomicExch(err, 1);
         ts = 0;
     }
     for (int j = lane; j < width; j += 32) {
-        out_ids[(size_t)q * width + j] = j < ts ? key_id(ws.T[j]) : -1;
+        out_ids[(size_t)q * width + j] = j < ts ? to.back((uint32_t)key_id(ws.T[j])) : -1;
         out_d[(size_t)q * width + j] = j < ts ? (double)key_d(ws.T[j]) : 0.0;
     }
     if (lane == 0) out_n[q] = ts;

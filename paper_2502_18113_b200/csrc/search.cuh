@@ -30,6 +30,9 @@ struct Graph {
     const int32_t *levels;
     const int64_t *uoff;
     int64_t nU;
+    int tie;  // tie order of the searches (TieOrder modes)
+    uint32_t *gvis;        // global visited tables, one per SM warp slot (or null)
+    uint32_t *gvis_epoch;  // their epoch counters
 };
 
 __device__ __forceinline__ const int32_t *row_ids(const Graph &g, int layer, int v) {
@@ -147,6 +150,91 @@ __device__ __forceinline__ bool hash_insert(uint32_t *H, int hlog2, int id) {
     }
 }
 
+// Exact visited set of one search: an open-addressing table in shared memory,
+// spilling to a per-warp-slot table in global memory (L2-resident) once the
+// shared one is 7/8 full.  An id lives in exactly one tier: lookups walk the
+// shared chain to its first empty slot, then the global chain.  Global slots
+// hold (epoch << 24 | id); entries of older epochs count as empty, so the
+// global table is cleared only once every 255 searches of its warp slot.
+constexpr int kGlobalHashLog2 = 14;
+constexpr int kMaxWarpsPerSM = 64;
+
+struct VisitedSet {
+    uint32_t *H;       // shared tier
+    int hlog2, hcount, hlimit;
+    uint32_t *G;       // global tier of this warp slot
+    uint32_t *gepoch;  // epoch counter of this warp slot
+    uint32_t epoch;
+    int gcount, glimit;
+
+    __device__ static uint32_t slot_id() {
+        uint32_t sm, w;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(w));
+        return sm * kMaxWarpsPerSM + w;
+    }
+
+    __device__ void begin(uint32_t *gtables, uint32_t *gepochs, int lane) {
+        hash_clear(H, hlog2, lane);
+        hcount = 0;
+        hlimit = (1 << hlog2) - (1 << hlog2) / 8;
+        gcount = 0;
+        glimit = (1 << kGlobalHashLog2) - (1 << kGlobalHashLog2) / 8;
+        G = nullptr;
+        if (gtables) {
+            const uint32_t slot = slot_id();
+            G = gtables + ((size_t)slot << kGlobalHashLog2);
+            gepoch = gepochs + slot;
+            uint32_t e = 0;
+            if (lane == 0) e = *gepoch + 1u;
+            e = __shfl_sync(0xffffffffu, e, 0);
+            if (e > 255u) {  // wrap: clear this slot's table once
+                uint4 z = make_uint4(0, 0, 0, 0);
+                for (int i = lane; i < (1 << kGlobalHashLog2) / 4; i += 32)
+                    reinterpret_cast<uint4 *>(G)[i] = z;
+                e = 1u;
+            }
+            epoch = e;
+            __syncwarp();
+            if (lane == 0) *gepoch = e;
+        }
+        __syncwarp();
+    }
+
+    // 0 = already visited, 1 = new (shared tier), 2 = new (global tier)
+    __device__ int visit(int id, bool to_shared) {
+        const uint32_t key = (uint32_t)id + 1u;
+        const uint32_t mask = (1u << hlog2) - 1u;
+        uint32_t h = (key * 2654435761u) >> (32 - hlog2);
+        while (true) {
+            uint32_t v = H[h];
+            if (v == key) return 0;
+            if (v == 0u) {
+                if (!to_shared) break;
+                uint32_t old = atomicCAS(H + h, 0u, key);
+                if (old == 0u) return 1;
+                if (old == key) return 0;
+                continue;  // lost the slot: re-read it
+            }
+            h = (h + 1u) & mask;
+        }
+        const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
+        const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
+        uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
+        while (true) {
+            uint32_t v = G[p];
+            if (v == gk) return 0;
+            if ((v >> 24) != epoch) {
+                uint32_t old = atomicCAS(G + p, v, gk);
+                if (old == v) return 2;
+                if (old == gk) return 0;
+                continue;
+            }
+            p = (p + 1u) & gmask;
+        }
+    }
+};
+
 // ---- sorted top-W buffer ---------------------------------------------------
 constexpr unsigned long long KEY_MAX = ~0ull;
 
@@ -155,6 +243,36 @@ __device__ __forceinline__ unsigned long long make_key(uint32_t d, int id) {
 }
 __device__ __forceinline__ int key_id(unsigned long long k) { return (int)((k >> 1) & 0x7fffffffu); }
 __device__ __forceinline__ uint32_t key_d(unsigned long long k) { return (uint32_t)(k >> 32); }
+
+// Order among equal distances inside one search.  mode 0: vertex id (the
+// reference's semantic core, _pycore.py tuple order).  mode 1: a fixed
+// bijective scramble of the id.  mode 2: the scramble salted per search (the
+// inserted vertex / query), a deterministic stand-in for the compiled core's
+// history-dependent heap order — without it, every insertion prefers the same
+// (lowest-id) vertices among the many uint8 ties and the graph degrades
+// (DESIGN.md §ties).  Keys carry the tie id; `back` recovers the vertex id.
+constexpr uint32_t kTieMul = 0x2545F491u;
+__host__ __device__ constexpr uint32_t tie_inverse(uint32_t a) {
+    uint32_t x = a;
+    for (int i = 0; i < 5; ++i) x *= 2u - a * x;
+    return x;
+}
+struct TieOrder {
+    int mode;
+    uint32_t salt;
+    __device__ static TieOrder make(int mode, uint32_t who) {
+        TieOrder t;
+        t.mode = mode;
+        t.salt = mode == 2 ? ((who + 1u) * 0x9E3779B1u) & 0x7fffffffu : 0u;
+        return t;
+    }
+    __device__ __forceinline__ uint32_t fwd(uint32_t u) const {
+        return mode ? ((u ^ salt) * kTieMul) & 0x7fffffffu : u;
+    }
+    __device__ __forceinline__ int back(uint32_t t) const {
+        return (int)(mode ? ((t * tie_inverse(kTieMul)) & 0x7fffffffu) ^ salt : t);
+    }
+};
 
 // number of entries of sorted a[0..n) strictly less than x
 __device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, unsigned long long x) {
@@ -238,16 +356,17 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
                                     const uint8_t *adt_s, unsigned long long *T, int &ts,
                                     unsigned long long *S, int32_t *TQ, int32_t *fresh,
                                     uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
-                                    int lane) {
+                                    const TieOrder &to, int lane) {
     const int cap = layer_cap(g, layer);
-    const int hlimit = (1 << hlog2) - (1 << hlog2) / 8;
-    hash_clear(H, hlog2, lane);
-    __syncwarp();
+    VisitedSet vs;
+    vs.H = H;
+    vs.hlog2 = hlog2;
+    vs.begin(g.gvis, g.gvis_epoch, lane);
     if (lane == 0) {
-        hash_insert(H, hlog2, entry);
-        T[0] = make_key(entry_d, entry);
+        vs.visit(entry, true);
+        T[0] = make_key(entry_d, (int)to.fwd((uint32_t)entry));
     }
-    int nvis = 1;
+    vs.hcount = 1;
     ts = 1;
     int cur = 0;          // T[0..cur) are expanded
     int tq_h = 0, tq_t = 0;  // tie queue TQ[tq_h..tq_t), distance == worst
@@ -264,7 +383,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         const unsigned long long kQ = tq_h < tq_t ? make_key(wd, TQ[tq_h]) : KEY_MAX;
         if (kT == KEY_MAX && kQ == KEY_MAX) break;
         const bool fromT = kT < kQ;
-        const int v = key_id(fromT ? kT : kQ);
+        const int v = to.back((uint32_t)key_id(fromT ? kT : kQ));
         int u[kRowChunks];
         if (v == pre_v) {
 #pragma unroll
@@ -278,7 +397,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             const int qh = fromT ? tq_h : tq_h + 1;
             const unsigned long long k2 = qh < tq_t ? make_key(wd, TQ[qh]) : KEY_MAX;
             const unsigned long long kn = k1 < k2 ? k1 : k2;
-            pre_v = kn != KEY_MAX ? key_id(kn) : -1;
+            pre_v = kn != KEY_MAX ? to.back((uint32_t)key_id(kn)) : -1;
             if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
         __syncwarp();
@@ -288,7 +407,8 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             ++tq_h;
         }
         cnt.visited++;
-        if (nvis + cap > hlimit) return false;
+        const bool to_shared = vs.hcount + cap <= vs.hlimit;
+        if (!to_shared && (vs.G == nullptr || vs.gcount + cap > vs.glimit)) return false;
         // visited filter over the row, compacted in slot order
         int nf = 0, nlive = 0;
 #pragma unroll
@@ -296,14 +416,16 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             if (k * 32 >= cap) break;
             const int x = u[k];
             bool live = x >= 0;
-            bool fr = live && hash_insert(H, hlog2, x);
+            const int r = live ? vs.visit(x, to_shared) : 0;
+            const bool fr = r != 0;
             unsigned bl = __ballot_sync(0xffffffffu, live);
             unsigned bf = __ballot_sync(0xffffffffu, fr);
             if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
             nf += __popc(bf);
             nlive += __popc(bl);
+            vs.hcount += __popc(__ballot_sync(0xffffffffu, r == 1));
+            vs.gcount += __popc(__ballot_sync(0xffffffffu, r == 2));
         }
-        nvis += nf;
         cnt.kcalls += (nlive + 15) >> 4;
         cnt.dist += nf;
         __syncwarp();
@@ -318,7 +440,9 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             const int f = base + lane;
             const bool ok = f < nf && fdist[f] < wd0;
             const unsigned b = __ballot_sync(0xffffffffu, ok);
-            if (ok) Sa[ns + __popc(b & ((1u << lane) - 1u))] = make_key(fdist[f], fresh[f]);
+            if (ok)
+                Sa[ns + __popc(b & ((1u << lane) - 1u))] =
+                    make_key(fdist[f], (int)to.fwd((uint32_t)fresh[f]));
             ns += __popc(b);
         }
         __syncwarp();

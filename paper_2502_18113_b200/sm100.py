@@ -39,9 +39,13 @@ KERNEL_NAMES = ("sm100",)
 
 BUILD_OPTIONS = {
     "batch_max": int(os.environ.get("FLASHANN_B200_BATCH_MAX", "4096")),
-    "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.02")),
-    "seq_prefix": int(os.environ.get("FLASHANN_B200_SEQ_PREFIX", "256")),
+    "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.1")),
+    "seq_prefix": int(os.environ.get("FLASHANN_B200_SEQ_PREFIX", "0")),
     "hash_log2": int(os.environ.get("FLASHANN_B200_HASH_LOG2", "0")),
+    # tie order among equal distances during insertion searches: 2 = id
+    # scramble salted per inserted vertex; 0 reproduces
+    # the reference's semantic core (_pycore) exactly
+    "tie": int(os.environ.get("FLASHANN_B200_TIE", "2")),
     "profile": 0,
 }
 
@@ -78,7 +82,7 @@ def build_options(C_: int) -> _lib.BuildOpts:
     o = BUILD_OPTIONS
     return _lib.BuildOpts(C=C_, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
                           seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
-                          profile=o.get("profile", 0))
+                          profile=o.get("profile", 0), tie=o.get("tie", 2))
 
 
 def _prov_arrays(prov: dict):

@@ -92,11 +92,13 @@ SCHEDULES = {
     "sequential": dict(batch_max=1, batch_frac=1.0, seq_prefix=1 << 30),
     "small": dict(batch_max=64, batch_frac=0.05, seq_prefix=64),
     "wide": dict(batch_max=512, batch_frac=0.5, seq_prefix=16),
+    "default": dict(batch_max=4096, batch_frac=0.1, seq_prefix=0),
 }
 
 
+@pytest.mark.parametrize("tie", [0, 1, 2])
 @pytest.mark.parametrize("sched", list(SCHEDULES))
-def test_batched_build_matches_oracle(core, golden, sched):
+def test_batched_build_matches_oracle(core, golden, sched, tie):
     from paper_2502_18113_b200 import layout
 
     g = gi.GRAPH
@@ -107,13 +109,13 @@ def test_batched_build_matches_oracle(core, golden, sched):
     upper = layout.empty_rows(int(levels.sum()), R, m)
     opts = SCHEDULES[sched]
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(opts, hash_log2=0)
+    core.BUILD_OPTIONS.update(opts, hash_log2=0, tie=tie)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, g["C"], R)
     finally:
         core.BUILD_OPTIONS.clear()
         core.BUILD_OPTIONS.update(saved)
-    hg = native.HostGraph(levels, uoff, R, m)
+    hg = native.HostGraph(levels, uoff, R, m, tie=tie)
     ores = hg.build(prov["proj"], prov["cent"], prov["dims"], prov["offs"], prov["dist_min"],
                     prov["delta"], prov["sdt"], g["C"], **opts)
     assert res["entry_point"] == ores["entry_point"]
@@ -165,7 +167,7 @@ def test_sequential_build_matches_semantic_core(core, golden):
     base = layout.empty_rows(pb["n"], 2 * R, m)
     upper = layout.empty_rows(int(levels.sum()), R, m)
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(SCHEDULES["sequential"])
+    core.BUILD_OPTIONS.update(SCHEDULES["sequential"], tie=0)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, pb["C"], R)
     finally:
