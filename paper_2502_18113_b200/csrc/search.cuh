@@ -293,6 +293,41 @@ __device__ __forceinline__ int count_less(const unsigned long long *a, int n, un
     return c;
 }
 
+// Merge the sorted keys S[0..ns) into the sorted T[0..ts) (ts + ns <= capacity)
+// in place: T's entries only move right, so 32-entry chunks are processed from
+// the top; the new keys land last.  Returns the lowest position written.
+__device__ __forceinline__ int merge_sorted_into(unsigned long long *T, int &ts,
+                                                 const unsigned long long *S, int ns, int lane) {
+    if (ns == 0) return ts;
+    const int p0 = lower_rank(T, ts, S[0]);
+    int spos[4];  // final slots of S[lane + 32c] (ns <= 128), from the original T
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = lane + 32 * c;
+        spos[c] = j < ns ? j + lower_rank(T, ts, S[j]) : -1;
+    }
+    if (ts > p0) {
+        for (int base = p0 + ((ts - 1 - p0) & ~31); base >= p0; base -= 32) {
+            const int i = base + lane;
+            unsigned long long t = 0;
+            int np = -1;
+            if (i < ts) {
+                t = T[i];
+                np = i + lower_rank(S, ns, t);
+            }
+            __syncwarp();
+            if (np >= 0) T[np] = t;
+            __syncwarp();
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (spos[c] >= 0) T[spos[c]] = S[lane + 32 * c];
+    __syncwarp();
+    ts += ns;
+    return p0;
+}
+
 // Move T[lo..hi) one slot right (T[hi] is overwritten), highest 32-entry chunk
 // first, so no entry is overwritten before it is read.
 __device__ __forceinline__ void shift_right1(unsigned long long *T, int lo, int hi, int lane) {
@@ -452,16 +487,14 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             Sb[count_less(Sa, ns, k)] = k;
         }
         __syncwarp();
-        // offer them in order; the accepted ones form a prefix
-        for (int j = 0; j < ns; ++j) {
+        // offer them in order; the accepted ones form a prefix.  While T is
+        // not full every offer is accepted without eviction: merge that part
+        // in one pass.
+        const int nfill = min(ns, W - ts);
+        if (nfill > 0) cur = min(cur, merge_sorted_into(T, ts, Sb, nfill, lane));
+        for (int j = nfill; j < ns; ++j) {
             const unsigned long long s = Sb[j];
-            if (ts < W) {
-                const int pos = lower_rank(T, ts, s);
-                shift_right1(T, pos, ts, lane);
-                if (lane == 0) T[pos] = s;
-                ++ts;
-                cur = min(cur, pos);
-            } else {
+            {
                 const uint32_t wd = key_d(T[W - 1]);
                 if (key_d(s) >= wd) break;
                 // evict the first member of the last distance group
