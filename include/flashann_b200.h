@@ -157,6 +157,8 @@ typedef struct {
                              0 vertex id (reference semantic core, _pycore.py),
                              1 fixed id scramble, 2 scramble salted per
                              inserted vertex (default of the Python layer)     */
+    int64_t *point_stats; /* optional DEVICE n x 2: expansions, SM cycles of
+                             each vertex's insertion search (diagnostics)      */
 } fa_build_opts;
 
 typedef struct {

@@ -459,7 +459,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         int grid = (b.size + kSearchWarps - 1) / kSearchWarps;
         build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
             gb, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
-            req, ctr, err);
+            req, ctr, err, opts->point_stats);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         size_t tb = cub_bytes;

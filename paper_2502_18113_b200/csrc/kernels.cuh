@@ -13,7 +13,8 @@ __global__ void build_search_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                     int ep, int ml, int C, int R, WarpLayout L,
                                     const int64_t *__restrict__ req_off,
                                     unsigned long long *__restrict__ req,
-                                    unsigned long long *__restrict__ ctr, int *err);
+                                    unsigned long long *__restrict__ ctr, int *err,
+                                    int64_t *__restrict__ stats);
 
 __global__ void query_search_kernel(Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep,
                                     int ml, int ef, int k, int rerank_depth,

@@ -43,7 +43,8 @@ __device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned
 __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
-    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err) {
+    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
+    int64_t *__restrict__ stats) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int sdt_bytes = round_up(g.m * 256, 128);
     uint8_t *sdtT = smem;
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     if (p >= size) return;
     WarpWS ws(smem + sdt_bytes + wid * L.total, L);
     const int x = start + p;
+    const long long t_begin = clock64();
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
     load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
     __syncwarp();
@@ -114,6 +116,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
         cur = to.back((uint32_t)key_id(ws.T[0]));
         curd = key_d(ws.T[0]);
         __syncwarp();
+    }
+    if (stats && lane == 0) {
+        stats[2 * (int64_t)x] = (int64_t)cnt.visited;
+        stats[2 * (int64_t)x + 1] = clock64() - t_begin;
     }
     flush_counters(cnt, ctr, lane);
 }

@@ -177,9 +177,9 @@ struct VisitedSet {
     __device__ void begin(uint32_t *gtables, uint32_t *gepochs, int lane) {
         hash_clear(H, hlog2, lane);
         hcount = 0;
-        hlimit = (1 << hlog2) - (1 << hlog2) / 8;
+        hlimit = (1 << hlog2) / 2;  // linear probing stays short at load <= 1/2
         gcount = 0;
-        glimit = (1 << kGlobalHashLog2) - (1 << kGlobalHashLog2) / 8;
+        glimit = (1 << kGlobalHashLog2) * 3 / 4;
         G = nullptr;
         if (gtables) {
             const uint32_t slot = slot_id();
