@@ -157,10 +157,11 @@ def run_reference(args):
     model = train_np.train(train_np.training_sample(data, 100_000, 0), c["d_f"], c["m_f"], 0, 10)
     prov = cpu_prov(data, model)
     lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
-    # size each step so the whole run stays within ~3 minutes
-    _, rate = ref_cpu_build(prov, lvf, 4000, c["efC"], c["M"], threads)
+    # size each step so the whole run stays within ~3 minutes (calibrated on
+    # 20K vectors; the rate falls with n, hence the 0.5 margin)
+    _, rate = ref_cpu_build(prov, lvf, 20_000, c["efC"], c["M"], threads)
     steps = args.steps + args.warmup
-    n_sub = int(min(args.ref_max, max(4000, rate * 150.0 / steps)))
+    n_sub = int(min(args.ref_max, max(20_000, 0.5 * rate * 150.0 / steps)))
     for _ in range(args.warmup):
         ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)
     times = [ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)[0]
@@ -358,11 +359,13 @@ def main():
                   "sdt": model.sdt, "dist_min": model.dist_min, "dist_max": model.dist_max}
             cprov = provider.core_arrays()
             lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
-            cal = ref_cpu_build(cprov, lvf, 4000, c["efC"], c["M"], threads)
+            # calibrate on 20K vectors; CPU throughput falls with n, so the
+            # bounded sample is sized conservatively from that rate
+            cal = ref_cpu_build(cprov, lvf, min(n, 20_000), c["efC"], c["M"], threads)
             if cal is None:
                 out["cpu_baseline"] = None
             else:
-                n_cpu = int(min(n, max(4000, cal[1] * args.cpu_seconds)))
+                n_cpu = int(min(n, max(20_000, 0.5 * cal[1] * args.cpu_seconds)))
                 dt, rate = ref_cpu_build(cprov, lvf, n_cpu, c["efC"], c["M"], threads)
                 out["cpu_baseline"] = {
                     "value": rate, "unit": "vectors/s", "cores": threads, "kind": "reference",

@@ -82,7 +82,7 @@ static int ensure_gvis(fa_index *ix) {
 
 static int pick_hash_log2(int W, int capmax, int R, int mpad, int req) {
     if (req > 0) return req;
-    int want = 8 * W + 2 * capmax;  // the global tier absorbs longer searches
+    int want = 16 * W + 2 * capmax;  // the global tier absorbs longer searches
     int l = 9;
     while ((1 << l) < want && l < 12) ++l;
     // kept ids + codes alias the hash during forward selection
