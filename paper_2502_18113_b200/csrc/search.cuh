@@ -285,6 +285,19 @@ __device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, un
     return lo;
 }
 
+// Warp-cooperative rank (entries of a[0..n) below x, same result in every
+// lane): independent loads + ballots instead of a chain of dependent loads.
+__device__ __forceinline__ int warp_rank(const unsigned long long *a, int n, unsigned long long x,
+                                         int lane) {
+    int r = 0;
+#pragma unroll 4
+    for (int c = 0; c < n; c += 32) {
+        const int i = c + lane;
+        r += __popc(__ballot_sync(0xffffffffu, i < n && a[i] < x));
+    }
+    return r;
+}
+
 // number of entries of the unsorted (small) a[0..n) strictly less than x;
 // every lane reads the same word: shared-memory broadcast
 __device__ __forceinline__ int count_less(const unsigned long long *a, int n, unsigned long long x) {
@@ -299,13 +312,13 @@ __device__ __forceinline__ int count_less(const unsigned long long *a, int n, un
 __device__ __forceinline__ int merge_sorted_into(unsigned long long *T, int &ts,
                                                  const unsigned long long *S, int ns, int lane) {
     if (ns == 0) return ts;
-    const int p0 = lower_rank(T, ts, S[0]);
     int spos[4];  // final slots of S[lane + 32c] (ns <= 128), from the original T
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int j = lane + 32 * c;
         spos[c] = j < ns ? j + lower_rank(T, ts, S[j]) : -1;
     }
+    const int p0 = __shfl_sync(0xffffffffu, spos[0], 0);  // S[0] is the smallest
     if (ts > p0) {
         for (int base = p0 + ((ts - 1 - p0) & ~31); base >= p0; base -= 32) {
             const int i = base + lane;
@@ -313,7 +326,7 @@ __device__ __forceinline__ int merge_sorted_into(unsigned long long *T, int &ts,
             int np = -1;
             if (i < ts) {
                 t = T[i];
-                np = i + lower_rank(S, ns, t);
+                np = i + count_less(S, ns, t);
             }
             __syncwarp();
             if (np >= 0) T[np] = t;
@@ -498,9 +511,9 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
                 const uint32_t wd = key_d(T[W - 1]);
                 if (key_d(s) >= wd) break;
                 // evict the first member of the last distance group
-                const int e = lower_rank(T, ts, (unsigned long long)wd << 32);
+                const int e = warp_rank(T, ts, (unsigned long long)wd << 32, lane);
                 const unsigned long long ev = T[e];
-                const int pos = lower_rank(T, e, s);  // s < ev, so pos <= e
+                const int pos = warp_rank(T, e, s, lane);  // s < ev, so pos <= e
                 __syncwarp();
                 if (lane == 0 && !(ev & 1ull)) TQ[tq_t] = key_id(ev);
                 if (!(ev & 1ull)) ++tq_t;
