@@ -236,13 +236,14 @@ static uint32_t tie_inv(void) {
  * or query), so different insertions break ties differently, as the compiled
  * core's history-dependent heap order does. */
 static uint32_t tie_salt(int tie, uint32_t who) {
-    return tie == 2 ? ((who + 1u) * 0x9E3779B1u) & 0x7fffffffu : 0u;
+    return tie == 2 ? ((who + 1u) * 0x9E3779B1u) & 0xffffffu : 0u;
 }
+/* tie ids are 24-bit bijections of the vertex id (ids < 2^24) */
 static uint32_t tie_fwd(int tie, uint32_t salt, uint32_t u) {
-    return tie ? ((u ^ salt) * TIE_MUL) & 0x7fffffffu : u;
+    return tie ? ((u ^ salt) * TIE_MUL) & 0xffffffu : u;
 }
 static uint32_t tie_back(int tie, uint32_t salt, uint32_t t) {
-    return tie ? ((t * tie_inv()) & 0x7fffffffu) ^ salt : t;
+    return tie ? ((t * tie_inv()) & 0xffffffu) ^ salt : t;
 }
 
 /* Best-first layer search with the semantics of the reference's semantic

@@ -162,7 +162,9 @@ using namespace fa;
 
 extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     FA_CHECK_ARG(desc && out, "null argument");
-    FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 31) - 1, "n=%lld out of range", (long long)desc->n);
+    // search keys carry 24-bit vertex ids (d << 24 | tie id)
+    FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 24), "n=%lld out of range [0, 2^24)",
+                 (long long)desc->n);
     FA_CHECK_ARG(desc->m >= 1 && desc->m <= 128, "m=%d outside [1,128]", desc->m);
     FA_CHECK_ARG(desc->R >= 1, "R must be >= 1");
     FA_CHECK_ARG(2 * desc->R <= 127, "base capacity 2R=%d exceeds 127", 2 * desc->R);

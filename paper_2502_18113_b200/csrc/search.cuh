@@ -52,8 +52,8 @@ struct WarpLayout {
         hash_log2 = hlog2;
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
-        T = o; o += round_up(W, 32) * 8;
-        S = o; o += 256 * 8;  // two 128-key candidate buffers
+        T = o; o += round_up(W, 32) * (8 + 4 + 1);  // results, 32-bit keys, flags
+        S = o; o += 256 * 8;  // candidate buffers
         TQ = o; o += round_up(W, 32) * 4;
         fresh = o; o += round_up(capmax, 32) * 4;
         fdist = o; o += round_up(capmax, 32) * 4;
@@ -260,17 +260,18 @@ __host__ __device__ constexpr uint32_t tie_inverse(uint32_t a) {
 struct TieOrder {
     int mode;
     uint32_t salt;
+    // tie ids are 24 bits (vertex ids < 2^24): keys are (d << 24 | tie id)
     __device__ static TieOrder make(int mode, uint32_t who) {
         TieOrder t;
         t.mode = mode;
-        t.salt = mode == 2 ? ((who + 1u) * 0x9E3779B1u) & 0x7fffffffu : 0u;
+        t.salt = mode == 2 ? ((who + 1u) * 0x9E3779B1u) & 0xffffffu : 0u;
         return t;
     }
     __device__ __forceinline__ uint32_t fwd(uint32_t u) const {
-        return mode ? ((u ^ salt) * kTieMul) & 0x7fffffffu : u;
+        return mode ? ((u ^ salt) * kTieMul) & 0xffffffu : u;
     }
     __device__ __forceinline__ int back(uint32_t t) const {
-        return (int)(mode ? ((t * tie_inverse(kTieMul)) & 0x7fffffffu) ^ salt : t);
+        return (int)(mode ? ((t * tie_inverse(kTieMul)) & 0xffffffu) ^ salt : t);
     }
 };
 
@@ -392,46 +393,92 @@ __device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane,
 //   * an expansion's fresh neighbours are offered in ascending (d, id); one is
 //     accepted while the set is not full or its distance is strictly below the
 //     worst, evicting the worst (largest d, smallest id on ties).
-// Representation: the result set T[0..ts) sorted by (d, id) with an
-// "expanded" bit (bit 0) — its unexpanded members are exactly the frontier
-// entries that can still be popped — plus the tie queue TQ of unexpanded
-// entries evicted at the current worst distance (a popped frontier entry with
-// d > worst stops the search, so nothing else in the frontier can matter).
-// Evictions at one worst distance remove members of the last distance group,
-// so TQ holds < W ids, ascending, and empties when the worst distance drops.
-// On return T[0..ts) is the result ascending by (d, id).  false = hash overflow.
+// Representation (B200): the result set is an UNSORTED array of 32-bit keys
+// (d << 24 | tie id) with an "expanded" byte each.  Pop = warp min-reduction
+// over the unexpanded keys, eviction = min over the largest-distance group,
+// acceptance = an O(1) append or slot replacement; the set is sorted once at
+// the end.  Its unexpanded members are exactly the frontier entries that can
+// still be popped, plus the tie queue TQ of unexpanded entries evicted at the
+// current worst distance (a popped frontier entry with d > worst stops the
+// search, so nothing else in the frontier can matter).  Evictions at one worst
+// distance remove members of the last distance group, so TQ holds < W tie ids,
+// ascending, and empties when the worst distance drops.
+// On return T[0..ts) holds the result as 64-bit keys (make_key of the tie id)
+// ascending by (d, tie id).  false = visited-set overflow.
+__device__ __forceinline__ uint32_t k32(uint32_t d, uint32_t tie) { return (d << 24) | tie; }
+
+// min key over entries with flag == 0 (mask_expanded) or over all entries
+// whose distance equals dsel (dsel < 256); returns (key, index), key = ~0u if none
+__device__ __forceinline__ uint32_t warp_argmin32(const uint32_t *K, const uint8_t *F, int n,
+                                                  int dsel, int lane, int &idx) {
+    uint32_t best = 0xffffffffu;
+    int bi = -1;
+#pragma unroll 4
+    for (int c = 0; c < n; c += 32) {
+        const int i = c + lane;
+        if (i < n) {
+            const uint32_t k = K[i];
+            const bool ok = dsel < 0 ? (F[i] == 0) : ((int)(k >> 24) == dsel);
+            if (ok && k < best) {
+                best = k;
+                bi = i;
+            }
+        }
+    }
+    const uint32_t m = __reduce_min_sync(0xffffffffu, best);
+    const unsigned own = __ballot_sync(0xffffffffu, best == m && bi >= 0);
+    idx = own ? __shfl_sync(0xffffffffu, bi, __ffs(own) - 1) : -1;
+    return m;
+}
+
+__device__ __forceinline__ uint32_t warp_maxd(const uint32_t *K, int n, int lane) {
+    uint32_t mx = 0;
+#pragma unroll 4
+    for (int c = 0; c < n; c += 32) {
+        const int i = c + lane;
+        if (i < n) mx = max(mx, K[i] >> 24);
+    }
+    return __reduce_max_sync(0xffffffffu, mx);
+}
+
 __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
                                     const uint8_t *adt_s, unsigned long long *T, int &ts,
                                     unsigned long long *S, int32_t *TQ, int32_t *fresh,
                                     uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
                                     const TieOrder &to, int lane) {
     const int cap = layer_cap(g, layer);
+    // workspace (WarpLayout::T): 64-bit result slots, then the 32-bit keys, then
+    // the expanded flags, Wp = round_up(W, 32) of each
+    const int Wp = round_up(W, 32);
+    uint32_t *K = reinterpret_cast<uint32_t *>(T + Wp);
+    uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
+    uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
+    uint32_t *Sb = Sa + 128;
     VisitedSet vs;
     vs.H = H;
     vs.hlog2 = hlog2;
     vs.begin(g.gvis, g.gvis_epoch, lane);
     if (lane == 0) {
         vs.visit(entry, true);
-        T[0] = make_key(entry_d, (int)to.fwd((uint32_t)entry));
+        K[0] = k32(entry_d, to.fwd((uint32_t)entry));
+        F[0] = 0;
     }
     vs.hcount = 1;
     ts = 1;
-    int cur = 0;          // T[0..cur) are expanded
-    int tq_h = 0, tq_t = 0;  // tie queue TQ[tq_h..tq_t), distance == worst
-    // speculative id row of the most likely next pop
-    int pre_v = -1;
+    uint32_t wd = 0xffffffffu;  // worst distance once the set is full
+    int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
+    int pre_v = -1;             // speculative id row of the most likely next pop
     int pre[kRowChunks];
     __syncwarp();
     while (true) {
-        // ---- pop the frontier minimum: first unexpanded of T vs tie queue head
-        const int c0 = next_unexpanded(T, ts, cur, lane);
-        cur = c0 >= 0 ? c0 : ts;
-        const unsigned long long kT = c0 >= 0 ? (T[c0] & ~1ull) : KEY_MAX;
-        const uint32_t wd = ts >= W ? key_d(T[W - 1]) : 0xffffffffu;
-        const unsigned long long kQ = tq_h < tq_t ? make_key(wd, TQ[tq_h]) : KEY_MAX;
-        if (kT == KEY_MAX && kQ == KEY_MAX) break;
+        // ---- pop the frontier minimum: unexpanded set member vs tie queue head
+        int ia;
+        const uint32_t kT = warp_argmin32(K, F, ts, -1, lane, ia);
+        const uint32_t kQ = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
+        if (kT == 0xffffffffu && kQ == 0xffffffffu) break;
         const bool fromT = kT < kQ;
-        const int v = to.back((uint32_t)key_id(fromT ? kT : kQ));
+        const uint32_t kpop = fromT ? kT : kQ;
+        const int v = to.back(kpop & 0xffffffu);
         int u[kRowChunks];
         if (v == pre_v) {
 #pragma unroll
@@ -439,20 +486,20 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         } else {
             load_row(row_ids(g, layer, v), cap, lane, u);
         }
-        {  // predict the next pop assuming nothing new enters
-            const int nt = fromT ? next_unexpanded(T, ts, cur + 1, lane) : c0;
-            const unsigned long long k1 = nt >= 0 ? (T[nt] & ~1ull) : KEY_MAX;
-            const int qh = fromT ? tq_h : tq_h + 1;
-            const unsigned long long k2 = qh < tq_t ? make_key(wd, TQ[qh]) : KEY_MAX;
-            const unsigned long long kn = k1 < k2 ? k1 : k2;
-            pre_v = kn != KEY_MAX ? to.back((uint32_t)key_id(kn)) : -1;
-            if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
-        }
         __syncwarp();
         if (fromT) {
-            if (lane == 0) T[cur] |= 1ull;
+            if (lane == 0) F[ia] = 1;
         } else {
             ++tq_h;
+        }
+        __syncwarp();
+        {  // predict the next pop assuming nothing new enters
+            int ib;
+            const uint32_t k1 = warp_argmin32(K, F, ts, -1, lane, ib);
+            const uint32_t k2 = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
+            const uint32_t kn = k1 < k2 ? k1 : k2;
+            pre_v = kn != 0xffffffffu ? to.back(kn & 0xffffffu) : -1;
+            if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
         cnt.visited++;
         const bool to_shared = vs.hcount + cap <= vs.hlimit;
@@ -479,53 +526,77 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         __syncwarp();
         if (nf == 0) continue;
         dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
-        // candidates that can possibly enter: all while T is not full, else
-        // d < worst; sorted ascending by (d, id) through their ranks
-        unsigned long long *Sa = S, *Sb = S + 128;
-        const uint32_t wd0 = ts >= W ? key_d(T[W - 1]) : 0xffffffffu;
+        // candidates that can possibly enter: all while the set is not full,
+        // else d < worst
         int ns = 0;
         for (int base = 0; base < nf; base += 32) {
             const int f = base + lane;
-            const bool ok = f < nf && fdist[f] < wd0;
+            const bool ok = f < nf && fdist[f] < wd;
             const unsigned b = __ballot_sync(0xffffffffu, ok);
             if (ok)
                 Sa[ns + __popc(b & ((1u << lane) - 1u))] =
-                    make_key(fdist[f], (int)to.fwd((uint32_t)fresh[f]));
+                    k32(fdist[f], to.fwd((uint32_t)fresh[f]));
             ns += __popc(b);
         }
         __syncwarp();
         if (ns == 0) continue;
+        const int nfill = min(ns, W - ts);
+        if (nfill == ns) {
+            // everything fits: append (no order needed)
+            for (int j = lane; j < ns; j += 32) {
+                K[ts + j] = Sa[j];
+                F[ts + j] = 0;
+            }
+            ts += ns;
+            __syncwarp();
+            if (ts == W) wd = warp_maxd(K, ts, lane);
+            continue;
+        }
+        // offers are processed in ascending order: rank-sort them
         for (int j = lane; j < ns; j += 32) {
-            const unsigned long long k = Sa[j];
-            Sb[count_less(Sa, ns, k)] = k;
+            const uint32_t k = Sa[j];
+            int r = 0;
+            for (int t = 0; t < ns; ++t) r += Sa[t] < k;
+            Sb[r] = k;
         }
         __syncwarp();
-        // offer them in order; the accepted ones form a prefix.  While T is
-        // not full every offer is accepted without eviction: merge that part
-        // in one pass.
-        const int nfill = min(ns, W - ts);
-        if (nfill > 0) cur = min(cur, merge_sorted_into(T, ts, Sb, nfill, lane));
+        for (int j = lane; j < nfill; j += 32) {
+            K[ts + j] = Sb[j];
+            F[ts + j] = 0;
+        }
+        ts += nfill;
+        __syncwarp();
+        wd = warp_maxd(K, ts, lane);
         for (int j = nfill; j < ns; ++j) {
-            const unsigned long long s = Sb[j];
-            {
-                const uint32_t wd = key_d(T[W - 1]);
-                if (key_d(s) >= wd) break;
-                // evict the first member of the last distance group
-                const int e = warp_rank(T, ts, (unsigned long long)wd << 32, lane);
-                const unsigned long long ev = T[e];
-                const int pos = warp_rank(T, e, s, lane);  // s < ev, so pos <= e
-                __syncwarp();
-                if (lane == 0 && !(ev & 1ull)) TQ[tq_t] = key_id(ev);
-                if (!(ev & 1ull)) ++tq_t;
-                shift_right1(T, pos, e, lane);  // T[e] (the evicted) is overwritten
-                if (lane == 0) T[pos] = s;
-                __syncwarp();
-                cur = min(cur, pos);
-                if (key_d(T[W - 1]) < wd) tq_h = tq_t = 0;  // worst dropped: ties are gone
+            const uint32_t s = Sb[j];
+            if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+            int e;
+            const uint32_t ev = warp_argmin32(K, F, ts, (int)wd, lane, e);
+            if (!F[e]) {
+                if (lane == 0) TQ[tq_t] = (int32_t)(ev & 0xffffffu);
+                ++tq_t;
             }
             __syncwarp();
+            if (lane == 0) {
+                K[e] = s;
+                F[e] = 0;
+            }
+            __syncwarp();
+            const uint32_t nwd = warp_maxd(K, ts, lane);
+            if (nwd < wd) {
+                wd = nwd;
+                tq_h = tq_t = 0;  // the evicted ties are beyond the new worst
+            }
         }
     }
+    // sort the keys once: rank by counting (keys are distinct) into the 64-bit slots
+    for (int i = lane; i < ts; i += 32) {
+        const uint32_t k = K[i];
+        int r = 0;
+        for (int t = 0; t < ts; ++t) r += K[t] < k;
+        T[r] = make_key(k >> 24, (int)(k & 0xffffffu));
+    }
+    __syncwarp();
     return true;
 }
 
