@@ -157,8 +157,10 @@ typedef struct {
                              0 vertex id (reference semantic core, _pycore.py),
                              1 fixed id scramble, 2 scramble salted per
                              inserted vertex (default of the Python layer)     */
-    int64_t *point_stats; /* optional DEVICE n x 2: expansions, SM cycles of
-                             each vertex's insertion search (diagnostics)      */
+    int64_t *point_stats; /* optional DEVICE n x 8 per inserted vertex
+                             (diagnostics): expansions, SM cycles, cycles in
+                             pop / row+visited / distances / acceptance,
+                             forward-selection cycles, distance evaluations   */
 } fa_build_opts;
 
 typedef struct {

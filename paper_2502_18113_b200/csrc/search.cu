@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
     load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
     __syncwarp();
-    SearchCounters cnt = {0, 0, 0, 0};
+    SearchCounters cnt = {};
     const int level = __ldg(g.levels + x);
     int cur = ep;
     uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
     unsigned long long *myreq = req + __ldg(req_off + p);
     int32_t *kept = reinterpret_cast<int32_t *>(ws.H);
     uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
+    long long sel_cycles = 0;
     for (int layer = top; layer >= 0; --layer) {
         int ts = 0;
         bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
         }
         unsigned long long sym = 0;
         const unsigned long long *T = ws.T;
+        const long long t_sel = clock64();
         int nsel = warp_select_heur(
             sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
             [&](int j, int &v, double &dv) {
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
             },
             kept, kcodes, lane, &sym);
         cnt.sym += sym;
+        sel_cycles += clock64() - t_sel;
         // forward row of x (write_forward, _core.pyx:424-438); rows past the
         // live count keep -1 so readers need only the id row
         int32_t *row = const_cast<int32_t *>(row_ids(g, layer, x));
@@ -118,8 +121,12 @@ __global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
         __syncwarp();
     }
     if (stats && lane == 0) {
-        stats[2 * (int64_t)x] = (int64_t)cnt.visited;
-        stats[2 * (int64_t)x + 1] = clock64() - t_begin;
+        int64_t *st = stats + 8 * (int64_t)x;
+        st[0] = (int64_t)cnt.visited;
+        st[1] = clock64() - t_begin;
+        for (int k = 0; k < 4; ++k) st[2 + k] = (int64_t)cnt.ph[k];
+        st[6] = sel_cycles;
+        st[7] = (int64_t)cnt.dist;
     }
     flush_counters(cnt, ctr, lane);
 }
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();
-    SearchCounters cnt = {0, 0, 0, 0};
+    SearchCounters cnt = {};
     int cur = ep;
     uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
     cnt.dist += 1;
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();
-    SearchCounters cnt = {0, 0, 0, 0};
+    SearchCounters cnt = {};
     const int entry = (int)entries[q];
     uint32_t d0 = adt_one(ws.adt, g.codes + (size_t)entry * g.mpad, g.mpad, lane);
     cnt.dist += 1;

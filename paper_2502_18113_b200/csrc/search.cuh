@@ -358,7 +358,16 @@ __device__ __forceinline__ void shift_right1(unsigned long long *T, int lo, int 
 
 struct SearchCounters {
     unsigned long long dist, kcalls, visited, sym;
+    // SM cycles per phase of layer_search (diagnostics, point_stats):
+    // 0 pop + prediction, 1 row + visited filter, 2 distances, 3 acceptance
+    unsigned long long ph[4];
 };
+
+__device__ __forceinline__ void phase_mark(SearchCounters &c, int k, long long &t) {
+    const long long now = clock64();
+    c.ph[k] += (unsigned long long)(now - t);
+    t = now;
+}
 
 // Warp-cooperative best-first search on one layer.
 // On return T[0..ts) holds the result ascending by (d, id).
@@ -469,9 +478,11 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
     int pre_v = -1;             // speculative id row of the most likely next pop
     int pre[kRowChunks];
+    long long tph = clock64();
     __syncwarp();
     while (true) {
         // ---- pop the frontier minimum: unexpanded set member vs tie queue head
+        phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
         int ia;
         const uint32_t kT = warp_argmin32(K, F, ts, -1, lane, ia);
         const uint32_t kQ = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
@@ -502,6 +513,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
         cnt.visited++;
+        phase_mark(cnt, 0, tph);
         const bool to_shared = vs.hcount + cap <= vs.hlimit;
         if (!to_shared && (vs.G == nullptr || vs.gcount + cap > vs.glimit)) return false;
         // visited filter over the row, compacted in slot order
@@ -524,8 +536,10 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         cnt.kcalls += (nlive + 15) >> 4;
         cnt.dist += nf;
         __syncwarp();
+        phase_mark(cnt, 1, tph);
         if (nf == 0) continue;
         dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
+        phase_mark(cnt, 2, tph);
         // candidates that can possibly enter: all while the set is not full,
         // else d < worst
         int ns = 0;

@@ -48,7 +48,7 @@ def main():
         over["batch_max"] = args.bmax
     if args.tie is not None:
         over["tie"] = args.tie
-    stats = torch.zeros((args.n, 2), dtype=torch.int64, device="cuda")
+    stats = torch.zeros((args.n, 8), dtype=torch.int64, device="cuda")
     for r in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -76,6 +76,11 @@ def main():
         "kcycles": {"mean": float(cyc.mean() / 1e3), **{f"p{p}": float(np.percentile(cyc, p) / 1e3)
                                                         for p in q}},
         "cycles_per_expansion": float(cyc.sum() / max(exp.sum(), 1)),
+        "phase_cycles_per_expansion": {
+            name: float(st[:, 2 + i].sum() / max(exp.sum(), 1))
+            for i, name in enumerate(["pop", "row_visit", "dists", "accept"])},
+        "select_cycles_per_insert": float(st[:, 6].mean()),
+        "dist_per_expansion": float(st[:, 7].sum() / max(exp.sum(), 1)),
     }))
 
 
