@@ -157,6 +157,8 @@ typedef struct {
                              0 vertex id (reference semantic core, _pycore.py),
                              1 fixed id scramble, 2 scramble salted per
                              inserted vertex (default of the Python layer)     */
+    int expand;           /* frontier entries expanded per search step during
+                             insertion (<= 1: one, the semantic core; max 8)  */
     int64_t *point_stats; /* optional DEVICE n x 8 per inserted vertex
                              (diagnostics): expansions, SM cycles, cycles in
                              pop / row+visited / distances / acceptance,

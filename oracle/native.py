@@ -30,7 +30,7 @@ class Graph(C.Structure):
     _fields_ = [("n", i64), ("nU", i64), ("m", C.c_int), ("cs", C.c_int), ("cap0", C.c_int),
                 ("capU", C.c_int), ("adj0", vp), ("cnt0", vp), ("adjU", vp), ("cntU", vp),
                 ("codes", vp), ("levels", vp), ("uoff", vp), ("upper_owner", vp),
-                ("tie", C.c_int)]
+                ("tie", C.c_int), ("expand", C.c_int)]
 
 
 class BuildResult(C.Structure):
@@ -162,7 +162,7 @@ def schedule(levels, batch_max, batch_frac, seq_prefix):
 class HostGraph:
     """Host graph in the device's logical layout (exact-cap id rows + counts)."""
 
-    def __init__(self, levels, upper_offsets, R, m, codes=None, tie=0):
+    def __init__(self, levels, upper_offsets, R, m, codes=None, tie=0, expand=1):
         self.levels = _c(levels, np.int32)
         self.uoff = _c(upper_offsets, np.int64)
         self.n = self.levels.shape[0]
@@ -181,7 +181,8 @@ class HostGraph:
         self.owner = owner
         self.s = Graph(self.n, self.nU, self.m, self.m, self.cap0, self.capU, _p(self.adj0),
                        _p(self.cnt0), _p(self.adjU), _p(self.cntU), _p(self.codes),
-                       _p(self.levels), _p(self.uoff), _p(self.owner), int(tie))
+                       _p(self.levels), _p(self.uoff), _p(self.owner), int(tie),
+                       int(expand))
 
     @classmethod
     def from_blocks(cls, levels, upper_offsets, base_blocks, upper_blocks, R, codes):

@@ -267,23 +267,35 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
     int nf = 0, nr = 0;
     heap_push_min(s->fr, &nf, ((uint64_t)entry_d << 32) | tie_fwd(tie, s->salt, (uint32_t)entry));
     heap_push_max(s->rs, &nr, rkey((uint64_t)entry_d, tie_fwd(tie, s->salt, (uint32_t)entry)));
+    /* E > 1: pop up to E poppable frontier entries per step and expand them
+     * together (a beam-search variant used for batched construction; E = 1 is
+     * exactly the semantic core).  Poppable = d <= worst once the set is full. */
+    const int E = g->expand > 1 ? g->expand : 1;
     while (nf > 0) {
-        uint64_t top = heap_pop_min(s->fr, &nf);
-        uint64_t d = top >> 32;
-        int v = (int)tie_back(tie, s->salt, (uint32_t)top);
-        if (nr >= W && d > (s->rs[0] >> 32)) break;
-        if (c) c->visited++;
-        int32_t *ids = row_of(g, layer, v);
-        int cnt = *cnt_of(g, layer, v);
-        if (cnt > cap) cnt = cap;
-        if (c) c->kernel_calls += (cnt + 15) >> 4;
+        int pops[64];
+        int npop = 0;
+        while (npop < E && nf > 0) {
+            uint64_t d = s->fr[0] >> 32;
+            if (nr >= W && d > (s->rs[0] >> 32)) break;
+            uint64_t top = heap_pop_min(s->fr, &nf);
+            pops[npop++] = (int)tie_back(tie, s->salt, (uint32_t)top);
+        }
+        if (npop == 0) break;
         int nfresh = 0;
-        for (int j = 0; j < cnt; ++j) {
-            int u = ids[j];
-            if (u < 0 || s->visited[u] == ep) continue;
-            s->visited[u] = ep;
-            uint64_t du = (uint64_t)adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
-            s->fresh[nfresh++] = (du << 32) | tie_fwd(tie, s->salt, (uint32_t)u);
+        for (int pi = 0; pi < npop; ++pi) {
+            int v = pops[pi];
+            if (c) c->visited++;
+            int32_t *ids = row_of(g, layer, v);
+            int cnt = *cnt_of(g, layer, v);
+            if (cnt > cap) cnt = cap;
+            if (c) c->kernel_calls += (cnt + 15) >> 4;
+            for (int j = 0; j < cnt; ++j) {
+                int u = ids[j];
+                if (u < 0 || s->visited[u] == ep) continue;
+                s->visited[u] = ep;
+                uint64_t du = (uint64_t)adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+                s->fresh[nfresh++] = (du << 32) | tie_fwd(tie, s->salt, (uint32_t)u);
+            }
         }
         if (c) c->dist_comps += nfresh;
         qsort(s->fresh, (size_t)nfresh, sizeof(uint64_t), cmp_u64);
@@ -346,7 +358,7 @@ static int scratch_init(scratch *s, int64_t n, int W, int capmax) {
     s->fr_cap = (size_t)(n > 0 ? n : 1) + 2;  /* each vertex is pushed at most once */
     s->fr = (uint64_t *)malloc(sizeof(uint64_t) * s->fr_cap);
     s->rs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 2));
-    s->fresh = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 8));
+    s->fresh = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(64 * capmax + 8));
     s->epoch = 0;
     s->salt = 0;
     return (s->visited && s->fr && s->rs && s->fresh) ? 0 : -1;

@@ -22,6 +22,7 @@ typedef struct {
     const int64_t *uoff;
     const int32_t *upper_owner; /* nU: vertex owning each upper row */
     int tie;                    /* 0: ties by id; 1: by the scrambled id    */
+    int expand;                 /* frontier entries expanded per step (<=1: 1) */
 } or_graph;
 
 typedef struct {

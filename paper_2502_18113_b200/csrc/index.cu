@@ -198,6 +198,7 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.adj0 = ix->adj0; g.cnt0 = ix->cnt0; g.cons0 = ix->cons0;
     g.adjU = ix->adjU; g.cntU = ix->cntU; g.consU = ix->consU;
     g.tie = 0;
+    g.expand = 1;
     g.gvis = nullptr;
     g.gvis_epoch = nullptr;
     // host copies of the layer draws drive the batch schedule
@@ -318,6 +319,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CHECK_ARG(opts->tie >= 0 && opts->tie <= 2, "tie mode must be 0, 1 or 2");
     Graph gb = g;  // the build's view: its own tie order
     gb.tie = opts->tie;
+    gb.expand = opts->expand > 1 ? std::min(opts->expand, kMaxExpand) : 1;
     if (g.n == 0) {
         ix->entry = -1;
         ix->max_layer = -1;
@@ -370,7 +372,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // ---- scratch ----
     const int capmax = std::max(g.cap0, g.capU);
     WarpLayout L;
-    L.init(g.mpad, C, capmax, pick_hash_log2(C, capmax, R, g.mpad, opts->hash_log2));
+    L.init(g.mpad, C, capmax,
+           pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2),
+           gb.expand);
     const size_t sdt_bytes = round_up(g.m * 256, 128);
     const size_t smem_search = sdt_bytes + (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
@@ -552,7 +556,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
-    L.init(ix->g.mpad, ef, capmax, pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0));
+    L.init(ix->g.mpad, ef, capmax, pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0), 1);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
     FA_CUDA(cudaFuncSetAttribute(query_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -571,6 +575,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
         int grid = (nq + kSearchWarps - 1) / kSearchWarps;
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
+        gq.expand = 1;
         query_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
             gq, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
             queries, L, out_ids, out_d, ctr, err);
@@ -609,7 +614,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
-    L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0));
+    L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
     FA_CUDA(cudaFuncSetAttribute(layer_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,6 +633,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
         int grid = (nq + kSearchWarps - 1) / kSearchWarps;
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
+        gq.expand = 1;
         layer_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
             gq, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
         cudaError_t e = cudaGetLastError();

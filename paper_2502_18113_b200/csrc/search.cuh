@@ -30,10 +30,22 @@ struct Graph {
     const int32_t *levels;
     const int64_t *uoff;
     int64_t nU;
-    int tie;  // tie order of the searches (TieOrder modes)
+    int tie;     // tie order of the searches (TieOrder modes)
+    int expand;  // frontier entries expanded per step (1 = semantic core)
     uint32_t *gvis;        // global visited tables, one per SM warp slot (or null)
     uint32_t *gvis_epoch;  // their epoch counters
 };
+
+constexpr int kMaxExpand = 8;
+
+// candidate slots one search step can produce: E rows of up to cap ids
+__host__ __device__ inline int cand_capacity(int expand, int capmax) {
+    const int e = expand > 1 ? (expand < kMaxExpand ? expand : kMaxExpand) : 1;
+    return e * round_up(capmax, 32);
+}
+__host__ __device__ inline int cand_capacity(const Graph &g) {
+    return cand_capacity(g.expand, g.cap0 > g.capU ? g.cap0 : g.capU);
+}
 
 __device__ __forceinline__ const int32_t *row_ids(const Graph &g, int layer, int v) {
     if (layer == 0) return g.adj0 + (int64_t)v * g.cap0p;
@@ -48,15 +60,16 @@ struct WarpLayout {
     int adt, T, S, TQ, fresh, fdist, hash, total;
     int hash_log2;
     __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
-    __host__ __device__ void init(int mpad, int W, int capmax, int hlog2) {
+    __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand) {
         hash_log2 = hlog2;
+        const int nc = cand_capacity(expand, capmax);
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
         T = o; o += round_up(W, 32) * (8 + 4 + 1);  // results, 32-bit keys, flags
-        S = o; o += 256 * 8;  // candidate buffers
+        S = o; o += 2 * nc * 4;                     // candidate keys (two buffers)
         TQ = o; o += round_up(W, 32) * 4;
-        fresh = o; o += round_up(capmax, 32) * 4;
-        fdist = o; o += round_up(capmax, 32) * 4;
+        fresh = o; o += nc * 4;
+        fdist = o; o += nc * 4;
         hash = o; o += (4 << hlog2);
         total = round_up(o, 128);
     }
@@ -462,7 +475,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     uint32_t *K = reinterpret_cast<uint32_t *>(T + Wp);
     uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
     uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
-    uint32_t *Sb = Sa + 128;
+    uint32_t *Sb = Sa + cand_capacity(g);
     VisitedSet vs;
     vs.H = H;
     vs.hlog2 = hlog2;
@@ -476,35 +489,51 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     ts = 1;
     uint32_t wd = 0xffffffffu;  // worst distance once the set is full
     int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
-    int pre_v = -1;             // speculative id row of the most likely next pop
+    int pre_v = -1;             // speculative id row of the most likely next pop (E == 1)
     int pre[kRowChunks];
+    // frontier entries expanded per step: 1 = the semantic core; E > 1 pops the
+    // E smallest poppable entries and expands them together (oracle: expand)
+    const int E = g.expand > 1 ? min(g.expand, kMaxExpand) : 1;
     long long tph = clock64();
     __syncwarp();
     while (true) {
-        // ---- pop the frontier minimum: unexpanded set member vs tie queue head
         phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
-        int ia;
-        const uint32_t kT = warp_argmin32(K, F, ts, -1, lane, ia);
-        const uint32_t kQ = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
-        if (kT == 0xffffffffu && kQ == 0xffffffffu) break;
-        const bool fromT = kT < kQ;
-        const uint32_t kpop = fromT ? kT : kQ;
-        const int v = to.back(kpop & 0xffffffu);
-        int u[kRowChunks];
-        if (v == pre_v) {
+        // ---- pop up to E frontier minima: unexpanded set members vs tie queue
+        int pv[kMaxExpand];
+        int npop = 0;
 #pragma unroll
-            for (int k = 0; k < kRowChunks; ++k) u[k] = pre[k];
-        } else {
-            load_row(row_ids(g, layer, v), cap, lane, u);
+        for (int r = 0; r < kMaxExpand; ++r) {
+            if (r >= E) break;
+            int ia;
+            const uint32_t kT = warp_argmin32(K, F, ts, -1, lane, ia);
+            const uint32_t kQ = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
+            if (kT == 0xffffffffu && kQ == 0xffffffffu) break;
+            const bool fromT = kT < kQ;
+            pv[r] = to.back((fromT ? kT : kQ) & 0xffffffu);
+            ++npop;
+            __syncwarp();
+            if (fromT) {
+                if (lane == 0) F[ia] = 1;
+            } else {
+                ++tq_h;
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        if (fromT) {
-            if (lane == 0) F[ia] = 1;
-        } else {
-            ++tq_h;
+        if (npop == 0) break;
+        // id rows of the popped vertices, all loads in flight together
+        int u[kMaxExpand][kRowChunks];
+#pragma unroll
+        for (int r = 0; r < kMaxExpand; ++r) {
+            if (r < npop) {
+                if (E == 1 && pv[0] == pre_v) {
+#pragma unroll
+                    for (int k = 0; k < kRowChunks; ++k) u[0][k] = pre[k];
+                } else {
+                    load_row(row_ids(g, layer, pv[r]), cap, lane, u[r]);
+                }
+            }
         }
-        __syncwarp();
-        {  // predict the next pop assuming nothing new enters
+        if (E == 1) {  // predict the next pop assuming nothing new enters
             int ib;
             const uint32_t k1 = warp_argmin32(K, F, ts, -1, lane, ib);
             const uint32_t k2 = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
@@ -512,28 +541,33 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
             pre_v = kn != 0xffffffffu ? to.back(kn & 0xffffffu) : -1;
             if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
-        cnt.visited++;
+        cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        const bool to_shared = vs.hcount + cap <= vs.hlimit;
-        if (!to_shared && (vs.G == nullptr || vs.gcount + cap > vs.glimit)) return false;
-        // visited filter over the row, compacted in slot order
-        int nf = 0, nlive = 0;
+        const bool to_shared = vs.hcount + npop * cap <= vs.hlimit;
+        if (!to_shared && (vs.G == nullptr || vs.gcount + npop * cap > vs.glimit)) return false;
+        // visited filter over the rows (pop order, slot order), compacted
+        int nf = 0;
 #pragma unroll
-        for (int k = 0; k < kRowChunks; ++k) {
-            if (k * 32 >= cap) break;
-            const int x = u[k];
-            bool live = x >= 0;
-            const int r = live ? vs.visit(x, to_shared) : 0;
-            const bool fr = r != 0;
-            unsigned bl = __ballot_sync(0xffffffffu, live);
-            unsigned bf = __ballot_sync(0xffffffffu, fr);
-            if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
-            nf += __popc(bf);
-            nlive += __popc(bl);
-            vs.hcount += __popc(__ballot_sync(0xffffffffu, r == 1));
-            vs.gcount += __popc(__ballot_sync(0xffffffffu, r == 2));
+        for (int r = 0; r < kMaxExpand; ++r) {
+            if (r >= npop) break;
+            int nlive = 0;
+#pragma unroll
+            for (int k = 0; k < kRowChunks; ++k) {
+                if (k * 32 >= cap) break;
+                const int x = u[r][k];
+                bool live = x >= 0;
+                const int rr = live ? vs.visit(x, to_shared) : 0;
+                const bool fr = rr != 0;
+                unsigned bl = __ballot_sync(0xffffffffu, live);
+                unsigned bf = __ballot_sync(0xffffffffu, fr);
+                if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
+                nf += __popc(bf);
+                nlive += __popc(bl);
+                vs.hcount += __popc(__ballot_sync(0xffffffffu, rr == 1));
+                vs.gcount += __popc(__ballot_sync(0xffffffffu, rr == 2));
+            }
+            cnt.kcalls += (nlive + 15) >> 4;
         }
-        cnt.kcalls += (nlive + 15) >> 4;
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);

@@ -46,6 +46,9 @@ BUILD_OPTIONS = {
     # scramble salted per inserted vertex; 0 reproduces
     # the reference's semantic core (_pycore) exactly
     "tie": int(os.environ.get("FLASHANN_B200_TIE", "2")),
+    # frontier entries expanded together per search step during insertion
+    # (1 = the semantic core)
+    "expand": int(os.environ.get("FLASHANN_B200_EXPAND", "4")),
     "profile": 0,
 }
 
@@ -82,7 +85,8 @@ def build_options(C_: int) -> _lib.BuildOpts:
     o = BUILD_OPTIONS
     return _lib.BuildOpts(C=C_, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
                           seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
-                          profile=o.get("profile", 0), tie=o.get("tie", 2))
+                          profile=o.get("profile", 0), tie=o.get("tie", 2),
+                          expand=o.get("expand", 1))
 
 
 def _prov_arrays(prov: dict):

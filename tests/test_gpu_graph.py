@@ -96,9 +96,10 @@ SCHEDULES = {
 }
 
 
-@pytest.mark.parametrize("tie", [0, 1, 2])
+@pytest.mark.parametrize("expand", [1, 4, 8])
+@pytest.mark.parametrize("tie", [0, 2])
 @pytest.mark.parametrize("sched", list(SCHEDULES))
-def test_batched_build_matches_oracle(core, golden, sched, tie):
+def test_batched_build_matches_oracle(core, golden, sched, tie, expand):
     from paper_2502_18113_b200 import layout
 
     g = gi.GRAPH
@@ -109,13 +110,13 @@ def test_batched_build_matches_oracle(core, golden, sched, tie):
     upper = layout.empty_rows(int(levels.sum()), R, m)
     opts = SCHEDULES[sched]
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(opts, hash_log2=0, tie=tie)
+    core.BUILD_OPTIONS.update(opts, hash_log2=0, tie=tie, expand=expand)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, g["C"], R)
     finally:
         core.BUILD_OPTIONS.clear()
         core.BUILD_OPTIONS.update(saved)
-    hg = native.HostGraph(levels, uoff, R, m, tie=tie)
+    hg = native.HostGraph(levels, uoff, R, m, tie=tie, expand=expand)
     ores = hg.build(prov["proj"], prov["cent"], prov["dims"], prov["offs"], prov["dist_min"],
                     prov["delta"], prov["sdt"], g["C"], **opts)
     assert res["entry_point"] == ores["entry_point"]
@@ -167,7 +168,7 @@ def test_sequential_build_matches_semantic_core(core, golden):
     base = layout.empty_rows(pb["n"], 2 * R, m)
     upper = layout.empty_rows(int(levels.sum()), R, m)
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(SCHEDULES["sequential"], tie=0)
+    core.BUILD_OPTIONS.update(SCHEDULES["sequential"], tie=0, expand=1)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, pb["C"], R)
     finally:
