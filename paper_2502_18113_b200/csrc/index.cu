@@ -65,12 +65,26 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
 // Global visited tier (VisitedSet): one 2^kGlobalHashLog2-entry table per
 // hardware warp slot, allocated on first use; absent for n >= 2^24 (the tier
 // packs ids into 24 bits), where the shared tier alone must suffice.
+__global__ void nsmid_kernel(uint32_t *out) {
+    uint32_t v;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+    *out = v;
+}
+
 static int ensure_gvis(fa_index *ix) {
     if (ix->gvis || ix->g.n >= (1ll << 24) - 1) return FA_OK;
-    int dev = 0, sms = 0;
-    FA_CUDA(cudaGetDevice(&dev));
-    FA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t slots = (size_t)sms * kMaxWarpsPerSM;
+    // warp slots are indexed by %smid, which is not dense on parts with fused-off
+    // SMs: size by %nsmid (an upper bound of %smid), not by the SM count
+    uint32_t *d_ns = nullptr, nsmid = 0;
+    FA_TRY(dev_alloc((void **)&d_ns, sizeof(uint32_t)));
+    nsmid_kernel<<<1, 1>>>(d_ns);
+    cudaError_t e = cudaMemcpy(&nsmid, d_ns, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d_ns);
+    if (e != cudaSuccess) {
+        set_error("reading %%nsmid: %s", cudaGetErrorString(e));
+        return FA_ECUDA;
+    }
+    const size_t slots = (size_t)nsmid * kMaxWarpsPerSM;
     FA_TRY(dev_alloc((void **)&ix->gvis, (slots << kGlobalHashLog2) * sizeof(uint32_t)));
     FA_TRY(dev_alloc((void **)&ix->gvis_epoch, slots * sizeof(uint32_t)));
     FA_CUDA(cudaMemset(ix->gvis, 0, (slots << kGlobalHashLog2) * sizeof(uint32_t)));

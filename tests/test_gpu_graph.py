@@ -96,10 +96,12 @@ SCHEDULES = {
 }
 
 
+@pytest.mark.parametrize("hash_log2", [0, 9])
 @pytest.mark.parametrize("expand", [1, 4, 8])
 @pytest.mark.parametrize("tie", [0, 2])
 @pytest.mark.parametrize("sched", list(SCHEDULES))
-def test_batched_build_matches_oracle(core, golden, sched, tie, expand):
+def test_batched_build_matches_oracle(core, golden, sched, tie, expand, hash_log2):
+    """hash_log2 = 9 (512 shared slots) forces the global visited tier."""
     from paper_2502_18113_b200 import layout
 
     g = gi.GRAPH
@@ -110,7 +112,7 @@ def test_batched_build_matches_oracle(core, golden, sched, tie, expand):
     upper = layout.empty_rows(int(levels.sum()), R, m)
     opts = SCHEDULES[sched]
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(opts, hash_log2=0, tie=tie, expand=expand)
+    core.BUILD_OPTIONS.update(opts, hash_log2=hash_log2, tie=tie, expand=expand)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, g["C"], R)
     finally:
