@@ -179,6 +179,7 @@ struct VisitedSet {
     uint32_t *gepoch;  // epoch counter of this warp slot
     uint32_t epoch;
     int gcount, glimit;
+    bool spilled;      // sticky: new ids go to the global tier
 
     __device__ static uint32_t slot_id() {
         uint32_t sm, w;
@@ -190,6 +191,7 @@ struct VisitedSet {
     __device__ void begin(uint32_t *gtables, uint32_t *gepochs, int lane) {
         hash_clear(H, hlog2, lane);
         hcount = 0;
+        spilled = false;
         hlimit = (1 << hlog2) / 2;  // linear probing stays short at load <= 1/2
         gcount = 0;
         glimit = (1 << kGlobalHashLog2) * 3 / 4;
@@ -543,7 +545,10 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        const bool to_shared = vs.hcount + npop * cap <= vs.hlimit;
+        // once a search spills to the global tier it never returns to the shared
+        // one: an id inserted globally must not be re-inserted in shared memory
+        vs.spilled |= vs.hcount + npop * cap > vs.hlimit;
+        const bool to_shared = !vs.spilled;
         if (!to_shared && (vs.G == nullptr || vs.gcount + npop * cap > vs.glimit)) return false;
         // visited filter over the rows (pop order, slot order), compacted
         int nf = 0;
