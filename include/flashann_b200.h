@@ -64,6 +64,12 @@ int fa_scan_select_dev(const uint8_t *adt, int nq, const uint8_t *blocks, int64_
                        int64_t block_stride, int64_t codes_off, int cap, int m,
                        const int32_t *sel, int nsel, uint64_t *out, void *stream);
 
+/* Same scan with the blocks staged by 1-D TMA bulk copies (cp.async.bulk)
+ * into a 4-deep shared-memory ring per warp; identical results.              */
+int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t *blocks, int64_t nblocks,
+                           int64_t block_stride, int64_t codes_off, int cap, int m,
+                           const int32_t *sel, int nsel, uint64_t *out, void *stream);
+
 /* fa_quantize (_simd.h:99-107) elementwise in IEEE double.                   */
 int fa_quantize_dev(const double *d, int64_t n, double dist_min, double delta, uint8_t *out,
                     void *stream);

@@ -57,6 +57,8 @@ _SIGS = {
     "fa_scan_blocks_dev": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
     "fa_scan_select_dev": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, C.c_int, C.c_int, vp,
                                      C.c_int, vp, vp]),
+    "fa_scan_select_tma_dev": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, C.c_int, C.c_int, vp,
+                                         C.c_int, vp, vp]),
     "fa_quantize_dev": (C.c_int, [vp, i64, f64, f64, vp, vp]),
     "fa_l2sq_rows_dev": (C.c_int, [vp, i64, vp, i64, i64, C.c_int, vp, vp]),
     "fa_encode_adt_dev": (C.c_int, [vp, i64, i64, vp, vp, vp, C.c_int, C.c_int, f64, f64, vp,

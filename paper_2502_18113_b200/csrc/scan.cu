@@ -81,9 +81,162 @@ __global__ void __launch_bounds__(256) scan_select_kernel(
     if (lane == 0 && best != ~0ull) atomicMin(out + q, best);
 }
 
+// ---- TMA-staged block scan -------------------------------------------------
+// Each block is one contiguous region, so a 1-D bulk copy (cp.async.bulk,
+// SASS UBLKCP) moves it into a per-warp ring of shared-memory stages; an
+// mbarrier per stage carries the transaction count.  Lane 0 keeps kStages
+// blocks in flight while the warp scans the oldest one from shared memory
+// (lane t reads row t of a batch: 16 contiguous bytes, conflict-free).
+constexpr int kScanStages = 4;
+constexpr int kScanWarps = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
+    const uint8_t *__restrict__ adt, int nq, const uint8_t *__restrict__ blocks,
+    int64_t block_stride, int64_t codes_off, uint32_t copy_bytes, uint32_t stage_bytes, int cap,
+    int m, const int32_t *__restrict__ sel, int nsel, int slices,
+    unsigned long long *__restrict__ out) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + wid * kScanStages;
+    uint8_t *ring = smem + 128 + (size_t)wid * kScanStages * stage_bytes;
+    if (lane == 0) {
+        for (int s = 0; s < kScanStages; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int gw = blockIdx.x * kScanWarps + wid;
+    const int q = gw / slices;
+    const int slice = gw % slices;
+    if (q >= nq) return;
+    WarpTable<NR> tab;
+    tab.load(adt + (size_t)q * m * 16, m, lane);
+    const int nb = (cap + 15) >> 4;
+    const int per = (nsel + slices - 1) / slices;
+    const int lo = slice * per;
+    const int hi = min(nsel, lo + per);
+    const int nblk = max(0, hi - lo);
+    const int32_t *qsel = sel + (size_t)q * nsel + lo;
+    if (lane == 0)
+        for (int s = 0; s < kScanStages && s < nblk; ++s) {
+            mbar_expect_tx(bars + s, copy_bytes);
+            bulk_g2s(ring + (size_t)s * stage_bytes, blocks + (int64_t)__ldg(qsel + s) * block_stride,
+                     copy_bytes, bars + s);
+        }
+    unsigned long long best = ~0ull;
+    for (int i = 0; i < nblk; ++i) {
+        const int st = i % kScanStages;
+        mbar_wait(bars + st, (uint32_t)((i / kScanStages) & 1));
+        const uint8_t *blk = ring + (size_t)st * stage_bytes;
+        const int cnt = min(*reinterpret_cast<const int32_t *>(blk), cap);
+        const int32_t *ids = reinterpret_cast<const int32_t *>(blk + 16);
+        const uint8_t *cod = blk + codes_off;
+        for (int b = 0; b < nb; ++b) {
+            uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int r = lane + 32 * k;
+                if (r < m)
+                    acc_row(tab.t[k], *reinterpret_cast<const uint4 *>(cod + (size_t)b * m * 16 + r * 16),
+                            acc);
+            }
+            const uint32_t v = reduce_batch(acc, lane);
+            const int slot = b * 16 + slot_of_lane(lane);
+            if ((lane & 2) == 0 && slot < cnt) {
+                const int id = ids[slot];
+                if (id >= 0) {
+                    const unsigned long long key = ((unsigned long long)v << 32) | (uint32_t)id;
+                    best = key < best ? key : best;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && i + kScanStages < nblk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bars + st, copy_bytes);
+            bulk_g2s(ring + (size_t)st * stage_bytes,
+                     blocks + (int64_t)__ldg(qsel + i + kScanStages) * block_stride, copy_bytes,
+                     bars + st);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other < best ? other : best;
+    }
+    if (lane == 0 && best != ~0ull) atomicMin(out + q, best);
+}
+
 }  // namespace fa
 
 using namespace fa;
+
+extern "C" int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t *blocks,
+                                      int64_t nblocks, int64_t block_stride, int64_t codes_off,
+                                      int cap, int m, const int32_t *sel, int nsel,
+                                      uint64_t *out_u64, void *stream) {
+    FA_CHECK_ARG(m >= 1 && m <= 128, "m=%d outside [1,128]", m);
+    FA_CHECK_ARG(codes_off % 16 == 0 && block_stride % 16 == 0, "block layout must be 16B aligned");
+    FA_CHECK_ARG(nq >= 0 && nsel >= 0 && nblocks >= 0, "negative sizes");
+    if (nq == 0) return FA_OK;
+    cudaStream_t st = as_stream(stream);
+    unsigned long long *out = reinterpret_cast<unsigned long long *>(out_u64);
+    FA_CUDA(cudaMemsetAsync(out, 0xff, sizeof(unsigned long long) * nq, st));
+    const int nb = (cap + 15) / 16;
+    const uint32_t copy_bytes = (uint32_t)round_up64(codes_off + (int64_t)nb * m * 16, 16);
+    FA_CHECK_ARG(copy_bytes <= (uint32_t)block_stride, "block stride smaller than its contents");
+    const uint32_t stage_bytes = (uint32_t)round_up64(copy_bytes, 128);
+    const size_t smem = 128 + (size_t)kScanWarps * kScanStages * stage_bytes;
+    FA_CHECK_ARG(smem <= 227 * 1024, "block too large for the staged scan");
+    int slices = 1;
+    while ((int64_t)nq * slices < 148 * 16 && slices * 8 <= nsel) slices *= 2;
+    const int64_t warps = (int64_t)nq * slices;
+    const int grid = (int)((warps + kScanWarps - 1) / kScanWarps);
+#define FA_TMA_LAUNCH(NR_)                                                                  \
+    do {                                                                                    \
+        FA_CUDA(cudaFuncSetAttribute(scan_select_tma_kernel<NR_>,                           \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        scan_select_tma_kernel<NR_><<<grid, kScanWarps * 32, smem, st>>>(                   \
+            adt, nq, blocks, block_stride, codes_off, copy_bytes, stage_bytes, cap, m, sel,  \
+            nsel, slices, out);                                                             \
+    } while (0)
+    if (m <= 32) FA_TMA_LAUNCH(1);
+    else if (m <= 64) FA_TMA_LAUNCH(2);
+    else if (m <= 96) FA_TMA_LAUNCH(3);
+    else FA_TMA_LAUNCH(4);
+#undef FA_TMA_LAUNCH
+    FA_LAUNCH_CHECK();
+    return FA_OK;
+}
 
 extern "C" int fa_scan_cases_dev(const uint8_t *adts, const uint8_t *codes, int m, int64_t ncases,
                                  uint8_t *out, void *stream) {
