@@ -65,7 +65,7 @@ int fa_scan_select_dev(const uint8_t *adt, int nq, const uint8_t *blocks, int64_
                        const int32_t *sel, int nsel, uint64_t *out, void *stream);
 
 /* Same scan with the blocks staged by 1-D TMA bulk copies (cp.async.bulk)
- * into a 4-deep shared-memory ring per warp; identical results.              */
+ * into a 2-deep shared-memory ring per warp; identical results.              */
 int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t *blocks, int64_t nblocks,
                            int64_t block_stride, int64_t codes_off, int cap, int m,
                            const int32_t *sel, int nsel, uint64_t *out, void *stream);

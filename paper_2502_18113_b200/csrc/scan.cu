@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(256) scan_select_kernel(
 // mbarrier per stage carries the transaction count.  Lane 0 keeps kStages
 // blocks in flight while the warp scans the oldest one from shared memory
 // (lane t reads row t of a batch: 16 contiguous bytes, conflict-free).
-constexpr int kScanStages = 4;
-constexpr int kScanWarps = 4;
+constexpr int kScanStages = 2;
+constexpr int kScanWarps = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -218,7 +218,7 @@ extern "C" int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t 
     const size_t smem = 128 + (size_t)kScanWarps * kScanStages * stage_bytes;
     FA_CHECK_ARG(smem <= 227 * 1024, "block too large for the staged scan");
     int slices = 1;
-    while ((int64_t)nq * slices < 148 * 16 && slices * 8 <= nsel) slices *= 2;
+    while ((int64_t)nq * slices < 148 * 96 && slices * 16 <= nsel) slices *= 2;
     const int64_t warps = (int64_t)nq * slices;
     const int grid = (int)((warps + kScanWarps - 1) / kScanWarps);
 #define FA_TMA_LAUNCH(NR_)                                                                  \
