@@ -405,6 +405,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, reverse_kernel,
                                                           kReverseWarps * 32, smem_rev));
     const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * kNumSMs;
+    int search_per_sm = 0;
+    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, build_search_kernel,
+                                                          kSearchWarps * 32, smem_search));
+    const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * kNumSMs;
 
     uint8_t *adt_batch = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
@@ -432,7 +436,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&ctr, sizeof(unsigned long long) * 8)) ||
         (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
         (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
-        (rc = dev_alloc((void **)&nheads, sizeof(int))) ||
+        (rc = dev_alloc((void **)&nheads, 2 * sizeof(int))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
         (rc = dev_alloc((void **)&err, sizeof(int)))) {
         cleanup();
@@ -476,17 +480,18 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             return rc;
         }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
-        int grid = (b.size + kSearchWarps - 1) / kSearchWarps;
+        // nheads[0]: reverse row heads, nheads[1]: the search's work counter
+        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), st));
+        int grid = (int)std::min<int64_t>(search_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
         build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
             gb, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
-            req, ctr, err, opts->point_stats);
+            req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         size_t tb = cub_bytes;
         FA_BUILD_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, req, req_sorted, (int)b.nreq, 0,
                                                      end_bit, st));
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 3], st));
-        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, sizeof(int), st));
         reverse_heads_kernel<<<(int)((b.nreq + 255) / 256), 256, 0, st>>>(req_sorted, b.nreq,
                                                                          heads, nheads, next_seg);
         FA_BUILD_CUDA(cudaGetLastError());

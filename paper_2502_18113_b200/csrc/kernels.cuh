@@ -14,7 +14,7 @@ __global__ void build_search_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                     const int64_t *__restrict__ req_off,
                                     unsigned long long *__restrict__ req,
                                     unsigned long long *__restrict__ ctr, int *err,
-                                    int64_t *__restrict__ stats);
+                                    int64_t *__restrict__ stats, int *__restrict__ work);
 
 __global__ void query_search_kernel(Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep,
                                     int ml, int ef, int k, int rerank_depth,

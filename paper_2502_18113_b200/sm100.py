@@ -48,7 +48,7 @@ BUILD_OPTIONS = {
     "tie": int(os.environ.get("FLASHANN_B200_TIE", "2")),
     # frontier entries expanded together per search step during insertion
     # (1 = the semantic core)
-    "expand": int(os.environ.get("FLASHANN_B200_EXPAND", "4")),
+    "expand": int(os.environ.get("FLASHANN_B200_EXPAND", "1")),
     "profile": 0,
 }
 
