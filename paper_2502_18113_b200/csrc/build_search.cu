@@ -1,0 +1,125 @@
+// K4+K5: the batched-insertion search kernel (one warp per inserted vertex),
+// instantiated per result-set variant and expansion width.
+#include "kernels.cuh"
+
+namespace fa {
+
+// One warp inserts one vertex of the batch: descent, per-layer beam search of
+// width C, forward selection (cap R), forward row write, reverse requests.
+// Mirrors insert_one (_core.pyx:501-536) against the graph as of batch start.
+template <int J, int EM>
+__global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
+    Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
+    int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
+    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
+    int64_t *__restrict__ stats, int *__restrict__ work) {
+    // sdtT: the transposed SDT in global memory (L1-resident; keeping it out of
+    // shared memory leaves room for one more CTA per SM)
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    WarpWS ws(smem + wid * L.total, L);
+    int32_t *kept = reinterpret_cast<int32_t *>(ws.H);
+    uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
+    CounterTotals total;
+    // persistent warps pull vertices from the batch; a slow search never holds
+    // its CTA siblings' slots idle
+    for (;;) {
+        int p = 0;
+        if (lane == 0) p = atomicAdd(work, 1);
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= size) break;
+        const int x = start + p;
+        const long long t_begin = clock64();
+        const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
+        __syncwarp();
+        load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
+        __syncwarp();
+        SearchCounters cnt = {};
+        const int level = __ldg(g.levels + x);
+        int cur = ep;
+        uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
+        cnt.dist += 1;
+        for (int layer = ml; layer > level; --layer)
+            hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+        const int top = min(ml, level);
+        unsigned long long *myreq = req + __ldg(req_off + p);
+        long long sel_cycles = 0;
+        for (int layer = top; layer >= 0; --layer) {
+            int ts = 0;
+            bool ok = layer_search<J, EM>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
+                                   ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
+            if (!ok) {
+                if (lane == 0) atomicExch(err, 1);
+                for (int l = layer; l >= 0; --l)
+                    for (int j = lane; j < R; j += 32) myreq[(size_t)(top - l) * R + j] = KEY_MAX;
+                break;
+            }
+            unsigned long long sym = 0;
+            const unsigned long long *T = ws.T;
+            const long long t_sel = clock64();
+            int nsel = warp_select_heur(
+                sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
+                [&](int j, int &v, double &dv) {
+                    unsigned long long k = T[j];
+                    v = to.back((uint32_t)key_id(k));
+                    dv = (double)key_d(k);
+                },
+                kept, kcodes, lane, &sym);
+            cnt.sym += sym;
+            sel_cycles += clock64() - t_sel;
+            // forward row of x (write_forward, _core.pyx:424-438); rows past the
+            // live count keep -1 so readers need only the id row
+            int32_t *row = const_cast<int32_t *>(row_ids(g, layer, x));
+            const int cap = layer_cap(g, layer);
+            for (int j = lane; j < cap; j += 32) row[j] = j < nsel ? kept[j] : -1;
+            if (lane == 0) {
+                if (layer == 0) {
+                    g.cnt0[x] = nsel;
+                    g.cons0[x] = 0;
+                } else {
+                    int64_t r = __ldg(g.uoff + x) + layer - 1;
+                    g.cntU[r] = nsel;
+                    g.consU[r] = 0;
+                }
+            }
+            unsigned long long *lreq = myreq + (size_t)(top - layer) * R;
+            for (int j = lane; j < R; j += 32)
+                lreq[j] = j < nsel ? ((unsigned long long)row_global(g, layer, kept[j]) << 32) |
+                                         (uint32_t)x
+                                   : KEY_MAX;
+            cur = to.back((uint32_t)key_id(ws.T[0]));
+            curd = key_d(ws.T[0]);
+            __syncwarp();
+        }
+        if (stats && lane == 0) {
+            int64_t *st = stats + 8 * (int64_t)x;
+            st[0] = (int64_t)cnt.visited;
+            st[1] = clock64() - t_begin;
+#if FA_PHASE_PROFILE
+            for (int k = 0; k < 4; ++k) st[2 + k] = (int64_t)cnt.ph[k];
+#endif
+            st[6] = sel_cycles;
+            st[7] = (int64_t)cnt.dist;
+        }
+        total.add(cnt);
+    }
+    flush_counters(total, ctr, lane);
+}
+
+BuildSearchFn build_search_variant(int W, int expand) {
+    const int v = set_variant(W);
+    if (expand > 1) {
+        if (v == 0) return build_search_kernel<0, 1>;
+        return v <= 8 ? build_search_kernel<8, kMaxExpand> : build_search_kernel<16, kMaxExpand>;
+    }
+    switch (v) {
+        case 2: return build_search_kernel<2, 1>;
+        case 4: return build_search_kernel<4, 1>;
+        case 8: return build_search_kernel<8, 1>;
+        case 16: return build_search_kernel<16, 1>;
+        default: return build_search_kernel<0, 1>;
+    }
+}
+
+}  // namespace fa

@@ -94,13 +94,21 @@ static int ensure_gvis(fa_index *ix) {
     return FA_OK;
 }
 
-static int pick_hash_log2(int W, int capmax, int R, int mpad, int req) {
-    if (req > 0) return req;
-    int want = 16 * W + 2 * capmax;  // the global tier absorbs longer searches
-    int l = 9;
-    while ((1 << l) < want && l < 12) ++l;
-    // kept ids + codes alias the hash during forward selection
-    while ((4 << l) < round_up(R * 4, 16) + R * kept_stride(mpad)) ++l;
+// log2 of the shared visited table's 16-bit slots (search.cuh VisitedSet);
+// the table also hosts the kept ids + codes of forward selection and the
+// rerank distances (alias_bytes).
+static int pick_hash_log2(int W, int capmax, int R, int mpad, int req, size_t alias_bytes = 0) {
+    int l;
+    if (req > 0) {
+        l = std::max(req, 9);
+    } else {
+        const int want = 16 * W + 2 * capmax;  // the global tier absorbs longer searches
+        l = 12;
+        while ((1 << l) < want && l < 13) ++l;
+    }
+    const size_t need =
+        std::max(alias_bytes, (size_t)round_up(R * 4, 16) + (size_t)R * kept_stride(mpad));
+    while (((size_t)16 << vis_buckets_log2(l)) < need) ++l;
     return l;
 }
 
@@ -390,11 +398,12 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
            pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2),
            gb.expand);
     const size_t sdt_bytes = round_up(g.m * 256, 128);
-    const size_t smem_search = sdt_bytes + (size_t)kSearchWarps * L.total;
+    const size_t smem_search = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
                  smem_search);
-    FA_CUDA(cudaFuncSetAttribute(build_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_search));
+    const BuildSearchFn search_fn = build_search_variant(C, gb.expand);
+    FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
     RL.init(capmax, g.mpad);
     const size_t smem_rev = 2 * sdt_bytes + (size_t)kReverseWarps * RL.total;
@@ -406,11 +415,11 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                                           kReverseWarps * 32, smem_rev));
     const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * kNumSMs;
     int search_per_sm = 0;
-    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, build_search_kernel,
+    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, search_fn,
                                                           kSearchWarps * 32, smem_search));
     const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * kNumSMs;
 
-    uint8_t *adt_batch = nullptr;
+    uint8_t *adt_batch = nullptr, *sdtT = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
     int *err = nullptr, *nheads = nullptr, *next_seg = nullptr;
@@ -420,7 +429,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     auto cleanup = [&]() {
         cudaFree(adt_batch); cudaFree(req); cudaFree(req_sorted); cudaFree(ctr);
         cudaFree(req_off_d); cudaFree(err); cudaFree(cub_tmp); cudaFree(heads);
-        cudaFree(nheads); cudaFree(next_seg);
+        cudaFree(nheads); cudaFree(next_seg); cudaFree(sdtT);
     };
     int end_bit = 32;
     {
@@ -438,6 +447,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&nheads, 2 * sizeof(int))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
+        (rc = dev_alloc((void **)&sdtT, sdt_bytes)) ||
         (rc = dev_alloc((void **)&err, sizeof(int)))) {
         cleanup();
         return rc;
@@ -458,6 +468,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }                                                                                \
     } while (0)
     FA_BUILD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 8, st));
+    transpose_sdt_kernel<<<1, 256, 0, st>>>(ix->d.sdt, g.m, sdtT);
+    FA_BUILD_CUDA(cudaGetLastError());
     FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
                                   cudaMemcpyHostToDevice, st));
@@ -468,7 +480,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         ev.resize(batches.size() * 5);
         for (auto &e : ev) FA_BUILD_CUDA(cudaEventCreate(&e));
     }
-    int64_t launches = 2;  // the two row resets of reset_graph
+    int64_t launches = 3;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 0], st));
@@ -483,8 +495,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         // nheads[0]: reverse row heads, nheads[1]: the search's work counter
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
-        build_search_kernel<<<grid, kSearchWarps * 32, smem_search, st>>>(
-            gb, ix->d.sdt, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+        search_fn<<<grid, kSearchWarps * 32, smem_search, st>>>(
+            gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
             req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
@@ -575,10 +587,14 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
-    L.init(ix->g.mpad, ef, capmax, pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0), 1);
+    L.init(ix->g.mpad, ef, capmax,
+           pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0,
+                          (size_t)8 * std::min(std::max(rerank_depth, 0), ef)),
+           1);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
-    FA_CUDA(cudaFuncSetAttribute(query_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const QuerySearchFn qfn = query_search_variant(ef);
+    FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     uint8_t *adt_q = nullptr;
     FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
@@ -595,7 +611,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
         gq.expand = 1;
-        query_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
+        qfn<<<grid, kSearchWarps * 32, smem, st>>>(
             gq, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
             queries, L, out_ids, out_d, ctr, err);
         cudaError_t e = cudaGetLastError();
@@ -636,7 +652,8 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
-    FA_CUDA(cudaFuncSetAttribute(layer_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const LayerSearchFn lfn = layer_search_variant(width);
+    FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     uint8_t *adt_q = nullptr;
     FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
@@ -653,7 +670,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
         gq.expand = 1;
-        layer_search_kernel<<<grid, kSearchWarps * 32, smem, st>>>(
+        lfn<<<grid, kSearchWarps * 32, smem, st>>>(
             gq, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);

@@ -8,26 +8,70 @@ namespace fa {
 constexpr int kSearchWarps = 4;   // warps (points) per CTA in the search kernels
 constexpr int kReverseWarps = 4;  // warps per CTA in the reverse-edge kernel
 
-__global__ void build_search_kernel(Graph g, const uint8_t *__restrict__ sdt,
-                                    const uint8_t *__restrict__ adt_batch, int start, int size,
-                                    int ep, int ml, int C, int R, WarpLayout L,
-                                    const int64_t *__restrict__ req_off,
-                                    unsigned long long *__restrict__ req,
-                                    unsigned long long *__restrict__ ctr, int *err,
-                                    int64_t *__restrict__ stats, int *__restrict__ work);
+__device__ __forceinline__ int64_t row_global(const Graph &g, int layer, int y) {
+    return layer == 0 ? (int64_t)y : g.n + __ldg(g.uoff + y) + layer - 1;
+}
 
-__global__ void query_search_kernel(Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep,
-                                    int ml, int ef, int k, int rerank_depth,
-                                    const float *__restrict__ vecs, int dim,
-                                    const float *__restrict__ queries, WarpLayout L,
-                                    int64_t *__restrict__ out_ids, double *__restrict__ out_d,
-                                    unsigned long long *__restrict__ ctr, int *err);
+// Per-warp workspace pointers.
+struct WarpWS {
+    uint8_t *adt;
+    unsigned long long *T, *S;
+    int32_t *TQ;
+    int32_t *fresh;
+    uint32_t *fdist;
+    uint32_t *H;
+    __device__ WarpWS(uint8_t *base, const WarpLayout &L) {
+        adt = base + L.adt;
+        T = reinterpret_cast<unsigned long long *>(base + L.T);
+        S = reinterpret_cast<unsigned long long *>(base + L.S);
+        TQ = reinterpret_cast<int32_t *>(base + L.TQ);
+        fresh = reinterpret_cast<int32_t *>(base + L.fresh);
+        fdist = reinterpret_cast<uint32_t *>(base + L.fdist);
+        H = reinterpret_cast<uint32_t *>(base + L.hash);
+    }
+};
 
-__global__ void layer_search_kernel(Graph g, const uint8_t *__restrict__ adt_q, int nq,
-                                    const int64_t *__restrict__ entries, int width, int layer,
-                                    WarpLayout L, int32_t *__restrict__ out_ids,
-                                    double *__restrict__ out_d, int32_t *__restrict__ out_n,
-                                    unsigned long long *__restrict__ ctr, int *err);
+// 64-bit running totals of SearchCounters over the searches of one warp
+struct CounterTotals {
+    unsigned long long dist = 0, kcalls = 0, visited = 0, sym = 0;
+    __device__ void add(const SearchCounters &c) {
+        dist += c.dist;
+        kcalls += c.kcalls;
+        visited += c.visited;
+        sym += c.sym;
+    }
+};
+
+__device__ __forceinline__ void flush_counters(const CounterTotals &c, unsigned long long *ctr,
+                                               int lane) {
+    if (lane == 0) {
+        atomicAdd(ctr + 0, c.dist);
+        atomicAdd(ctr + 1, c.sym);
+        atomicAdd(ctr + 2, c.kcalls);
+        atomicAdd(ctr + 3, c.visited);
+    }
+}
+__device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned long long *ctr,
+                                               int lane) {
+    CounterTotals t;
+    t.add(c);
+    flush_counters(t, ctr, lane);
+}
+
+using BuildSearchFn = void (*)(Graph, const uint8_t *, const uint8_t *, int, int, int, int, int,
+                               int, WarpLayout, const int64_t *, unsigned long long *,
+                               unsigned long long *, int *, int64_t *, int *);
+using QuerySearchFn = void (*)(Graph, const uint8_t *, int, int, int, int, int, int, const float *,
+                               int, const float *, WarpLayout, int64_t *, double *,
+                               unsigned long long *, int *);
+using LayerSearchFn = void (*)(Graph, const uint8_t *, int, const int64_t *, int, int, WarpLayout,
+                               int32_t *, double *, int32_t *, unsigned long long *, int *);
+
+// Kernel instantiations per result-set variant (set_variant(W)) and, for the
+// build, per expansion width (1 or kMaxExpand).
+BuildSearchFn build_search_variant(int W, int expand);
+QuerySearchFn query_search_variant(int W);
+LayerSearchFn layer_search_variant(int W);
 
 struct ReverseLayout {
     int row, cand, kept, kcodes, total;

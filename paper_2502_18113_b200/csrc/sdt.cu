@@ -17,6 +17,11 @@ __global__ void sdt_sum_kernel(const uint8_t *__restrict__ sdt, int m, const uin
     }
 }
 
+__global__ void transpose_sdt_kernel(const uint8_t *__restrict__ sdt, int m,
+                                     uint8_t *__restrict__ sdtT) {
+    stage_sdt_T(sdt, m, sdtT, threadIdx.x, blockDim.x);
+}
+
 // One warp: the whole candidate list of a select_neighbors call.
 __global__ void select_hook_kernel(const uint8_t *__restrict__ sdt, int m, int mpad,
                                    const uint8_t *__restrict__ codes, int cs,

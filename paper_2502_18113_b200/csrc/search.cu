@@ -1,146 +1,8 @@
-// Search kernels: batched-insertion search (build), query search with exact
-// rerank (search_batch), and the single-layer hook (greedy_search_layer).
+// Query search kernels: search with exact rerank (search_batch) and the
+// single-layer hook (greedy_search_layer); the build search is build_search.cu.
 #include "kernels.cuh"
 
 namespace fa {
-
-__device__ __forceinline__ int64_t row_global(const Graph &g, int layer, int y) {
-    return layer == 0 ? (int64_t)y : g.n + __ldg(g.uoff + y) + layer - 1;
-}
-
-// Per-warp workspace pointers.
-struct WarpWS {
-    uint8_t *adt;
-    unsigned long long *T, *S;
-    int32_t *TQ;
-    int32_t *fresh;
-    uint32_t *fdist;
-    uint32_t *H;
-    __device__ WarpWS(uint8_t *base, const WarpLayout &L) {
-        adt = base + L.adt;
-        T = reinterpret_cast<unsigned long long *>(base + L.T);
-        S = reinterpret_cast<unsigned long long *>(base + L.S);
-        TQ = reinterpret_cast<int32_t *>(base + L.TQ);
-        fresh = reinterpret_cast<int32_t *>(base + L.fresh);
-        fdist = reinterpret_cast<uint32_t *>(base + L.fdist);
-        H = reinterpret_cast<uint32_t *>(base + L.hash);
-    }
-};
-
-__device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned long long *ctr,
-                                               int lane) {
-    if (lane == 0) {
-        atomicAdd(ctr + 0, c.dist);
-        atomicAdd(ctr + 1, c.sym);
-        atomicAdd(ctr + 2, c.kcalls);
-        atomicAdd(ctr + 3, c.visited);
-    }
-}
-
-// One warp inserts one vertex of the batch: descent, per-layer beam search of
-// width C, forward selection (cap R), forward row write, reverse requests.
-// Mirrors insert_one (_core.pyx:501-536) against the graph as of batch start.
-__global__ void __launch_bounds__(kSearchWarps * 32) build_search_kernel(
-    Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ adt_batch, int start,
-    int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
-    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
-    int64_t *__restrict__ stats, int *__restrict__ work) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int sdt_bytes = round_up(g.m * 256, 128);
-    uint8_t *sdtT = smem;
-    stage_sdt_T(sdt, g.m, sdtT, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int lane = lane_id();
-    const int wid = threadIdx.x >> 5;
-    WarpWS ws(smem + sdt_bytes + wid * L.total, L);
-    int32_t *kept = reinterpret_cast<int32_t *>(ws.H);
-    uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
-    SearchCounters total = {};
-    // persistent warps pull vertices from the batch; a slow search never holds
-    // its CTA siblings' slots idle
-    for (;;) {
-        int p = 0;
-        if (lane == 0) p = atomicAdd(work, 1);
-        p = __shfl_sync(0xffffffffu, p, 0);
-        if (p >= size) break;
-        const int x = start + p;
-        const long long t_begin = clock64();
-        const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
-        __syncwarp();
-        load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
-        __syncwarp();
-        SearchCounters cnt = {};
-        const int level = __ldg(g.levels + x);
-        int cur = ep;
-        uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
-        cnt.dist += 1;
-        for (int layer = ml; layer > level; --layer)
-            hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
-        const int top = min(ml, level);
-        unsigned long long *myreq = req + __ldg(req_off + p);
-        long long sel_cycles = 0;
-        for (int layer = top; layer >= 0; --layer) {
-            int ts = 0;
-            bool ok = layer_search(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
-                                   ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
-            if (!ok) {
-                if (lane == 0) atomicExch(err, 1);
-                for (int l = layer; l >= 0; --l)
-                    for (int j = lane; j < R; j += 32) myreq[(size_t)(top - l) * R + j] = KEY_MAX;
-                break;
-            }
-            unsigned long long sym = 0;
-            const unsigned long long *T = ws.T;
-            const long long t_sel = clock64();
-            int nsel = warp_select_heur(
-                sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
-                [&](int j, int &v, double &dv) {
-                    unsigned long long k = T[j];
-                    v = to.back((uint32_t)key_id(k));
-                    dv = (double)key_d(k);
-                },
-                kept, kcodes, lane, &sym);
-            cnt.sym += sym;
-            sel_cycles += clock64() - t_sel;
-            // forward row of x (write_forward, _core.pyx:424-438); rows past the
-            // live count keep -1 so readers need only the id row
-            int32_t *row = const_cast<int32_t *>(row_ids(g, layer, x));
-            const int cap = layer_cap(g, layer);
-            for (int j = lane; j < cap; j += 32) row[j] = j < nsel ? kept[j] : -1;
-            if (lane == 0) {
-                if (layer == 0) {
-                    g.cnt0[x] = nsel;
-                    g.cons0[x] = 0;
-                } else {
-                    int64_t r = __ldg(g.uoff + x) + layer - 1;
-                    g.cntU[r] = nsel;
-                    g.consU[r] = 0;
-                }
-            }
-            unsigned long long *lreq = myreq + (size_t)(top - layer) * R;
-            for (int j = lane; j < R; j += 32)
-                lreq[j] = j < nsel ? ((unsigned long long)row_global(g, layer, kept[j]) << 32) |
-                                         (uint32_t)x
-                                   : KEY_MAX;
-            cur = to.back((uint32_t)key_id(ws.T[0]));
-            curd = key_d(ws.T[0]);
-            __syncwarp();
-        }
-        if (stats && lane == 0) {
-            int64_t *st = stats + 8 * (int64_t)x;
-            st[0] = (int64_t)cnt.visited;
-            st[1] = clock64() - t_begin;
-            for (int k = 0; k < 4; ++k) st[2 + k] = (int64_t)cnt.ph[k];
-            st[6] = sel_cycles;
-            st[7] = (int64_t)cnt.dist;
-        }
-        total.dist += cnt.dist;
-        total.sym += cnt.sym;
-        total.kcalls += cnt.kcalls;
-        total.visited += cnt.visited;
-    }
-    flush_counters(total, ctr, lane);
-}
 
 // Warp-cooperative fp32 L2 (fa_l2sq_f32 tree, common.cuh l2_tree) of four
 // (query, vector) pairs at once: lane group g = lane/8 handles pair g and lane
@@ -181,6 +43,7 @@ __device__ __forceinline__ float warp_l2_group(const float *q, const float *v, i
 // search_one (_core.pyx:784-814): descent on layers ml..1, layer-0 search of
 // width ef, optional exact rerank of the first rerank_depth results with
 // (d, id) ordering (fa_sort_pairs), then the first k.
+template <int J>
 __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep, int ml, int ef, int k,
     int rerank_depth, const float *__restrict__ vecs, int dim, const float *__restrict__ queries,
@@ -202,7 +65,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
     for (int layer = ml; layer > 0; --layer)
         hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
     int ts = 0;
-    bool ok = layer_search(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh, ws.fdist,
+    bool ok = layer_search<J, 1>(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh, ws.fdist,
                            ws.H, L.hash_log2, cnt, to, lane);
     int64_t *oid = out_ids + (size_t)q * k;
     double *od = out_d + (size_t)q * k;
@@ -258,6 +121,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
 }
 
 // greedy_search_layer (_core.pyx:891-939): one layer from a given entry.
+template <int J>
 __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     Graph g, const uint8_t *__restrict__ adt_q, int nq, const int64_t *__restrict__ entries,
     int width, int layer, WarpLayout L, int32_t *__restrict__ out_ids, double *__restrict__ out_d,
@@ -276,7 +140,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     uint32_t d0 = adt_one(ws.adt, g.codes + (size_t)entry * g.mpad, g.mpad, lane);
     cnt.dist += 1;
     int ts = 0;
-    bool ok = layer_search(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
+    bool ok = layer_search<J, 1>(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                            ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
     if (!ok) {
         if (lane == 0) atomicExch(err, 1);
@@ -288,6 +152,26 @@ __global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
     }
     if (lane == 0) out_n[q] = ts;
     flush_counters(cnt, ctr, lane);
+}
+
+QuerySearchFn query_search_variant(int W) {
+    switch (set_variant(W)) {
+        case 2: return query_search_kernel<2>;
+        case 4: return query_search_kernel<4>;
+        case 8: return query_search_kernel<8>;
+        case 16: return query_search_kernel<16>;
+        default: return query_search_kernel<0>;
+    }
+}
+
+LayerSearchFn layer_search_variant(int W) {
+    switch (set_variant(W)) {
+        case 2: return layer_search_kernel<2>;
+        case 4: return layer_search_kernel<4>;
+        case 8: return layer_search_kernel<8>;
+        case 16: return layer_search_kernel<16>;
+        default: return layer_search_kernel<0>;
+    }
 }
 
 }  // namespace fa

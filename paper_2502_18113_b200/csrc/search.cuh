@@ -16,6 +16,10 @@
 
 #include "select.cuh"
 
+#ifndef FA_PHASE_PROFILE
+#define FA_PHASE_PROFILE 0
+#endif
+
 namespace fa {
 
 struct Graph {
@@ -56,6 +60,18 @@ __device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
 }
 
 // ---- per-warp workspace ----------------------------------------------------
+// Largest search width kept in registers (lane l owns slots l + 32 j, j < 16);
+// wider searches keep their result set in shared memory.
+constexpr int kRegSetMax = 512;
+
+// Visited table geometry for a requested size of 2^hlog2 16-bit slots: buckets
+// of 8 slots, at least 2^9 buckets (15-bit remainders of 24-bit ids); below
+// 2^12 slots only the first 2^hlog2 / 512 slots of each bucket are used.
+__host__ __device__ inline int vis_buckets_log2(int hlog2) { return hlog2 > 12 ? hlog2 - 3 : 9; }
+__host__ __device__ inline int vis_bucket_slots(int hlog2) {
+    return hlog2 >= 12 ? 8 : 1 << (hlog2 > 9 ? hlog2 - 9 : 0);
+}
+
 struct WarpLayout {
     int adt, T, S, TQ, fresh, fdist, hash, total;
     int hash_log2;
@@ -63,14 +79,17 @@ struct WarpLayout {
     __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand) {
         hash_log2 = hlog2;
         const int nc = cand_capacity(expand, capmax);
+        const int Wp = round_up(W, 32);
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
-        T = o; o += round_up(W, 32) * (8 + 4 + 1);  // results, 32-bit keys, flags
+        // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
+        T = o; o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
+        o = round_up(o, 16);
         S = o; o += 2 * nc * 4;                     // candidate keys (two buffers)
-        TQ = o; o += round_up(W, 32) * 4;
+        TQ = o; o += Wp * 4;                        // tie queue, then the final sort
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
-        hash = o; o += (4 << hlog2);
+        hash = o; o += 16 << vis_buckets_log2(hlog2);
         total = round_up(o, 128);
     }
 };
@@ -144,42 +163,41 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *c
     __syncwarp();
 }
 
-// ---- visited hash (exact, open addressing in shared memory) ---------------
-__device__ __forceinline__ void hash_clear(uint32_t *H, int hlog2, int lane) {
-    uint4 z = make_uint4(0, 0, 0, 0);
-    const int n4 = (1 << hlog2) >> 2;
-    for (int i = lane; i < n4; i += 32) reinterpret_cast<uint4 *>(H)[i] = z;
-}
-// true iff id was absent (and is now present)
-__device__ __forceinline__ bool hash_insert(uint32_t *H, int hlog2, int id) {
-    const uint32_t key = (uint32_t)id + 1u;
-    const uint32_t mask = (1u << hlog2) - 1u;
-    uint32_t h = (key * 2654435761u) >> (32 - hlog2);
-    while (true) {
-        uint32_t old = atomicCAS(H + h, 0u, key);
-        if (old == 0u) return true;
-        if (old == key) return false;
-        h = (h + 1u) & mask;
-    }
-}
-
-// Exact visited set of one search: an open-addressing table in shared memory,
-// spilling to a per-warp-slot table in global memory (L2-resident) once the
-// shared one is 7/8 full.  An id lives in exactly one tier: lookups walk the
-// shared chain to its first empty slot, then the global chain.  Global slots
-// hold (epoch << 24 | id); entries of older epochs count as empty, so the
-// global table is cleared only once every 255 searches of its warp slot.
+// ---- visited set (exact) ---------------------------------------------------
+// Shared tier: 2^kb buckets of eight 16-bit slots.  A 24-bit id maps through a
+// bijection h = id * odd (mod 2^24) to bucket h >> (24 - kb) and remainder
+// (h & low bits) + 1 (0 = empty), so a slot needs 16 bits and one 16-byte load
+// tests a whole bucket.  Slots fill in order and are never removed; an id whose
+// bucket is full lives in the global tier: a per-warp-slot open-addressing
+// table in global memory (L2-resident) holding (epoch << 24 | id).  Entries of
+// older epochs count as empty, so a slot's table is cleared only once every
+// 255 searches.  Either way every id lives in exactly one tier.
 constexpr int kGlobalHashLog2 = 14;
 constexpr int kMaxWarpsPerSM = 64;
+constexpr uint32_t kVisMul = 0x9E3779B1u;
+
+__device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p))
+                 : "memory");
+    return v;
+}
+
+// two bits per 32-bit word: half 0 / half 1 equal to zero
+__device__ __forceinline__ uint32_t zero_halves(uint32_t w) {
+    return (uint32_t)((w & 0xffffu) == 0u) | ((uint32_t)((w >> 16) == 0u) << 1);
+}
 
 struct VisitedSet {
-    uint32_t *H;       // shared tier
-    int hlog2, hcount, hlimit;
+    uint4 *B;          // shared tier buckets
+    int kb;            // log2 buckets
+    uint32_t usable;   // mask of usable slots per bucket
     uint32_t *G;       // global tier of this warp slot
     uint32_t *gepoch;  // epoch counter of this warp slot
     uint32_t epoch;
     int gcount, glimit;
-    bool spilled;      // sticky: new ids go to the global tier
 
     __device__ static uint32_t slot_id() {
         uint32_t sm, w;
@@ -188,11 +206,12 @@ struct VisitedSet {
         return sm * kMaxWarpsPerSM + w;
     }
 
-    __device__ void begin(uint32_t *gtables, uint32_t *gepochs, int lane) {
-        hash_clear(H, hlog2, lane);
-        hcount = 0;
-        spilled = false;
-        hlimit = (1 << hlog2) / 2;  // linear probing stays short at load <= 1/2
+    __device__ void begin(void *H, int hlog2, uint32_t *gtables, uint32_t *gepochs, int lane) {
+        B = reinterpret_cast<uint4 *>(H);
+        kb = vis_buckets_log2(hlog2);
+        usable = (1u << vis_bucket_slots(hlog2)) - 1u;
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
         gcount = 0;
         glimit = (1 << kGlobalHashLog2) * 3 / 4;
         G = nullptr;
@@ -204,7 +223,6 @@ struct VisitedSet {
             if (lane == 0) e = *gepoch + 1u;
             e = __shfl_sync(0xffffffffu, e, 0);
             if (e > 255u) {  // wrap: clear this slot's table once
-                uint4 z = make_uint4(0, 0, 0, 0);
                 for (int i = lane; i < (1 << kGlobalHashLog2) / 4; i += 32)
                     reinterpret_cast<uint4 *>(G)[i] = z;
                 e = 1u;
@@ -216,23 +234,31 @@ struct VisitedSet {
         __syncwarp();
     }
 
-    // 0 = already visited, 1 = new (shared tier), 2 = new (global tier)
-    __device__ int visit(int id, bool to_shared) {
-        const uint32_t key = (uint32_t)id + 1u;
-        const uint32_t mask = (1u << hlog2) - 1u;
-        uint32_t h = (key * 2654435761u) >> (32 - hlog2);
+    // 0 = already visited, 1 = new (shared tier), 2 = new (global tier),
+    // 3 = the global tier is unavailable (overflow)
+    __device__ int visit(int id) {
+        const uint32_t h = ((uint32_t)id * kVisMul) & 0xffffffu;
+        const uint32_t r = (h & ((1u << (24 - kb)) - 1u)) + 1u;
+        uint4 *bk = B + (h >> (24 - kb));
+        const uint32_t rr = r | (r << 16);
         while (true) {
-            uint32_t v = H[h];
-            if (v == key) return 0;
-            if (v == 0u) {
-                if (!to_shared) break;
-                uint32_t old = atomicCAS(H + h, 0u, key);
-                if (old == 0u) return 1;
-                if (old == key) return 0;
-                continue;  // lost the slot: re-read it
-            }
-            h = (h + 1u) & mask;
+            const uint4 v = lds128_volatile(bk);
+            if ((__vcmpeq2(v.x, rr) | __vcmpeq2(v.y, rr) | __vcmpeq2(v.z, rr) |
+                 __vcmpeq2(v.w, rr)) != 0u)
+                return 0;
+            const uint32_t zm = (zero_halves(v.x) | (zero_halves(v.y) << 2) |
+                                 (zero_halves(v.z) << 4) | (zero_halves(v.w) << 6)) &
+                                usable;
+            if (zm == 0u) break;
+            const int e = __ffs(zm) - 1;
+            const int wi = e >> 1;
+            const uint32_t ow = wi == 0 ? v.x : wi == 1 ? v.y : wi == 2 ? v.z : v.w;
+            const uint32_t nw = ow | (r << (16 * (e & 1)));
+            if (atomicCAS(reinterpret_cast<uint32_t *>(bk) + wi, ow, nw) == ow) return 1;
+            // another lane took the slot: re-read the bucket
         }
+        if (G == nullptr) return 3;
+        const uint32_t key = (uint32_t)id + 1u;
         const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
         const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
         uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
@@ -371,18 +397,29 @@ __device__ __forceinline__ void shift_right1(unsigned long long *T, int lo, int 
     }
 }
 
+// Per-search counters (32-bit: one search never reaches 2^32 of anything);
+// kernels accumulate them into 64-bit totals.
 struct SearchCounters {
-    unsigned long long dist, kcalls, visited, sym;
-    // SM cycles per phase of layer_search (diagnostics, point_stats):
-    // 0 pop + prediction, 1 row + visited filter, 2 distances, 3 acceptance
+    uint32_t dist, kcalls, visited, sym;
+#if FA_PHASE_PROFILE
+    // SM cycles per phase of layer_search (diagnostics, point_stats; build with
+    // -DFA_PHASE_PROFILE=1): 0 pop + prediction, 1 row + visited filter,
+    // 2 distances, 3 acceptance
     unsigned long long ph[4];
+#endif
 };
 
+#if FA_PHASE_PROFILE
+__device__ __forceinline__ long long phase_clock() { return clock64(); }
 __device__ __forceinline__ void phase_mark(SearchCounters &c, int k, long long &t) {
     const long long now = clock64();
     c.ph[k] += (unsigned long long)(now - t);
     t = now;
 }
+#else
+__device__ __forceinline__ long long phase_clock() { return 0; }
+__device__ __forceinline__ void phase_mark(SearchCounters &, int, long long &) {}
+#endif
 
 // Warp-cooperative best-first search on one layer.
 // On return T[0..ts) holds the result ascending by (d, id).
@@ -465,7 +502,300 @@ __device__ __forceinline__ uint32_t warp_maxd(const uint32_t *K, int n, int lane
     return __reduce_max_sync(0xffffffffu, mx);
 }
 
-__device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
+// ---- register-resident result set (W <= kRegSetMax) -------------------------
+// Lane l owns slots l + 32 j (j < J); slot s is live iff s < ts.  Bit j of `fl`
+// marks slot j expanded.  Every loop over j is unrolled (no dynamic register
+// indexing), so pop / worst distance / eviction are register compares plus one
+// warp reduction instead of passes over shared memory.
+template <int J>
+struct RegSet {
+    uint32_t key[J];
+    uint32_t fl;
+    // smallest key over live unexpanded slots (dsel < 0) or over live slots at
+    // distance dsel; has = any such slot
+    __device__ __forceinline__ bool local_min(int ts, int lane, int dsel, uint32_t &best,
+                                              int &bj) const {
+        bool has = false;
+        best = 0xffffffffu;
+        bj = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const bool ok = lane + 32 * j < ts &&
+                            (dsel < 0 ? ((fl >> j) & 1u) == 0u : (int)(key[j] >> 24) == dsel);
+            if (ok && (!has || key[j] < best)) {
+                best = key[j];
+                bj = j;
+                has = true;
+            }
+        }
+        return has;
+    }
+    // smallest and second smallest live unexpanded keys of this lane
+    __device__ __forceinline__ int local_min2(int ts, int lane, uint32_t &b1, int &j1,
+                                              uint32_t &b2) const {
+        int n = 0;
+        b1 = b2 = 0xffffffffu;
+        j1 = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            if (lane + 32 * j < ts && ((fl >> j) & 1u) == 0u) {
+                const uint32_t k = key[j];
+                if (n == 0 || k < b1) {
+                    b2 = b1;
+                    b1 = k;
+                    j1 = j;
+                } else if (n == 1 || k < b2) {
+                    b2 = k;
+                }
+                ++n;
+            }
+        }
+        return n;
+    }
+    __device__ __forceinline__ uint32_t maxd(int ts, int lane) const {
+        uint32_t mx = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+            if (lane + 32 * j < ts) mx = max(mx, key[j] >> 24);
+        return __reduce_max_sync(0xffffffffu, mx);
+    }
+    __device__ __forceinline__ void put(int js, uint32_t k) {
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+            if (j == js) key[j] = k;
+        fl &= ~(1u << js);
+    }
+};
+
+// warp minimum of the lanes' candidates (keys are distinct); false if none
+__device__ __forceinline__ bool warp_pick(bool has, uint32_t best, uint32_t &m, int &owner) {
+    const unsigned any = __ballot_sync(0xffffffffu, has);
+    if (!any) return false;
+    m = __reduce_min_sync(0xffffffffu, has ? best : 0xffffffffu);
+    owner = __ffs(__ballot_sync(0xffffffffu, has && best == m)) - 1;
+    return true;
+}
+
+template <int J, int EM>
+__device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int entry,
+                                                 uint32_t entry_d, int W, const uint8_t *adt_s,
+                                                 unsigned long long *T, int &ts_out,
+                                                 unsigned long long *S, int32_t *TQ,
+                                                 int32_t *fresh, uint32_t *fdist, uint32_t *H,
+                                                 int hlog2, SearchCounters &cnt,
+                                                 const TieOrder &to, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int cap = layer_cap(g, layer);
+    uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
+    uint32_t *Sb = Sa + cand_capacity(g);
+    const unsigned lt = (1u << lane) - 1u;
+    VisitedSet vs;
+    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
+    if (lane == 0) vs.visit(entry);
+    RegSet<J> rs;
+#pragma unroll
+    for (int j = 0; j < J; ++j) rs.key[j] = 0u;
+    rs.fl = 0u;
+    if (lane == 0) rs.key[0] = k32(entry_d, to.fwd((uint32_t)entry));
+    int ts = 1;
+    uint32_t wd = 0xffffffffu;  // worst distance once the set is full
+    int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
+    int pre_v = -1;             // speculative id row of the most likely next pop (EM == 1)
+    int pre[kRowChunks];
+    const int E = EM > 1 ? min(max(g.expand, 1), EM) : 1;
+    long long tph = phase_clock();
+    __syncwarp();
+    while (true) {
+        phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
+        // ---- pop up to E frontier minima: unexpanded set members vs tie queue
+        int pv[EM];
+        int npop = 0;
+        int u[EM][kRowChunks];
+        if (EM == 1) {
+            uint32_t b1, b2;
+            int j1;
+            const int nl = rs.local_min2(ts, lane, b1, j1, b2);
+            uint32_t m = 0;
+            int owner = -1;
+            const bool anyT = warp_pick(nl > 0, b1, m, owner);
+            const bool anyQ = tq_h < tq_t;
+            if (!anyT && !anyQ) break;
+            const uint32_t kQ = anyQ ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
+            const bool fromT = anyT && (!anyQ || m < kQ);
+            pv[0] = to.back((fromT ? m : kQ) & 0xffffffu);
+            npop = 1;
+            if (fromT) {
+                if (lane == owner) rs.fl |= 1u << j1;
+            } else {
+                ++tq_h;
+            }
+            if (pv[0] == pre_v) {
+#pragma unroll
+                for (int k = 0; k < kRowChunks; ++k) u[0][k] = pre[k];
+            } else {
+                load_row(row_ids(g, layer, pv[0]), cap, lane, u[0]);
+            }
+            // predict the next pop assuming nothing new enters: the popped
+            // lane offers its second smallest key
+            const bool h2 = fromT && lane == owner ? nl > 1 : nl > 0;
+            const uint32_t c2 = fromT && lane == owner ? b2 : b1;
+            uint32_t m2 = 0;
+            int o2 = -1;
+            const bool anyT2 = warp_pick(h2, c2, m2, o2);
+            const bool anyQ2 = tq_h < tq_t;
+            if (anyT2 || anyQ2) {
+                const uint32_t kQ2 = anyQ2 ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
+                pre_v = to.back((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu);
+                load_row(row_ids(g, layer, pre_v), cap, lane, pre);
+            } else {
+                pre_v = -1;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < EM; ++r) {
+                if (r >= E) break;
+                uint32_t best;
+                int bj;
+                const bool has = rs.local_min(ts, lane, -1, best, bj);
+                uint32_t m = 0;
+                int owner = -1;
+                const bool anyT = warp_pick(has, best, m, owner);
+                const bool anyQ = tq_h < tq_t;
+                if (!anyT && !anyQ) break;
+                const uint32_t kQ = anyQ ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
+                const bool fromT = anyT && (!anyQ || m < kQ);
+                pv[r] = to.back((fromT ? m : kQ) & 0xffffffu);
+                ++npop;
+                if (fromT) {
+                    if (lane == owner) rs.fl |= 1u << bj;
+                } else {
+                    ++tq_h;
+                }
+            }
+            if (npop == 0) break;
+            // id rows of the popped vertices, all loads in flight together
+#pragma unroll
+            for (int r = 0; r < EM; ++r)
+                if (r < npop) load_row(row_ids(g, layer, pv[r]), cap, lane, u[r]);
+        }
+        cnt.visited += npop;
+        phase_mark(cnt, 0, tph);
+        if (vs.gcount + npop * cap > vs.glimit) return false;
+        // visited filter over the rows (pop order, slot order), compacted
+        bool over = false;
+        int nf = 0;
+#pragma unroll
+        for (int r = 0; r < EM; ++r) {
+            if (r >= npop) break;
+            int nlive = 0;
+#pragma unroll
+            for (int k = 0; k < kRowChunks; ++k) {
+                if (k * 32 >= cap) break;
+                const int x = u[r][k];
+                const bool live = x >= 0;
+                const int rr = live ? vs.visit(x) : 0;
+                over |= rr == 3;
+                const bool fr = rr == 1 || rr == 2;
+                const unsigned bl = __ballot_sync(FULL, live);
+                const unsigned bf = __ballot_sync(FULL, fr);
+                if (fr) fresh[nf + __popc(bf & lt)] = x;
+                nf += __popc(bf);
+                nlive += __popc(bl);
+                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
+            }
+            cnt.kcalls += (nlive + 15) >> 4;
+        }
+        if (__any_sync(FULL, over)) return false;
+        cnt.dist += nf;
+        __syncwarp();
+        phase_mark(cnt, 1, tph);
+        if (nf == 0) continue;
+        dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
+        phase_mark(cnt, 2, tph);
+        // candidates that can possibly enter: all while the set is not full,
+        // else d < worst
+        int ns = 0;
+        for (int base = 0; base < nf; base += 32) {
+            const int f = base + lane;
+            const bool ok = f < nf && fdist[f] < wd;
+            const unsigned b = __ballot_sync(FULL, ok);
+            if (ok) Sa[ns + __popc(b & lt)] = k32(fdist[f], to.fwd((uint32_t)fresh[f]));
+            ns += __popc(b);
+        }
+        __syncwarp();
+        if (ns == 0) continue;
+        const int nfill = min(ns, W - ts);
+        const uint32_t *src = Sa;
+        if (nfill < ns) {
+            // offers are processed in ascending order: rank-sort them
+            for (int j = lane; j < ns; j += 32) {
+                const uint32_t k = Sa[j];
+                int r = 0;
+                for (int t = 0; t < ns; ++t) r += Sa[t] < k;
+                Sb[r] = k;
+            }
+            __syncwarp();
+            src = Sb;
+        }
+        // the first nfill offers fill slots ts .. ts + nfill
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int o = lane + 32 * j - ts;
+            if (o >= 0 && o < nfill) {
+                rs.key[j] = src[o];
+                rs.fl &= ~(1u << j);
+            }
+        }
+        ts += nfill;
+        if (ts == W) wd = rs.maxd(ts, lane);
+        for (int j = nfill; j < ns; ++j) {
+            const uint32_t s = src[j];
+            if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+            // evict the smallest key of the worst-distance group
+            uint32_t best;
+            int bj;
+            const bool has = rs.local_min(ts, lane, (int)wd, best, bj);
+            uint32_t m = 0;
+            int owner = 0;
+            warp_pick(has, best, m, owner);
+            const uint32_t expd = __shfl_sync(FULL, (rs.fl >> bj) & 1u, owner);
+            if (!expd) {
+                if (lane == 0) TQ[tq_t] = (int32_t)(m & 0xffffffu);
+                ++tq_t;
+            }
+            if (lane == owner) rs.put(bj, s);
+            const uint32_t nwd = rs.maxd(ts, lane);
+            if (nwd < wd) {
+                wd = nwd;
+                tq_h = tq_t = 0;  // the evicted ties are beyond the new worst
+            }
+        }
+        __syncwarp();
+    }
+    // sort once: stage the keys (the tie queue's space is free now), rank by
+    // counting (keys are distinct) into the 64-bit slots
+    uint32_t *Ks = reinterpret_cast<uint32_t *>(TQ);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+        if (lane + 32 * j < ts) Ks[lane + 32 * j] = rs.key[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        if (lane + 32 * j < ts) {
+            const uint32_t k = rs.key[j];
+            int r = 0;
+            for (int t = 0; t < ts; ++t) r += Ks[t] < k;
+            T[r] = make_key(k >> 24, (int)(k & 0xffffffu));
+        }
+    }
+    __syncwarp();
+    ts_out = ts;
+    return true;
+}
+
+// Shared-memory variant for W > kRegSetMax (same rules, same results).
+__device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
                                     const uint8_t *adt_s, unsigned long long *T, int &ts,
                                     unsigned long long *S, int32_t *TQ, int32_t *fresh,
                                     uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
@@ -479,15 +809,12 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
     uint32_t *Sb = Sa + cand_capacity(g);
     VisitedSet vs;
-    vs.H = H;
-    vs.hlog2 = hlog2;
-    vs.begin(g.gvis, g.gvis_epoch, lane);
+    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
     if (lane == 0) {
-        vs.visit(entry, true);
+        vs.visit(entry);
         K[0] = k32(entry_d, to.fwd((uint32_t)entry));
         F[0] = 0;
     }
-    vs.hcount = 1;
     ts = 1;
     uint32_t wd = 0xffffffffu;  // worst distance once the set is full
     int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
@@ -496,7 +823,7 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     // frontier entries expanded per step: 1 = the semantic core; E > 1 pops the
     // E smallest poppable entries and expands them together (oracle: expand)
     const int E = g.expand > 1 ? min(g.expand, kMaxExpand) : 1;
-    long long tph = clock64();
+    long long tph = phase_clock();
     __syncwarp();
     while (true) {
         phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
@@ -545,11 +872,8 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        // once a search spills to the global tier it never returns to the shared
-        // one: an id inserted globally must not be re-inserted in shared memory
-        vs.spilled |= vs.hcount + npop * cap > vs.hlimit;
-        const bool to_shared = !vs.spilled;
-        if (!to_shared && (vs.G == nullptr || vs.gcount + npop * cap > vs.glimit)) return false;
+        if (vs.gcount + npop * cap > vs.glimit) return false;
+        bool over = false;
         // visited filter over the rows (pop order, slot order), compacted
         int nf = 0;
 #pragma unroll
@@ -561,18 +885,19 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
                 if (k * 32 >= cap) break;
                 const int x = u[r][k];
                 bool live = x >= 0;
-                const int rr = live ? vs.visit(x, to_shared) : 0;
-                const bool fr = rr != 0;
+                const int rr = live ? vs.visit(x) : 0;
+                over |= rr == 3;
+                const bool fr = rr == 1 || rr == 2;
                 unsigned bl = __ballot_sync(0xffffffffu, live);
                 unsigned bf = __ballot_sync(0xffffffffu, fr);
                 if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
                 nf += __popc(bf);
                 nlive += __popc(bl);
-                vs.hcount += __popc(__ballot_sync(0xffffffffu, rr == 1));
                 vs.gcount += __popc(__ballot_sync(0xffffffffu, rr == 2));
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
+        if (__any_sync(0xffffffffu, over)) return false;
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
@@ -651,6 +976,29 @@ __device__ inline bool layer_search(const Graph &g, int layer, int entry, uint32
     }
     __syncwarp();
     return true;
+}
+
+
+// Best-first layer search with the result-set variant J chosen by the host
+// (set_variant): J slots per lane in registers, J = 0 the shared-memory set.
+template <int J, int EM>
+__device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
+                                             int W, const uint8_t *adt_s, unsigned long long *T,
+                                             int &ts, unsigned long long *S, int32_t *TQ,
+                                             int32_t *fresh, uint32_t *fdist, uint32_t *H,
+                                             int hlog2, SearchCounters &cnt, const TieOrder &to,
+                                             int lane) {
+    if constexpr (J == 0)
+        return layer_search_smem(g, layer, entry, entry_d, W, adt_s, T, ts, S, TQ, fresh, fdist, H,
+                                 hlog2, cnt, to, lane);
+    else
+        return layer_search_reg<J, EM>(g, layer, entry, entry_d, W, adt_s, T, ts, S, TQ, fresh,
+                                       fdist, H, hlog2, cnt, to, lane);
+}
+
+// result-set variant for a search width W: register slots per lane, 0 = shared
+__host__ __device__ inline int set_variant(int W) {
+    return W <= 64 ? 2 : W <= 128 ? 4 : W <= 256 ? 8 : W <= kRegSetMax ? 16 : 0;
 }
 
 // Width-1 greedy descent (hill_climb, _core.pyx:345-385): move to the first

@@ -29,6 +29,10 @@ __device__ __forceinline__ void stage_sdt_T(const uint8_t *__restrict__ sdt, int
     }
 }
 
+// The same transposition into a global buffer (m x 256 bytes), one CTA.
+__global__ void transpose_sdt_kernel(const uint8_t *__restrict__ sdt, int m,
+                                     uint8_t *__restrict__ sdtT);
+
 // min(sum_i sdt[i][cu_i][cv_i], 255) with cu from shared (word-aligned row)
 // and cv from global/shared (uniform across the warp).
 __device__ __forceinline__ uint32_t sdt_sum_rows(const uint8_t *sdtT, int m, const uint8_t *cu,
