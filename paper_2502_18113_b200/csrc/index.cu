@@ -23,6 +23,7 @@ struct fa_index {
     uint8_t *codes = nullptr;
     int32_t *adj0 = nullptr, *cnt0 = nullptr, *adjU = nullptr, *cntU = nullptr;
     uint8_t *cons0 = nullptr, *consU = nullptr;
+    uint8_t *dist0 = nullptr, *distU = nullptr;  // prune-distance caches
     int32_t *upper_owner = nullptr;
     uint32_t *gvis = nullptr, *gvis_epoch = nullptr;  // global visited tier
     int search_tie = 0;
@@ -215,10 +216,13 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     if ((rc = dev_alloc((void **)&ix->adjU, sizeof(int32_t) * g.nU * g.capUp))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->cntU, sizeof(int32_t) * g.nU))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->consU, g.nU))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->dist0, (size_t)g.n * g.cap0p))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->distU, (size_t)g.nU * g.capUp))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->upper_owner, sizeof(int32_t) * g.nU))) return fail(rc);
     g.codes = ix->codes;
     g.adj0 = ix->adj0; g.cnt0 = ix->cnt0; g.cons0 = ix->cons0;
     g.adjU = ix->adjU; g.cntU = ix->cntU; g.consU = ix->consU;
+    g.dist0 = ix->dist0; g.distU = ix->distU;
     g.tie = 0;
     g.expand = 1;
     g.gvis = nullptr;
@@ -272,6 +276,7 @@ extern "C" int fa_index_destroy(fa_index *ix) {
     cudaFree(ix->codes);
     cudaFree(ix->adj0); cudaFree(ix->cnt0); cudaFree(ix->cons0);
     cudaFree(ix->adjU); cudaFree(ix->cntU); cudaFree(ix->consU);
+    cudaFree(ix->dist0); cudaFree(ix->distU);
     cudaFree(ix->upper_owner);
     cudaFree(ix->gvis);
     cudaFree(ix->gvis_epoch);

@@ -74,10 +74,12 @@ QuerySearchFn query_search_variant(int W);
 LayerSearchFn layer_search_variant(int W);
 
 struct ReverseLayout {
-    int row, cand, kept, kcodes, total;
+    int row, rowd, keptd, cand, kept, kcodes, total;
     __host__ __device__ void init(int capmax, int mpad) {
         int o = 0;
         row = o; o += round_up(capmax, 32) * 4;
+        rowd = o; o += round_up(capmax, 32);
+        keptd = o; o += round_up(capmax, 32);
         cand = o; o += 128 * 8;
         kept = o; o += round_up(capmax, 32) * 4;
         kcodes = o; o += round_up(capmax * kept_stride(mpad), 16);

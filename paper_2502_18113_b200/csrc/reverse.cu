@@ -16,21 +16,38 @@
 
 namespace fa {
 
-// u uniform across the warp: sdtN[i][cu][cv] rows are 16 contiguous bytes.
-__device__ __forceinline__ uint32_t sdt_sum_u_uniform(const uint8_t *sdtN, int m, const uint8_t *cu,
-                                                      const uint8_t *cv) {
+// sum_i tab[(i << 8) + (p_i << 4) + q_i] over i < m, saturated at 255; p, q
+// are code rows of the flat table (16-byte aligned, zero padded to mpad).
+// With p uniform across the warp every lane reads inside one 16-byte row.
+__device__ __forceinline__ uint32_t sdt_sum16(const uint8_t *tab, int m,
+                                              const uint8_t *__restrict__ p,
+                                              const uint8_t *__restrict__ q) {
     uint32_t acc = 0;
-    int i = 0;
-    for (; i + 4 <= m; i += 4) {
-        uint32_t wu = *reinterpret_cast<const uint32_t *>(cu + i);
-        uint32_t wv = *reinterpret_cast<const uint32_t *>(cv + i);
+    for (int i0 = 0; i0 < m; i0 += 16) {
+        const uint4 wp = __ldg(reinterpret_cast<const uint4 *>(p + i0));
+        const uint4 wq = __ldg(reinterpret_cast<const uint4 *>(q + i0));
+        const uint32_t P[4] = {wp.x, wp.y, wp.z, wp.w};
+        const uint32_t Q[4] = {wq.x, wq.y, wq.z, wq.w};
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            uint32_t a_ = (wu >> (8 * b)) & 0xffu, b_ = (wv >> (8 * b)) & 0xffu;
-            acc += sdtN[((i + b) << 8) + (a_ << 4) + b_];
-        }
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int i = i0 + 4 * w + b;
+                if (i < m)
+                    acc += tab[(i << 8) + (((P[w] >> (8 * b)) & 0xffu) << 4) +
+                               ((Q[w] >> (8 * b)) & 0xffu)];
+            }
     }
-    for (; i < m; ++i) acc += sdtN[(i << 8) + (cu[i] << 4) + cv[i]];
+    return acc > 255u ? 255u : acc;
+}
+
+// The same sum for one pair, split across the warp (same value in every lane).
+__device__ __forceinline__ uint32_t sdt_sum_warp(const uint8_t *tab, int m,
+                                                 const uint8_t *__restrict__ p,
+                                                 const uint8_t *__restrict__ q, int lane) {
+    uint32_t acc = 0;
+    for (int i = lane; i < m; i += 32) acc += tab[(i << 8) + (__ldg(p + i) << 4) + __ldg(q + i)];
+    acc = __reduce_add_sync(0xffffffffu, acc);
     return acc > 255u ? 255u : acc;
 }
 
@@ -68,6 +85,8 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
     const int wid = threadIdx.x >> 5;
     uint8_t *base = smem + 2 * tb + wid * L.total;
     int32_t *row_s = reinterpret_cast<int32_t *>(base + L.row);
+    uint8_t *rowd_s = base + L.rowd;
+    uint8_t *keptd = base + L.keptd;
     unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
     int32_t *kept = reinterpret_cast<int32_t *>(base + L.kept);
     uint8_t *kcodes = base + L.kcodes;
@@ -97,10 +116,15 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
         int32_t *ids = l0 ? g.adj0 + rowg * g.cap0p : g.adjU + (rowg - g.n) * g.capUp;
         int32_t *cntp = l0 ? g.cnt0 + rowg : g.cntU + (rowg - g.n);
         uint8_t *consp = l0 ? g.cons0 + rowg : g.consU + (rowg - g.n);
-        for (int j = lane; j < cap; j += 32) row_s[j] = ids[j];
+        uint8_t *distp = l0 ? g.dist0 + rowg * g.cap0p : g.distU + (rowg - g.n) * g.capUp;
         int cnt = *cntp;
         int cons = *consp;
+        for (int j = lane; j < cap; j += 32) {
+            row_s[j] = ids[j];
+            if (cons) rowd_s[j] = distp[j];
+        }
         const uint8_t *cy = g.codes + (size_t)y * g.mpad;
+        bool dirty = false;
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
             const int x = (int)(keys[t] & 0xffffffffu);
@@ -108,20 +132,21 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 if (lane == 0) row_s[cnt] = x;
                 ++cnt;
                 cons = 0;
+                dirty = true;
                 ++n_app;
                 __syncwarp();
                 continue;
             }
             ++n_prune;
             const uint8_t *cx = g.codes + (size_t)x * g.mpad;
-            const uint32_t dx = sdt_sum_u_uniform(sdtN, g.m, cy, cx);
+            const uint32_t dx = sdt_sum_warp(sdtN, g.m, cy, cx, lane);
             const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
             int nk = 0;
             if (cons) {
-                // L = row_s is sorted by (d, id) and pairwise non-dominated.
-                // p = position of x among the candidates; x survives iff no
-                // L_j (j < p) dominates it; L_j (j >= p) drops iff x survives
-                // and dominates it.
+                // L = row_s is sorted by (d, id) and pairwise non-dominated, its
+                // distances d(y, L_j) cached in rowd_s.  p = position of x among
+                // the candidates; x survives iff no L_j (j < p) dominates it;
+                // L_j (j >= p) drops iff x survives and dominates it.
                 int p = 0;
                 unsigned long long kj[kRowChunks];
                 bool domx = false;
@@ -131,16 +156,16 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                     kj[c] = KEY_MAX;
                     if (j < cap) {
                         const int uj = row_s[j];
-                        const uint8_t *cu = g.codes + (size_t)uj * g.mpad;
-                        const uint32_t dj = sdt_sum_u_uniform(sdtN, g.m, cy, cu);
-                        kj[c] = ((unsigned long long)dj << 32) | (uint32_t)uj;
-                        if (kj[c] < kx) domx |= sdt_sum_rows(sdtT, g.m, cu, cx) < dx;
+                        kj[c] = ((unsigned long long)rowd_s[j] << 32) | (uint32_t)uj;
+                        if (kj[c] < kx)
+                            domx |= sdt_sum16(sdtT, g.m, cx, g.codes + (size_t)uj * g.mpad) < dx;
                     }
                     p += __popc(__ballot_sync(0xffffffffu, kj[c] < kx));
                 }
                 const bool xkept = !__any_sync(0xffffffffu, domx);
                 n_sym += cap + 1 + p;
-                if (xkept) n_sym += cap - p;
+                if (!xkept) continue;  // the row is unchanged (and still consistent)
+                n_sym += cap - p;
                 // survivors in candidate order: L_0..L_{p-1}, x, L_p..
 #pragma unroll
                 for (int c = 0; c < kRowChunks; ++c) {
@@ -150,31 +175,33 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                     if (j < cap) {
                         uj = (int)(kj[c] & 0xffffffffu);
                         keep = true;
-                        if (j >= p && xkept)
-                            keep = sdt_sum_u_uniform(sdtN, g.m, cx, g.codes + (size_t)uj * g.mpad) >=
+                        if (j >= p)
+                            keep = sdt_sum16(sdtN, g.m, cx, g.codes + (size_t)uj * g.mpad) >=
                                    (uint32_t)(kj[c] >> 32);
                     }
                     const unsigned bk = __ballot_sync(0xffffffffu, keep);
                     if (keep) {
                         int pos = nk + __popc(bk & ((1u << lane) - 1u));
-                        if (j >= p && xkept) ++pos;  // x sits at position p
-                        if (pos < cap) kept[pos] = uj;
+                        if (j >= p) ++pos;  // x sits at position p
+                        if (pos < cap) {
+                            kept[pos] = uj;
+                            keptd[pos] = (uint8_t)(kj[c] >> 32);
+                        }
                     }
                     nk += __popc(bk);
                 }
-                if (xkept) {
-                    if (lane == 0 && p < cap) kept[p] = x;
-                    ++nk;
+                if (lane == 0 && p < cap) {
+                    kept[p] = x;
+                    keptd[p] = (uint8_t)dx;
                 }
-                nk = min(nk, cap);
+                nk = min(nk + 1, cap);
             } else {
                 ++n_full;
                 // candidates row + x with (d, id) keys, sorted by rank
                 for (int j = lane; j <= cap; j += 32) {
                     if (j < cap) {
                         const int uj = row_s[j];
-                        const uint32_t dj =
-                            sdt_sum_u_uniform(sdtN, g.m, cy, g.codes + (size_t)uj * g.mpad);
+                        const uint32_t dj = sdt_sum16(sdtN, g.m, cy, g.codes + (size_t)uj * g.mpad);
                         cand[j] = ((unsigned long long)dj << 32) | (uint32_t)uj;
                     } else {
                         cand[j] = kx;
@@ -205,19 +232,28 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                         v = (int)(k & 0xffffffffu);
                         dv = (double)(uint32_t)(k >> 32);
                     },
-                    kept, kcodes, lane, &sym);
+                    kept, kcodes, lane, &sym, keptd);
                 n_sym += cap + 1 + sym;
             }
             __syncwarp();
-            for (int j = lane; j < cap; j += 32) row_s[j] = j < nk ? kept[j] : -1;
+            for (int j = lane; j < cap; j += 32) {
+                row_s[j] = j < nk ? kept[j] : -1;
+                rowd_s[j] = j < nk ? keptd[j] : 0;
+            }
             cnt = nk;
             cons = 1;
+            dirty = true;
             __syncwarp();
         }
-        for (int j = lane; j < cap; j += 32) ids[j] = j < cnt ? row_s[j] : -1;
-        if (lane == 0) {
-            *cntp = cnt;
-            *consp = (uint8_t)cons;
+        if (dirty) {
+            for (int j = lane; j < cap; j += 32) {
+                ids[j] = j < cnt ? row_s[j] : -1;
+                if (cons) distp[j] = rowd_s[j];
+            }
+            if (lane == 0) {
+                *cntp = cnt;
+                *consp = (uint8_t)cons;
+            }
         }
         __syncwarp();
     }

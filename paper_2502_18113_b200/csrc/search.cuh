@@ -30,6 +30,7 @@ struct Graph {
     int32_t *adj0, *cnt0;
     int32_t *adjU, *cntU;
     uint8_t *cons0, *consU;  // row holds exactly a prune result, in order
+    uint8_t *dist0, *distU;  // per slot: SDT distance owner -> member (valid iff cons)
     const uint8_t *codes;    // n x mpad
     const int32_t *levels;
     const int64_t *uoff;

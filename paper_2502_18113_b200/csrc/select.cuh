@@ -58,11 +58,12 @@ __device__ __forceinline__ uint32_t sdt_sum_rows(const uint8_t *sdtT, int m, con
 // hook inputs).  Candidate code rows are read from `codes` (global, row
 // stride cs bytes, 4-byte aligned, zero padded to mpad).  Returns the number
 // kept; kept ids in kept_ids[0..nk), their codes in kept_codes rows.
+// kept_d (optional): the kept candidates' distances (< 256), as uint8.
 template <class Get>
 __device__ int warp_select_heur(const uint8_t *sdtT, int m, int mpad,
                                 const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
                                 Get get, int32_t *kept_ids, uint8_t *kept_codes, int lane,
-                                unsigned long long *sym_count) {
+                                unsigned long long *sym_count, uint8_t *kept_d = nullptr) {
     const int ks = kept_stride(mpad);
     int nk = 0;
     unsigned long long sym = 0;
@@ -78,7 +79,10 @@ __device__ int warp_select_heur(const uint8_t *sdtT, int m, int mpad,
         }
         sym += nk;
         if (!__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) kept_ids[nk] = v;
+            if (lane == 0) {
+                kept_ids[nk] = v;
+                if (kept_d) kept_d[nk] = (uint8_t)dv;
+            }
             for (int i = lane * 4; i < mpad; i += 128)
                 *reinterpret_cast<uint32_t *>(kept_codes + nk * ks + i) =
                     *reinterpret_cast<const uint32_t *>(cv + i);
