@@ -27,6 +27,9 @@ INCLUDE = PKG.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
               "--extended-lambda", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v"]
+# diagnostics build: per-phase SM cycles of the layer search in point_stats
+if os.environ.get("FLASHANN_B200_PHASE_PROFILE") == "1":
+    NVCC_FLAGS.append("-DFA_PHASE_PROFILE=1")
 
 
 def nvcc() -> str:

@@ -400,8 +400,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int capmax = std::max(g.cap0, g.capU);
     WarpLayout L;
     L.init(g.mpad, C, capmax,
-           pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2),
-           gb.expand);
+           pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2,
+                          (size_t)round_up(C, 32) * 8 + round_up(R * 4, 16) +
+                              (size_t)R * kept_stride(g.mpad)),
+           gb.expand, true);
     const size_t sdt_bytes = round_up(g.m * 256, 128);
     const size_t smem_search = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",

@@ -149,21 +149,29 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 // L_j (j >= p) drops iff x survives and dominates it.
                 int p = 0;
                 unsigned long long kj[kRowChunks];
-                bool domx = false;
 #pragma unroll
                 for (int c = 0; c < kRowChunks; ++c) {
                     const int j = c * 32 + lane;
                     kj[c] = KEY_MAX;
-                    if (j < cap) {
-                        const int uj = row_s[j];
-                        kj[c] = ((unsigned long long)rowd_s[j] << 32) | (uint32_t)uj;
-                        if (kj[c] < kx)
-                            domx |= sdt_sum16(sdtT, g.m, cx, g.codes + (size_t)uj * g.mpad) < dx;
-                    }
+                    if (j < cap) kj[c] = ((unsigned long long)rowd_s[j] << 32) | (uint32_t)row_s[j];
                     p += __popc(__ballot_sync(0xffffffffu, kj[c] < kx));
                 }
-                const bool xkept = !__any_sync(0xffffffffu, domx);
                 n_sym += cap + 1 + p;
+                // domination of x, one 32-member chunk at a time: the first
+                // dominating member settles it
+                bool xkept = true;
+#pragma unroll
+                for (int c = 0; c < kRowChunks; ++c) {
+                    if (c * 32 >= p) break;
+                    bool domx = false;
+                    if (kj[c] < kx)
+                        domx = sdt_sum16(sdtT, g.m, cx,
+                                         g.codes + (size_t)(uint32_t)kj[c] * g.mpad) < dx;
+                    if (__any_sync(0xffffffffu, domx)) {
+                        xkept = false;
+                        break;
+                    }
+                }
                 if (!xkept) continue;  // the row is unchanged (and still consistent)
                 n_sym += cap - p;
                 // survivors in candidate order: L_0..L_{p-1}, x, L_p..

@@ -77,20 +77,31 @@ struct WarpLayout {
     int adt, T, S, TQ, fresh, fdist, hash, total;
     int hash_log2;
     __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
-    __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand) {
+    // t_alias: the sorted results live at the end of the visited table (the
+    // build: the table is dead once a layer search has sorted its results, and
+    // forward selection's kept rows use only its start)
+    __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand,
+                                  bool t_alias = false) {
         hash_log2 = hlog2;
         const int nc = cand_capacity(expand, capmax);
         const int Wp = round_up(W, 32);
+        const bool alias = t_alias && W <= kRegSetMax;
+        const int hbytes = 16 << vis_buckets_log2(hlog2);
         int o = 0;
         adt = o; o += round_up(adt_bytes(mpad), 16);
         // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
-        T = o; o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
-        o = round_up(o, 16);
+        if (!alias) {
+            T = o;
+            o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
+            o = round_up(o, 16);
+        }
         S = o; o += 2 * nc * 4;                     // candidate keys (two buffers)
         TQ = o; o += Wp * 4;                        // tie queue, then the final sort
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
-        hash = o; o += 16 << vis_buckets_log2(hlog2);
+        o = round_up(o, 16);
+        hash = o; o += hbytes;
+        if (alias) T = hash + hbytes - Wp * 8;
         total = round_up(o, 128);
     }
 };
@@ -186,15 +197,10 @@ __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
     return v;
 }
 
-// two bits per 32-bit word: half 0 / half 1 equal to zero
-__device__ __forceinline__ uint32_t zero_halves(uint32_t w) {
-    return (uint32_t)((w & 0xffffu) == 0u) | ((uint32_t)((w >> 16) == 0u) << 1);
-}
-
 struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
-    uint32_t usable;   // mask of usable slots per bucket
+    int nslots;        // usable slots per bucket
     uint32_t *G;       // global tier of this warp slot
     uint32_t *gepoch;  // epoch counter of this warp slot
     uint32_t epoch;
@@ -210,7 +216,7 @@ struct VisitedSet {
     __device__ void begin(void *H, int hlog2, uint32_t *gtables, uint32_t *gepochs, int lane) {
         B = reinterpret_cast<uint4 *>(H);
         kb = vis_buckets_log2(hlog2);
-        usable = (1u << vis_bucket_slots(hlog2)) - 1u;
+        nslots = vis_bucket_slots(hlog2);
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
         gcount = 0;
@@ -247,11 +253,11 @@ struct VisitedSet {
             if ((__vcmpeq2(v.x, rr) | __vcmpeq2(v.y, rr) | __vcmpeq2(v.z, rr) |
                  __vcmpeq2(v.w, rr)) != 0u)
                 return 0;
-            const uint32_t zm = (zero_halves(v.x) | (zero_halves(v.y) << 2) |
-                                 (zero_halves(v.z) << 4) | (zero_halves(v.w) << 6)) &
-                                usable;
-            if (zm == 0u) break;
-            const int e = __ffs(zm) - 1;
+            // slots fill in order: the first empty slot = the number of filled ones
+            const uint32_t f = __vsetne2(v.x, 0u) + __vsetne2(v.y, 0u) + __vsetne2(v.z, 0u) +
+                               __vsetne2(v.w, 0u);
+            const int e = (int)((f & 0xffffu) + (f >> 16));
+            if (e >= nslots) break;
             const int wi = e >> 1;
             const uint32_t ow = wi == 0 ? v.x : wi == 1 ? v.y : wi == 2 ? v.z : v.w;
             const uint32_t nw = ow | (r << (16 * (e & 1)));
@@ -512,46 +518,43 @@ template <int J>
 struct RegSet {
     uint32_t key[J];
     uint32_t fl;
-    // smallest key over live unexpanded slots (dsel < 0) or over live slots at
-    // distance dsel; has = any such slot
-    __device__ __forceinline__ bool local_min(int ts, int lane, int dsel, uint32_t &best,
-                                              int &bj) const {
-        bool has = false;
-        best = 0xffffffffu;
-        bj = 0;
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const bool ok = lane + 32 * j < ts &&
-                            (dsel < 0 ? ((fl >> j) & 1u) == 0u : (int)(key[j] >> 24) == dsel);
-            if (ok && (!has || key[j] < best)) {
-                best = key[j];
-                bj = j;
-                has = true;
-            }
-        }
-        return has;
+    // this lane's live slots when the set holds ts entries (a prefix of j)
+    __device__ __forceinline__ static uint32_t live_mask(int ts, int lane) {
+        const int c = ts > lane ? (ts - lane + 31) >> 5 : 0;
+        return c >= 32 ? 0xffffffffu : (1u << c) - 1u;
     }
-    // smallest and second smallest live unexpanded keys of this lane
-    __device__ __forceinline__ int local_min2(int ts, int lane, uint32_t &b1, int &j1,
-                                              uint32_t &b2) const {
-        int n = 0;
+    // smallest key (b1, slot j1; j1 = -1 if none) and second smallest key b2
+    // over the slots of mask um
+    __device__ __forceinline__ void min2(uint32_t um, uint32_t &b1, int &j1, uint32_t &b2) const {
         b1 = b2 = 0xffffffffu;
-        j1 = 0;
+        j1 = -1;
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            if (lane + 32 * j < ts && ((fl >> j) & 1u) == 0u) {
-                const uint32_t k = key[j];
-                if (n == 0 || k < b1) {
+            const uint32_t k = key[j];
+            if ((um >> j) & 1u) {
+                if (j1 < 0 || k < b1) {
                     b2 = b1;
                     b1 = k;
                     j1 = j;
-                } else if (n == 1 || k < b2) {
-                    b2 = k;
+                } else {
+                    b2 = min(b2, k);
                 }
-                ++n;
             }
         }
-        return n;
+    }
+    // eviction victim over the slots of mask lm: the largest distance, smallest
+    // tie among those = the largest key ^ 0xFFFFFF (vf; vj = -1 if none)
+    __device__ __forceinline__ void victim(uint32_t lm, uint32_t &vf, int &vj) const {
+        vf = 0;
+        vj = -1;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const uint32_t kf = key[j] ^ 0xffffffu;
+            if (((lm >> j) & 1u) && (vj < 0 || kf > vf)) {
+                vf = kf;
+                vj = j;
+            }
+        }
     }
     __device__ __forceinline__ uint32_t maxd(int ts, int lane) const {
         uint32_t mx = 0;
@@ -573,6 +576,14 @@ __device__ __forceinline__ bool warp_pick(bool has, uint32_t best, uint32_t &m, 
     const unsigned any = __ballot_sync(0xffffffffu, has);
     if (!any) return false;
     m = __reduce_min_sync(0xffffffffu, has ? best : 0xffffffffu);
+    owner = __ffs(__ballot_sync(0xffffffffu, has && best == m)) - 1;
+    return true;
+}
+// warp maximum, same contract
+__device__ __forceinline__ bool warp_pick_max(bool has, uint32_t best, uint32_t &m, int &owner) {
+    const unsigned any = __ballot_sync(0xffffffffu, has);
+    if (!any) return false;
+    m = __reduce_max_sync(0xffffffffu, has ? best : 0u);
     owner = __ffs(__ballot_sync(0xffffffffu, has && best == m)) - 1;
     return true;
 }
@@ -615,7 +626,9 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         if (EM == 1) {
             uint32_t b1, b2;
             int j1;
-            const int nl = rs.local_min2(ts, lane, b1, j1, b2);
+            const uint32_t um = RegSet<J>::live_mask(ts, lane) & ~rs.fl;
+            rs.min2(um, b1, j1, b2);
+            const int nl = __popc(um);
             uint32_t m = 0;
             int owner = -1;
             const bool anyT = warp_pick(nl > 0, b1, m, owner);
@@ -655,9 +668,10 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
 #pragma unroll
             for (int r = 0; r < EM; ++r) {
                 if (r >= E) break;
-                uint32_t best;
+                uint32_t best, b2;
                 int bj;
-                const bool has = rs.local_min(ts, lane, -1, best, bj);
+                rs.min2(RegSet<J>::live_mask(ts, lane) & ~rs.fl, best, bj, b2);
+                const bool has = bj >= 0;
                 uint32_t m = 0;
                 int owner = -1;
                 const bool anyT = warp_pick(has, best, m, owner);
@@ -748,27 +762,44 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             }
         }
         ts += nfill;
-        if (ts == W) wd = rs.maxd(ts, lane);
-        for (int j = nfill; j < ns; ++j) {
-            const uint32_t s = src[j];
-            if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
-            // evict the smallest key of the worst-distance group
-            uint32_t best;
-            int bj;
-            const bool has = rs.local_min(ts, lane, (int)wd, best, bj);
-            uint32_t m = 0;
-            int owner = 0;
-            warp_pick(has, best, m, owner);
-            const uint32_t expd = __shfl_sync(FULL, (rs.fl >> bj) & 1u, owner);
-            if (!expd) {
-                if (lane == 0) TQ[tq_t] = (int32_t)(m & 0xffffffu);
-                ++tq_t;
+        // worst distance wd: recomputed lazily (as the next victim's distance);
+        // stale = the set changed since wd was last known
+        bool stale = ts == W && nfill > 0;
+        if (nfill < ns) {
+            const uint32_t lm = RegSet<J>::live_mask(ts, lane);
+            for (int j = nfill; j < ns; ++j) {
+                const uint32_t s = src[j];
+                // victim: largest distance, smallest tie; its distance is the
+                // current worst
+                uint32_t vf;
+                int vj;
+                rs.victim(lm, vf, vj);
+                uint32_t m = 0;
+                int owner = 0;
+                warp_pick_max(vj >= 0, vf, m, owner);
+                const uint32_t cur = m >> 24;
+                if (cur < wd) {
+                    // the evicted ties are beyond the new worst (none before the
+                    // set first fills)
+                    if (wd != 0xffffffffu) tq_h = tq_t = 0;
+                    wd = cur;
+                }
+                stale = false;
+                if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+                const uint32_t expd = __shfl_sync(FULL, (rs.fl >> vj) & 1u, owner);
+                if (!expd) {
+                    if (lane == 0) TQ[tq_t] = (int32_t)((m ^ 0xffffffu) & 0xffffffu);
+                    ++tq_t;
+                }
+                if (lane == owner) rs.put(vj, s);
+                stale = true;
             }
-            if (lane == owner) rs.put(bj, s);
+        }
+        if (stale) {
             const uint32_t nwd = rs.maxd(ts, lane);
             if (nwd < wd) {
+                if (wd != 0xffffffffu) tq_h = tq_t = 0;
                 wd = nwd;
-                tq_h = tq_t = 0;  // the evicted ties are beyond the new worst
             }
         }
         __syncwarp();
