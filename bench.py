@@ -129,6 +129,21 @@ def ref_cpu_build(prov_full, levels_fn, n_sub, C, R, threads):
     return dt, n_sub / dt
 
 
+def size_cpu_sample(build, n_max, target_s, n0=20_000):
+    """Grow a prefix by doubling until one reference build takes about
+    target_s / 3 (the CPU rate falls steeply with n once the graph leaves the
+    caches, so a small calibration cannot be extrapolated).  Returns
+    (n, seconds, vec/s) of the last build, or None."""
+    n = min(n_max, n0)
+    r = build(n)
+    if r is None:
+        return None
+    while r[0] < target_s / 3.0 and n < n_max:
+        n = min(n_max, 2 * n)
+        r = build(n)
+    return n, r[0], r[1]
+
+
 def cpu_prov(data, model):
     """Reference-shaped prov dict from a trained model (host arrays)."""
     proj = model["proj_fn"](data)
@@ -157,11 +172,10 @@ def run_reference(args):
     model = train_np.train(train_np.training_sample(data, 100_000, 0), c["d_f"], c["m_f"], 0, 10)
     prov = cpu_prov(data, model)
     lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
-    # size each step so the whole run stays within ~3 minutes (calibrated on
-    # 20K vectors; the rate falls with n, hence the 0.5 margin)
-    _, rate = ref_cpu_build(prov, lvf, 20_000, c["efC"], c["M"], threads)
+    # size each step so the whole run stays within ~3 minutes
     steps = args.steps + args.warmup
-    n_sub = int(min(args.ref_max, max(20_000, 0.5 * rate * 150.0 / steps)))
+    n_sub = size_cpu_sample(lambda k: ref_cpu_build(prov, lvf, k, c["efC"], c["M"], threads),
+                            args.ref_max, 150.0 / steps)[0]
     for _ in range(args.warmup):
         ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)
     times = [ref_cpu_build(prov, lvf, n_sub, c["efC"], c["M"], threads)[0]
@@ -367,14 +381,15 @@ def main():
                   "sdt": model.sdt, "dist_min": model.dist_min, "dist_max": model.dist_max}
             cprov = provider.core_arrays()
             lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
-            # calibrate on 20K vectors; CPU throughput falls with n, so the
-            # bounded sample is sized conservatively from that rate
-            cal = ref_cpu_build(cprov, lvf, min(n, 20_000), c["efC"], c["M"], threads)
-            if cal is None:
+            # bounded sample: the largest doubling of a 20K prefix whose build
+            # stays near cpu_seconds
+            r = size_cpu_sample(
+                lambda k: ref_cpu_build(cprov, lvf, k, c["efC"], c["M"], threads), n,
+                args.cpu_seconds)
+            if r is None:
                 out["cpu_baseline"] = None
             else:
-                n_cpu = int(min(n, max(20_000, 0.5 * cal[1] * args.cpu_seconds)))
-                dt, rate = ref_cpu_build(cprov, lvf, n_cpu, c["efC"], c["M"], threads)
+                n_cpu, dt, rate = r
                 out["cpu_baseline"] = {
                     "value": rate, "unit": "vectors/s", "cores": threads, "kind": "reference",
                     "sample": f"first {n_cpu} of {n} vectors (prefix, same model), reference "
