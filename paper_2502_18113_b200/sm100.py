@@ -38,8 +38,8 @@ KIND_FLASH = 4
 KERNEL_NAMES = ("sm100",)
 
 BUILD_OPTIONS = {
-    "batch_max": int(os.environ.get("FLASHANN_B200_BATCH_MAX", "16384")),
-    "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.1")),
+    "batch_max": int(os.environ.get("FLASHANN_B200_BATCH_MAX", "65536")),
+    "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.2")),
     "seq_prefix": int(os.environ.get("FLASHANN_B200_SEQ_PREFIX", "0")),
     "hash_log2": int(os.environ.get("FLASHANN_B200_HASH_LOG2", "0")),
     # tie order among equal distances during insertion searches: 2 = id

@@ -98,6 +98,9 @@ def main():
         "f02": dict(batch_max=4096, batch_frac=0.02, seq_prefix=0),
         "f05": dict(batch_max=4096, batch_frac=0.05, seq_prefix=0),
         "f10": dict(batch_max=4096, batch_frac=0.10, seq_prefix=0),
+        "f10b16k": dict(batch_max=16384, batch_frac=0.10, seq_prefix=0),
+        "f20b64k": dict(batch_max=65536, batch_frac=0.20, seq_prefix=0),
+        "f30b64k": dict(batch_max=65536, batch_frac=0.30, seq_prefix=0),
         "default": dict(sm100.BUILD_OPTIONS),
     }
     schedules = {k: presets[k] for k in args.schedules.split(",")}
