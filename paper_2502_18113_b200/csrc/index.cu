@@ -353,8 +353,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         return FA_OK;
     }
     FA_CHECK_ARG(ix->d.proj, "build needs the projected vectors (per-insertion tables)");
-    const int Bmax = opts->batch_max > 0 ? opts->batch_max : 4096;
-    const double frac = opts->batch_frac > 0 ? opts->batch_frac : 0.02;
+    const int Bmax = opts->batch_max > 0 ? opts->batch_max : 65536;
+    const double frac = opts->batch_frac > 0 ? opts->batch_frac : 0.2;
     const int prefix = opts->seq_prefix >= 0 ? opts->seq_prefix : 256;
 
     // ---- schedule (pure function of the layer draws) ----
