@@ -157,7 +157,9 @@ typedef struct {
     int batch_max;        /* largest insertion batch (0 = default)               */
     double batch_frac;    /* batch <= frac * |inserted| (0 = default)            */
     int seq_prefix;       /* first vertices inserted one per batch (-1 default)  */
-    int hash_log2;        /* visited-hash size per warp = 2^hash_log2 (0 = auto) */
+    int hash_log2;        /* shared visited table: 2^hash_log2 16-bit slots per
+                             warp, >= 2^12 stored (0 = auto; 9..11 use only
+                             2^hash_log2 / 512 slots per bucket)            */
     int profile;          /* 1: time every kernel class with CUDA events        */
     int tie;              /* order among equal distances in the searches:
                              0 vertex id (reference semantic core, _pycore.py),
@@ -167,7 +169,8 @@ typedef struct {
                              insertion (<= 1: one, the semantic core; max 8)  */
     int64_t *point_stats; /* optional DEVICE n x 8 per inserted vertex
                              (diagnostics): expansions, SM cycles, cycles in
-                             pop / row+visited / distances / acceptance,
+                             pop / row+visited / distances / acceptance (0
+                             unless built with FA_PHASE_PROFILE=1),
                              forward-selection cycles, distance evaluations   */
 } fa_build_opts;
 
