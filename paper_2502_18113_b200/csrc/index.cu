@@ -10,6 +10,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -425,6 +427,16 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, search_fn,
                                                           kSearchWarps * 32, smem_search));
     const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * kNumSMs;
+    // carve out only the shared memory the resident CTAs use: the rest stays
+    // L1, which holds the transposed SDT and the hot code rows
+    {
+        const double need = (double)std::max(search_per_sm, 1) * (smem_search + 1024);
+        int pct = (int)std::ceil(100.0 * need / (228.0 * 1024.0));
+        if (const char *e = getenv("FLASHANN_B200_CARVEOUT")) pct = atoi(e);
+        FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     std::min(100, std::max(0, pct))));
+    }
 
     uint8_t *adt_batch = nullptr, *sdtT = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
