@@ -15,12 +15,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) build_search_kernel(
     int64_t *__restrict__ stats, int *__restrict__ work) {
     // sdtT: the transposed SDT in global memory (L1-resident; keeping it out of
     // shared memory leaves room for one more CTA per SM)
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
     WarpWS ws(smem + wid * L.total, L);
-    int32_t *kept = reinterpret_cast<int32_t *>(ws.H);
-    uint8_t *kcodes = reinterpret_cast<uint8_t *>(ws.H) + round_up(R * 4, 16);
     CounterTotals total;
     // persistent warps pull vertices from the batch; a slow search never holds
     // its CTA siblings' slots idle
@@ -58,14 +56,15 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) build_search_kernel(
             unsigned long long sym = 0;
             const unsigned long long *T = ws.T;
             const long long t_sel = clock64();
-            int nsel = warp_select_heur(
+            int32_t *kept;
+            int nsel = warp_select_tv(
                 sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
-                [&](int j, int &v, double &dv) {
+                [&](int j, int &v, uint32_t &dv) {
                     unsigned long long k = T[j];
                     v = to.back((uint32_t)key_id(k));
-                    dv = (double)key_d(k);
+                    dv = key_d(k);
                 },
-                kept, kcodes, lane, &sym);
+                reinterpret_cast<uint8_t *>(ws.H), lane, &sym, kept);
             cnt.sym += sym;
             sel_cycles += clock64() - t_sel;
             // forward row of x (write_forward, _core.pyx:424-438); rows past the

@@ -403,8 +403,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     WarpLayout L;
     L.init(g.mpad, C, capmax,
            pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2,
-                          (size_t)round_up(C, 32) * 8 + round_up(R * 4, 16) +
-                              (size_t)R * kept_stride(g.mpad)),
+                          (size_t)round_up(C, 32) * 8 + select_tv_bytes(g.m, g.mpad, R)),
            gb.expand, true);
     const size_t sdt_bytes = round_up(g.m * 256, 128);
     const size_t smem_search = (size_t)kSearchWarps * L.total;

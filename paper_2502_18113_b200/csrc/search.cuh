@@ -99,10 +99,10 @@ struct WarpLayout {
         TQ = o; o += Wp * 4;                        // tie queue, then the final sort
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
-        o = round_up(o, 16);
+        o = round_up(o, 256);  // forward selection's tables are 256-aligned
         hash = o; o += hbytes;
         if (alias) T = hash + hbytes - Wp * 8;
-        total = round_up(o, 128);
+        total = round_up(o, 256);
     }
 };
 

@@ -94,4 +94,88 @@ __device__ int warp_select_heur(const uint8_t *sdtT, int m, int mpad,
     return nk;
 }
 
+// ---- forward selection of the build (K5, per-candidate table variant) ------
+// The same decisions as warp_select_heur for integer candidate distances.
+// For candidate v, sdt(u, v) = sum_i sdt[i][u_i][v_i] = sum_i Tv[i][u_i] with
+// Tv[i][*] = sdtT row (i, v_i): the warp copies v's m table rows (16 B each,
+// one 16-byte load per row) into shared memory, then lane t sums kept[t]'s
+// lookups.  Kept code rows are stored pre-offset: byte i holds
+// (i % 16) * 16 + u_i, so within a 16-subspace chunk (256 table bytes) one PRMT
+// merges the chunk base (256-aligned) with the byte into the lookup address.
+__host__ __device__ inline int kept_enc_stride(int mpad) { return mpad + 16; }
+__host__ __device__ inline int select_tv_bytes(int m, int mpad, int cap) {
+    return round_up(cap * 4, 256) + round_up(cap * kept_enc_stride(mpad), 256) +
+           round_up(mpad * 16, 256);
+}
+
+// chunk-local row offsets (i % 16) * 16 of the four bytes of code word q
+__device__ __forceinline__ uint32_t kept_enc_add(int q) {
+    return 0x30201000u + 0x40404040u * (uint32_t)(q & 3);
+}
+
+template <class Get>
+__device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
+                              const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
+                              Get get, uint8_t *ws, int lane, unsigned long long *sym_count,
+                              int32_t *&kept_out) {
+    const int ks = kept_enc_stride(mpad);
+    int32_t *kept_ids = reinterpret_cast<int32_t *>(ws);
+    uint8_t *kenc = ws + round_up(cap * 4, 256);
+    uint8_t *Tv = kenc + round_up(cap * ks, 256);
+    kept_out = kept_ids;
+    int nk = 0;
+    unsigned long long sym = 0;
+    for (int j = 0; j < ncand && nk < cap; ++j) {
+        int v;
+        uint32_t dv;
+        get(j, v, dv);
+        const uint8_t *cv = codes + (size_t)v * cs;
+        bool bad = false;
+        if (nk > 0) {
+            for (int i = lane; i < mpad; i += 32) {
+                uint4 row = make_uint4(0, 0, 0, 0);
+                if (i < m)
+                    row = __ldg(reinterpret_cast<const uint4 *>(sdtT + (i << 8) +
+                                                                 ((uint32_t)__ldg(cv + i) << 4)));
+                *reinterpret_cast<uint4 *>(Tv + i * 16) = row;
+            }
+            __syncwarp();
+            const uint32_t tv = (uint32_t)__cvta_generic_to_shared(Tv);
+            for (int t = lane; t < nk; t += 32) {
+                const uint8_t *ku = kenc + t * ks;
+                uint32_t acc = 0;
+                for (int c = 0; c < mpad; c += 16) {
+                    const uint4 w = *reinterpret_cast<const uint4 *>(ku + c);
+                    const uint32_t base = tv + (uint32_t)c * 16u;  // 256-aligned
+                    const uint32_t W[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t b[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            uint32_t a = prmt(W[q], base, 0x7650u + (uint32_t)k);
+                            uint32_t x;
+                            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x) : "r"(a));
+                            b[k] = x;
+                        }
+                        acc += b[0] + b[1] + b[2] + b[3];
+                    }
+                }
+                bad |= (acc > 255u ? 255u : acc) < dv;
+            }
+            sym += nk;
+        }
+        if (!__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) kept_ids[nk] = v;
+            for (int q = lane; q < mpad / 4; q += 32)
+                *reinterpret_cast<uint32_t *>(kenc + nk * ks + 4 * q) =
+                    __ldg(reinterpret_cast<const uint32_t *>(cv) + q) + kept_enc_add(q);
+            ++nk;
+        }
+        __syncwarp();
+    }
+    if (sym_count && lane == 0) *sym_count += sym;
+    return nk;
+}
+
 }  // namespace fa
