@@ -588,6 +588,39 @@ __device__ __forceinline__ bool warp_pick_max(bool has, uint32_t best, uint32_t 
     return true;
 }
 
+// Ascending bitonic sort of the warp's 32 * J register keys; element
+// e = 32 j + lane lives in key[j] of lane `lane`.
+template <int J>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&k)[J], int lane) {
+    constexpr int N = 32 * J;
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                const int rsd = stride >> 5;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    if ((j & rsd) == 0) {
+                        const bool up = ((32 * j) & size) == 0;
+                        const uint32_t a = k[j], b = k[j | rsd];
+                        k[j] = up ? min(a, b) : max(a, b);
+                        k[j | rsd] = up ? max(a, b) : min(a, b);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, k[j], stride);
+                    const bool up = ((32 * j + lane) & size) == 0;
+                    const bool lower = (lane & stride) == 0;
+                    k[j] = (up == lower) ? min(k[j], o) : max(k[j], o);
+                }
+            }
+        }
+    }
+}
+
 template <int J, int EM>
 __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int entry,
                                                  uint32_t entry_d, int W, const uint8_t *adt_s,
@@ -804,22 +837,16 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         }
         __syncwarp();
     }
-    // sort once: stage the keys (the tie queue's space is free now), rank by
-    // counting (keys are distinct) into the 64-bit slots
-    uint32_t *Ks = reinterpret_cast<uint32_t *>(TQ);
-    __syncwarp();
+    // sort once: bitonic network over the 32 * J register slots (empty slots
+    // hold the largest key and sort last), then the first ts go out
 #pragma unroll
     for (int j = 0; j < J; ++j)
-        if (lane + 32 * j < ts) Ks[lane + 32 * j] = rs.key[j];
-    __syncwarp();
+        if (lane + 32 * j >= ts) rs.key[j] = 0xffffffffu;
+    warp_bitonic<J>(rs.key, lane);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-        if (lane + 32 * j < ts) {
-            const uint32_t k = rs.key[j];
-            int r = 0;
-            for (int t = 0; t < ts; ++t) r += Ks[t] < k;
-            T[r] = make_key(k >> 24, (int)(k & 0xffffffu));
-        }
+        const int e = 32 * j + lane;
+        if (e < ts) T[e] = make_key(rs.key[j] >> 24, (int)(rs.key[j] & 0xffffffu));
     }
     __syncwarp();
     ts_out = ts;
