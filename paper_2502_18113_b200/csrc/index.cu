@@ -414,7 +414,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
     RL.init(capmax, g.mpad);
-    const size_t smem_rev = 2 * sdt_bytes + (size_t)kReverseWarps * RL.total;
+    const size_t smem_rev = (size_t)kReverseWarps * RL.total;
     FA_CUDA(cudaFuncSetAttribute(reverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));
 
@@ -529,7 +529,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         int rgrid = (int)std::min<int64_t>(rev_ctas, (b.nreq + 32 * kReverseWarps - 1) /
                                                           (32 * kReverseWarps) + 1);
         reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
-            gb, ix->d.sdt, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
+            gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL,
+            ctr);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
         launches += 4;

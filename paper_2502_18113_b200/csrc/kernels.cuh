@@ -74,16 +74,18 @@ QuerySearchFn query_search_variant(int W);
 LayerSearchFn layer_search_variant(int W);
 
 struct ReverseLayout {
-    int row, rowd, keptd, cand, kept, kcodes, total;
+    int tdom, tkeep, row, rowd, keptd, cand, kept, kcodes, total;
     __host__ __device__ void init(int capmax, int mpad) {
         int o = 0;
+        tdom = o; o += round_up(mpad * 16, 256);   // x's row tables (256-aligned)
+        tkeep = o; o += round_up(mpad * 16, 256);
         row = o; o += round_up(capmax, 32) * 4;
         rowd = o; o += round_up(capmax, 32);
         keptd = o; o += round_up(capmax, 32);
         cand = o; o += 128 * 8;
         kept = o; o += round_up(capmax, 32) * 4;
         kcodes = o; o += round_up(capmax * kept_stride(mpad), 16);
-        total = round_up(o, 128);
+        total = round_up(o, 256);
     }
 };
 
@@ -92,6 +94,7 @@ __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys
                                      int *__restrict__ next);
 
 __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,
+                               const uint8_t *__restrict__ sdtT,
                                const unsigned long long *__restrict__ keys, int64_t N,
                                const int64_t *__restrict__ heads, const int *__restrict__ nheads,
                                int *__restrict__ next, const int32_t *__restrict__ upper_owner,

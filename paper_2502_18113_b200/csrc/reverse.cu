@@ -69,21 +69,20 @@ __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys
     if (h) heads[base + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = i;
 }
 
-__global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
-    Graph g, const uint8_t *__restrict__ sdt, const unsigned long long *__restrict__ keys,
-    int64_t N, const int64_t *__restrict__ heads, const int *__restrict__ nheads,
-    int *__restrict__ next, const int32_t *__restrict__ upper_owner, ReverseLayout L,
-    unsigned long long *__restrict__ ctr) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int tb = round_up(g.m * 256, 128);
-    uint8_t *sdtN = smem;
-    uint8_t *sdtT = smem + tb;
-    for (int t = threadIdx.x; t < g.m * 256; t += blockDim.x) sdtN[t] = sdt[t];
-    stage_sdt_T(sdt, g.m, sdtT, threadIdx.x, blockDim.x);
-    __syncthreads();
+__global__ void __maxnreg__(96) reverse_kernel(
+    Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ sdtT,
+    const unsigned long long *__restrict__ keys, int64_t N, const int64_t *__restrict__ heads,
+    const int *__restrict__ nheads, int *__restrict__ next, const int32_t *__restrict__ upper_owner,
+    ReverseLayout L, unsigned long long *__restrict__ ctr) {
+    // sdt, sdtT: the SDT and its transpose in global memory (L1-resident)
+    extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
-    uint8_t *base = smem + 2 * tb + wid * L.total;
+    uint8_t *base = smem + wid * L.total;
+    uint8_t *tdom = base + L.tdom;
+    uint8_t *tkeep = base + L.tkeep;
+    const uint32_t tdom_a = (uint32_t)__cvta_generic_to_shared(tdom);
+    const uint32_t tkeep_a = (uint32_t)__cvta_generic_to_shared(tkeep);
     int32_t *row_s = reinterpret_cast<int32_t *>(base + L.row);
     uint8_t *rowd_s = base + L.rowd;
     uint8_t *keptd = base + L.keptd;
@@ -139,7 +138,7 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
             }
             ++n_prune;
             const uint8_t *cx = g.codes + (size_t)x * g.mpad;
-            const uint32_t dx = sdt_sum_warp(sdtN, g.m, cy, cx, lane);
+            const uint32_t dx = sdt_sum_warp(sdt, g.m, cy, cx, lane);
             const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
             int nk = 0;
             if (cons) {
@@ -160,13 +159,18 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 // domination of x, one 32-member chunk at a time: the first
                 // dominating member settles it
                 bool xkept = true;
+                if (p > 0) {
+                    // Tdom[i][c] = sdt[i][c][x_i]: d(L_j, x) = sum_i Tdom[i][L_j,i]
+                    build_row_table(sdtT, g.m, g.mpad, cx, tdom, lane);
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int c = 0; c < kRowChunks; ++c) {
                     if (c * 32 >= p) break;
                     bool domx = false;
                     if (kj[c] < kx)
-                        domx = sdt_sum16(sdtT, g.m, cx,
-                                         g.codes + (size_t)(uint32_t)kj[c] * g.mpad) < dx;
+                        domx = row_table_sum(tdom_a, g.codes + (size_t)(uint32_t)kj[c] * g.mpad,
+                                             g.mpad) < dx;
                     if (__any_sync(0xffffffffu, domx)) {
                         xkept = false;
                         break;
@@ -174,6 +178,11 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 }
                 if (!xkept) continue;  // the row is unchanged (and still consistent)
                 n_sym += cap - p;
+                if (p < cap) {
+                    // Tkeep[i][c] = sdt[i][x_i][c]: d(x, L_j) = sum_i Tkeep[i][L_j,i]
+                    build_row_table(sdt, g.m, g.mpad, cx, tkeep, lane);
+                    __syncwarp();
+                }
                 // survivors in candidate order: L_0..L_{p-1}, x, L_p..
 #pragma unroll
                 for (int c = 0; c < kRowChunks; ++c) {
@@ -184,8 +193,8 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                         uj = (int)(kj[c] & 0xffffffffu);
                         keep = true;
                         if (j >= p)
-                            keep = sdt_sum16(sdtN, g.m, cx, g.codes + (size_t)uj * g.mpad) >=
-                                   (uint32_t)(kj[c] >> 32);
+                            keep = row_table_sum(tkeep_a, g.codes + (size_t)uj * g.mpad,
+                                                 g.mpad) >= (uint32_t)(kj[c] >> 32);
                     }
                     const unsigned bk = __ballot_sync(0xffffffffu, keep);
                     if (keep) {
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(kReverseWarps * 32) reverse_kernel(
                 for (int j = lane; j <= cap; j += 32) {
                     if (j < cap) {
                         const int uj = row_s[j];
-                        const uint32_t dj = sdt_sum16(sdtN, g.m, cy, g.codes + (size_t)uj * g.mpad);
+                        const uint32_t dj = sdt_sum16(sdt, g.m, cy, g.codes + (size_t)uj * g.mpad);
                         cand[j] = ((unsigned long long)dj << 32) | (uint32_t)uj;
                     } else {
                         cand[j] = kx;

@@ -113,6 +113,44 @@ __device__ __forceinline__ uint32_t kept_enc_add(int q) {
     return 0x30201000u + 0x40404040u * (uint32_t)(q & 3);
 }
 
+// Copy the 16-byte rows tab[i][x_i] (i < m; zero rows up to mpad) of a
+// global m x 16 x 16 table into T (shared, 256-aligned): T[i][c] = tab[i][x_i][c].
+__device__ __forceinline__ void build_row_table(const uint8_t *__restrict__ tab, int m, int mpad,
+                                                const uint8_t *__restrict__ cx, uint8_t *T,
+                                                int lane) {
+    for (int i = lane; i < mpad; i += 32) {
+        uint4 row = make_uint4(0, 0, 0, 0);
+        if (i < m)
+            row = __ldg(reinterpret_cast<const uint4 *>(tab + (i << 8) +
+                                                         ((uint32_t)__ldg(cx + i) << 4)));
+        *reinterpret_cast<uint4 *>(T + i * 16) = row;
+    }
+}
+
+// sum_i T[i][u_i], saturated, for a raw code row u (global, 16-byte aligned,
+// zero padded to mpad); T at shared address tbase (256-aligned).
+__device__ __forceinline__ uint32_t row_table_sum(uint32_t tbase, const uint8_t *__restrict__ cu,
+                                                  int mpad) {
+    uint32_t acc = 0;
+    for (int c = 0; c < mpad; c += 16) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(cu + c));
+        const uint32_t base = tbase + (uint32_t)c * 16u;
+        const uint32_t W[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t e = W[q] + kept_enc_add(q);
+            uint32_t b[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t a = prmt(e, base, 0x7650u + (uint32_t)k);
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[k]) : "r"(a));
+            }
+            acc += b[0] + b[1] + b[2] + b[3];
+        }
+    }
+    return acc > 255u ? 255u : acc;
+}
+
 template <class Get>
 __device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
                               const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
