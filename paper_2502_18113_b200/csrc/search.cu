@@ -44,7 +44,7 @@ __device__ __forceinline__ float warp_l2_group(const float *q, const float *v, i
 // width ef, optional exact rerank of the first rerank_depth results with
 // (d, id) ordering (fa_sort_pairs), then the first k.
 template <int J>
-__global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
+__global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     Graph g, const uint8_t *__restrict__ adt_q, int nq, int ep, int ml, int ef, int k,
     int rerank_depth, const float *__restrict__ vecs, int dim, const float *__restrict__ queries,
     WarpLayout L, int64_t *__restrict__ out_ids, double *__restrict__ out_d,
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32) query_search_kernel(
 
 // greedy_search_layer (_core.pyx:891-939): one layer from a given entry.
 template <int J>
-__global__ void __launch_bounds__(kSearchWarps * 32) layer_search_kernel(
+__global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     Graph g, const uint8_t *__restrict__ adt_q, int nq, const int64_t *__restrict__ entries,
     int width, int layer, WarpLayout L, int32_t *__restrict__ out_ids, double *__restrict__ out_d,
     int32_t *__restrict__ out_n, unsigned long long *__restrict__ ctr, int *err) {
