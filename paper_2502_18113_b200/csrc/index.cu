@@ -413,7 +413,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
-    RL.init(capmax, g.mpad);
+    RL.init(capmax, g.m, g.mpad);
     const size_t smem_rev = (size_t)kReverseWarps * RL.total;
     FA_CUDA(cudaFuncSetAttribute(reverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));

@@ -74,8 +74,8 @@ QuerySearchFn query_search_variant(int W);
 LayerSearchFn layer_search_variant(int W);
 
 struct ReverseLayout {
-    int tdom, tkeep, row, rowd, keptd, cand, kept, kcodes, total;
-    __host__ __device__ void init(int capmax, int mpad) {
+    int tdom, tkeep, row, rowd, keptd, cand, sel, total;
+    __host__ __device__ void init(int capmax, int m, int mpad) {
         int o = 0;
         tdom = o; o += round_up(mpad * 16, 256);   // x's row tables (256-aligned)
         tkeep = o; o += round_up(mpad * 16, 256);
@@ -83,8 +83,8 @@ struct ReverseLayout {
         rowd = o; o += round_up(capmax, 32);
         keptd = o; o += round_up(capmax, 32);
         cand = o; o += 128 * 8;
-        kept = o; o += round_up(capmax, 32) * 4;
-        kcodes = o; o += round_up(capmax * kept_stride(mpad), 16);
+        o = round_up(o, 256);
+        sel = o; o += select_tv_bytes(m, mpad, capmax);  // kept ids first
         total = round_up(o, 256);
     }
 };

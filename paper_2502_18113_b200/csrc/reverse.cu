@@ -87,8 +87,8 @@ __global__ void __maxnreg__(96) reverse_kernel(
     uint8_t *rowd_s = base + L.rowd;
     uint8_t *keptd = base + L.keptd;
     unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
-    int32_t *kept = reinterpret_cast<int32_t *>(base + L.kept);
-    uint8_t *kcodes = base + L.kcodes;
+    uint8_t *selws = base + L.sel;
+    int32_t *kept = reinterpret_cast<int32_t *>(selws);  // = warp_select_tv's kept ids
     const int nseg = *nheads;
     unsigned long long n_prune = 0, n_app = 0, n_sym = 0, n_full = 0;
     while (true) {
@@ -242,14 +242,15 @@ __global__ void __maxnreg__(96) reverse_kernel(
                     if (rk[c] >= 0) cand[rk[c]] = mine[c];
                 __syncwarp();
                 unsigned long long sym = 0;
-                nk = warp_select_heur(
+                int32_t *kept_sel;
+                nk = warp_select_tv(
                     sdtT, g.m, g.mpad, g.codes, g.mpad, cap + 1, cap,
-                    [&](int j, int &v, double &dv) {
+                    [&](int j, int &v, uint32_t &dv) {
                         unsigned long long k = cand[j];
                         v = (int)(k & 0xffffffffu);
-                        dv = (double)(uint32_t)(k >> 32);
+                        dv = (uint32_t)(k >> 32);
                     },
-                    kept, kcodes, lane, &sym, keptd);
+                    selws, lane, &sym, kept_sel, keptd);
                 n_sym += cap + 1 + sym;
             }
             __syncwarp();

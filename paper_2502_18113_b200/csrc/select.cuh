@@ -155,7 +155,7 @@ template <class Get>
 __device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
                               const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
                               Get get, uint8_t *ws, int lane, unsigned long long *sym_count,
-                              int32_t *&kept_out) {
+                              int32_t *&kept_out, uint8_t *kept_d = nullptr) {
     const int ks = kept_enc_stride(mpad);
     int32_t *kept_ids = reinterpret_cast<int32_t *>(ws);
     uint8_t *kenc = ws + round_up(cap * 4, 256);
@@ -204,7 +204,10 @@ __device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
             sym += nk;
         }
         if (!__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) kept_ids[nk] = v;
+            if (lane == 0) {
+                kept_ids[nk] = v;
+                if (kept_d) kept_d[nk] = (uint8_t)dv;
+            }
             for (int q = lane; q < mpad / 4; q += 32)
                 *reinterpret_cast<uint32_t *>(kenc + nk * ks + 4 * q) =
                     __ldg(reinterpret_cast<const uint32_t *>(cv) + q) + kept_enc_add(q);
