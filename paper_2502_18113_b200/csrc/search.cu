@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     int rerank_depth, const float *__restrict__ vecs, int dim, const float *__restrict__ queries,
     WarpLayout L, int64_t *__restrict__ out_ids, double *__restrict__ out_d,
     unsigned long long *__restrict__ ctr, int *err) {
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
     const int q = blockIdx.x * kSearchWarps + wid;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     Graph g, const uint8_t *__restrict__ adt_q, int nq, const int64_t *__restrict__ entries,
     int width, int layer, WarpLayout L, int32_t *__restrict__ out_ids, double *__restrict__ out_d,
     int32_t *__restrict__ out_n, unsigned long long *__restrict__ ctr, int *err) {
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
     const int q = blockIdx.x * kSearchWarps + wid;

@@ -76,7 +76,7 @@ __host__ __device__ inline int vis_bucket_slots(int hlog2) {
 struct WarpLayout {
     int adt, T, S, TQ, fresh, fdist, hash, total;
     int hash_log2;
-    __host__ __device__ static int adt_bytes(int mpad) { return (mpad + mpad / 16) * 16; }
+    __host__ __device__ static int adt_bytes(int mpad) { return round_up(mpad * 16, 256); }
     // t_alias: the sorted results live at the end of the visited table (the
     // build: the table is dead once a layer search has sorted its results, and
     // forward selection's kept rows use only its start)
@@ -88,7 +88,7 @@ struct WarpLayout {
         const bool alias = t_alias && W <= kRegSetMax;
         const int hbytes = 16 << vis_buckets_log2(hlog2);
         int o = 0;
-        adt = o; o += round_up(adt_bytes(mpad), 16);
+        adt = o; o += adt_bytes(mpad);  // offset 0: 256-aligned chunks
         // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
         if (!alias) {
             T = o;
@@ -106,9 +106,15 @@ struct WarpLayout {
     }
 };
 
-// Skewed ADT rows: row r at ((r + r/16) * 16) so the 16-subspace chunks read by
-// different lane groups fall in different banks.
-__device__ __forceinline__ int adt_row_off(int r) { return (r + (r >> 4)) << 4; }
+// ADT rows in shared memory: 16-row chunks of 256 bytes (256-aligned), row r
+// of chunk c stored at slot (r + c) mod 16, so the lane groups that read the
+// same row of different chunks hit different banks.  A lookup address is then
+// chunk base | byte, byte = slot * 16 + code: one PRMT merges a pre-offset code
+// byte into the base.
+__device__ __forceinline__ int adt_row_off(int r) {
+    const int c = r >> 4;
+    return (c << 8) + ((((r & 15) + c) & 15) << 4);
+}
 
 __device__ __forceinline__ void load_adt_smem(uint8_t *adt_s, const uint8_t *adt, int mpad,
                                               int lane) {
@@ -127,51 +133,47 @@ __device__ __forceinline__ uint32_t adt_one(const uint8_t *adt_s, const uint8_t 
     return s > 255u ? 255u : s;
 }
 
-// Distances of the nf ids in ids_s[] (shared) into out_s[] (shared).  G lanes per
-// id, each summing one 16-subspace chunk gathered with a 16-byte load.
-template <int G>
-__device__ __forceinline__ void gather_dists(const uint8_t *adt_s, const uint8_t *__restrict__ codes,
-                                             int mpad, const int32_t *ids_s, int nf,
-                                             uint32_t *out_s, int lane) {
-    constexpr int PER = 32 / G;
-    const int gi = lane / G, c = lane % G;
-    for (int base = 0; base < nf; base += PER) {
+// Distances of the nf ids in ids_s[] (shared) into out_s[] (shared).  G lanes
+// per id (G = chunks rounded up to a power of two), each summing one
+// 16-subspace chunk gathered with a 16-byte load.
+__device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *__restrict__ codes,
+                                          int mpad, const int32_t *ids_s, int nf,
+                                          uint32_t *out_s, int lane) {
+    const int chunks = mpad >> 4;
+    const int lg = chunks <= 1 ? 0 : 32 - __clz(chunks - 1);
+    const int G = 1 << lg;
+    const int gi = lane >> lg, c = lane & (G - 1);
+    const bool active = c < chunks;
+    const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(adt_s) + ((uint32_t)c << 8);
+    // pre-offsets of the 4 code bytes of word q: slot((4q + b + c) mod 16) * 16
+    uint32_t K[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        K[q] = ((0x03020100u + 0x04040404u * (uint32_t)q + 0x01010101u * (uint32_t)c) &
+                0x0f0f0f0fu)
+               << 4;
+    for (int base = 0; base < nf; base += (32 >> lg)) {
         const int f = base + gi;
         uint32_t sum = 0;
-        if (f < nf && c * 16 < mpad) {
+        if (f < nf && active) {
             const int id = ids_s[f];
-            uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
-            const uint8_t *rowbase = adt_s + adt_row_off(c * 16);
-            uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+            const uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
+            const uint32_t W[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                const uint32_t e = W[q] + K[q];
+                uint32_t b[4];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    int r = q * 4 + b;  // row within chunk; chunk rows are contiguous
-                    sum += rowbase[r * 16 + ((ww[q] >> (8 * b)) & 0xffu)];
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t a = prmt(e, cbase, 0x7650u + (uint32_t)k);
+                    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[k]) : "r"(a));
                 }
+                sum += b[0] + b[1] + b[2] + b[3];
             }
         }
-#pragma unroll
         for (int o = 1; o < G; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (c == 0 && f < nf) out_s[f] = sum > 255u ? 255u : sum;
     }
-}
-
-template <int G>
-__device__ __forceinline__ void gather_dists_dispatch(const uint8_t *adt_s, const uint8_t *codes,
-                                                      int mpad, const int32_t *ids_s, int nf,
-                                                      uint32_t *out_s, int lane) {
-    gather_dists<G>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
-}
-
-__device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *codes, int mpad,
-                                          const int32_t *ids_s, int nf, uint32_t *out_s, int lane) {
-    const int chunks = mpad >> 4;
-    if (chunks <= 1) gather_dists<1>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
-    else if (chunks <= 2) gather_dists<2>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
-    else if (chunks <= 4) gather_dists<4>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
-    else gather_dists<8>(adt_s, codes, mpad, ids_s, nf, out_s, lane);
     __syncwarp();
 }
 
