@@ -197,6 +197,13 @@ def run_reference(args):
     }))
 
 
+def load_traffic():
+    """Per-launch DRAM bytes of the roofline kernels from the newest committed
+    ncu capture summary (profiles/*_traffic.json), or {}."""
+    files = sorted((ROOT / "profiles").glob("*_traffic.json"))
+    return json.loads(files[-1].read_text()) if files else {}
+
+
 def scan_benchmark(lib, torch, m, cap, peak, reps=5):
     """Standalone K1 block scan over a > L2 padded block array."""
     from paper_2502_18113_b200._lib import check
@@ -242,7 +249,12 @@ def scan_benchmark(lib, torch, m, cap, peak, reps=5):
                      "unit": "GB/s", "frac": gbs / peak}
     del blocks
     best = max(res.values(), key=lambda r: r["achieved"])
-    return dict(best, bound="hbm", traffic=None,
+    # ncu DRAM bytes of one launch of the TMA variant at the config-2 shape
+    tr = load_traffic().get("scan_select_tma_kernel")
+    traffic = None
+    if tr and tr.get("algorithmic_bytes") == alg_bytes and "tma" in best["kernel"]:
+        traffic = tr["dram_bytes"]
+    return dict(best, bound="hbm", traffic=traffic,
                 shape=f"m={m} cap={cap}, {nq} queries x {ns} random blocks of {nblocks} "
                       f"(working set {nblocks * stride / 1e9:.2f} GB > L2)",
                 variants={k: {"achieved": v["achieved"], "frac": v["frac"],
@@ -333,10 +345,15 @@ def main():
     # code row of every evaluated vertex
     search_bytes = prof["visited"] * cap0 * 4 + prof["dist_comps"] * c["m_f"]
     search_gbs = search_bytes / (prof["ms_search"] * 1e-3) / 1e9
+    # DRAM bytes per build at the captured launch's bytes per inserted vector
+    tr = load_traffic().get("build_search_kernel")
+    search_traffic = int(tr["dram_bytes"] / tr["vectors"] * n) if tr else None
     roofline = {"bound": "hbm", "kernel": "build_search_kernel (K4+K5)",
                 "achieved": search_gbs, "peak": peak, "unit": "GB/s",
-                "frac": search_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                "frac": search_gbs / peak, "traffic": search_traffic, "peak_kind": peak_kind,
                 "bytes_per_build": search_bytes,
+                "traffic_basis": "per build: ncu DRAM bytes per inserted vector of one captured "
+                                 "launch x n (profiles/*_traffic.json)",
                 "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}
 
     out = {"metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world,
