@@ -204,6 +204,31 @@ def load_traffic():
     return json.loads(files[-1].read_text()) if files else {}
 
 
+def query_benchmark(torch, g, provider, data, queries, reps=3):
+    """§8(f) row 1: search_batch over the built graph (K2 query tables + K8),
+    device-resident queries, ef 64, k 10; recall@10 against GPU brute force."""
+    from paper_2502_18113_b200 import dataset, evaluation
+
+    gt = dataset.brute_force_knn(data, queries, 10)
+    q_dev = torch.from_numpy(queries).cuda()
+    res = {"queries": int(queries.shape[0]), "ef": 64, "k": 10}
+    for tag, rr in (("flash", 0), ("rerank64", 64)):
+        sp = evaluation.SearchParams(ef=64, k=10, rerank_depth=rr)
+        for _ in range(2):
+            evaluation.search_batch_dev(g, provider, q_dev, sp)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ids, _, _ = evaluation.search_batch_dev(g, provider, q_dev, sp)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res[tag] = {"qps": queries.shape[0] / (ms * 1e-3), "ms": ms,
+                    "recall@10": evaluation.recall_at_k(ids.cpu().numpy(), gt)}
+    return res
+
+
 def scan_benchmark(lib, torch, m, cap, peak, reps=5):
     """Standalone K1 block scan over a > L2 padded block array."""
     from paper_2502_18113_b200._lib import check
@@ -272,6 +297,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-search", action="store_true", help="skip the query-search leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -292,7 +318,7 @@ def main():
     c = dataset.CONFIGS[CFG]
     n = args.n or c["n"]
     peak, peak_kind = load_peaks()
-    data, _ = dataset.baseline_config(CFG, n=n, nq=0)
+    data, queries = dataset.baseline_config(CFG, n=n, nq=0 if args.no_search else c["nq"])
     x_dev = torch.from_numpy(data).cuda()
 
     # coder training on the GPU (coding_seconds)
@@ -374,6 +400,8 @@ def main():
 
     if rank == 0:
         out["scan"] = scan_benchmark(lib, torch, c["m_f"], cap0, peak)
+        if not args.no_search:
+            out["search"] = query_benchmark(torch, g, provider, data, queries)
         if not args.no_e2e:
             prov = provider.core_arrays()
             prov = dict(prov, codes=prov["codes"].copy())
