@@ -410,13 +410,19 @@ def main():
             h2d = prov["proj"].nbytes + prov["codes"].nbytes + levels.nbytes + \
                 g.upper_offsets.nbytes + model.cent.nbytes + model.sdt.nbytes
             d2h = prov["codes"].nbytes + base.nbytes + upper.nbytes
+            # one untimed call (pinned staging pool, allocator warm-up), then
+            # the timed calls: each uploads its inputs and reads back all rows
+            e2e_steps = max(1, min(args.steps, 3))
+            for it in range(1 + e2e_steps):
+                if it == 1:
+                    torch.cuda.synchronize()
+                    t1 = time.perf_counter()
+                sm100.build_graph(4, prov, levels, base, g.upper_offsets, upper, c["efC"],
+                                  c["M"])
             torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            sm100.build_graph(4, prov, levels, base, g.upper_offsets, upper, c["efC"], c["M"])
-            torch.cuda.synchronize()
-            e2e_s = time.perf_counter() - t1
+            e2e_s = (time.perf_counter() - t1) / e2e_steps
             out["e2e"] = {"value": n / e2e_s, "unit": "vectors/s", "h2d_bytes_per_step": h2d,
-                          "d2h_bytes_per_step": d2h, "seconds": e2e_s,
+                          "d2h_bytes_per_step": d2h, "seconds": e2e_s, "steps": e2e_steps,
                           "api": "sm100.build_graph (host numpy arrays, reference layout)"}
         if not args.no_cpu_baseline:
             from oracle import train_np

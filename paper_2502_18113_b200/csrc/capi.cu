@@ -2,7 +2,11 @@
 // mirror the reference core's blocking Cython entry points
 // (build_graph _core.pyx:711-764, search_batch _core.pyx:817-888).
 #include <stdarg.h>
+#include <string.h>
 
+#include <algorithm>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -30,13 +34,80 @@ struct DevBuf {
         }
         return FA_OK;
     }
-    int upload(const void *src, size_t bytes) {
-        FA_TRY(alloc(bytes));
-        if (bytes) FA_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
-        return FA_OK;
-    }
+    int upload(const void *src, size_t bytes);
     template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
 };
+
+// ---- pageable host <-> device copies --------------------------------------
+// The drop-ins take the caller's (pageable) numpy buffers.  Large transfers
+// go through per-worker pinned staging buffers: each worker thread moves its
+// own chunks (DMA on its own stream + host memcpy), so the DMA of one chunk
+// overlaps the host copies of the others and the host side runs on several
+// cores.  The pinned pool is allocated once per process.
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr int kStageWorkers = 8;
+static std::mutex g_stage_mu;
+static std::vector<void *> g_stage;
+
+static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
+    if (bytes == 0) return FA_OK;
+    const size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
+    if (nchunk < 2) {
+        FA_CUDA(d2h ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost)
+                    : cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
+        return FA_OK;
+    }
+    std::lock_guard<std::mutex> lk(g_stage_mu);  // one staged copy at a time
+    const int T = (int)std::min<size_t>(kStageWorkers, nchunk);
+    while ((int)g_stage.size() < T) {
+        void *p = nullptr;
+        cudaError_t e = cudaHostAlloc(&p, kStageBytes, cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            set_error("cudaHostAlloc(%zu): %s", kStageBytes, cudaGetErrorString(e));
+            return FA_ENOMEM;
+        }
+        g_stage.push_back(p);
+    }
+    int device = 0;
+    FA_CUDA(cudaGetDevice(&device));
+    std::vector<cudaError_t> err(T, cudaSuccess);
+    std::vector<std::thread> th;
+    for (int w = 0; w < T; ++w)
+        th.emplace_back([&, w]() {
+            cudaError_t e = cudaSetDevice(device);
+            cudaStream_t s = nullptr;
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+            uint8_t *buf = static_cast<uint8_t *>(g_stage[w]);
+            for (size_t c = w; c < nchunk && e == cudaSuccess; c += T) {
+                const size_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
+                uint8_t *h = static_cast<uint8_t *>(host) + off;
+                uint8_t *d = static_cast<uint8_t *>(dev) + off;
+                if (d2h) {
+                    e = cudaMemcpyAsync(buf, d, len, cudaMemcpyDeviceToHost, s);
+                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                    if (e == cudaSuccess) memcpy(h, buf, len);
+                } else {
+                    memcpy(buf, h, len);
+                    e = cudaMemcpyAsync(d, buf, len, cudaMemcpyHostToDevice, s);
+                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                }
+            }
+            if (s) cudaStreamDestroy(s);
+            err[w] = e;
+        });
+    for (auto &t : th) t.join();
+    for (cudaError_t e : err)
+        if (e != cudaSuccess) {
+            set_error("staged %s copy: %s", d2h ? "D2H" : "H2D", cudaGetErrorString(e));
+            return FA_ECUDA;
+        }
+    return FA_OK;
+}
+
+int DevBuf::upload(const void *src, size_t bytes) {
+    FA_TRY(alloc(bytes));
+    return staged_copy(const_cast<void *>(src), p, bytes, false);
+}
 
 struct IndexGuard {
     fa_index *ix = nullptr;
@@ -94,10 +165,10 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     FA_TRY(dupper.alloc((size_t)n_upper_rows * upper_stride));
     FA_TRY(fa_index_export_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
                                   upper_stride, nullptr));
-    FA_CUDA(cudaMemcpy(base_blocks, dbase.p, (size_t)n * base_stride, cudaMemcpyDeviceToHost));
+    FA_CUDA(cudaDeviceSynchronize());
+    FA_TRY(staged_copy(base_blocks, dbase.p, (size_t)n * base_stride, true));
     if (n_upper_rows)
-        FA_CUDA(cudaMemcpy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride,
-                           cudaMemcpyDeviceToHost));
+        FA_TRY(staged_copy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride, true));
     return FA_OK;
 }
 
