@@ -8,7 +8,7 @@ namespace fa {
 // width C, forward selection (cap R), forward row write, reverse requests.
 // Mirrors insert_one (_core.pyx:501-536) against the graph as of batch start.
 template <int J, int EM>
-__global__ void __launch_bounds__(kSearchWarps * 32, 4) build_search_kernel(
+__global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
     unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) build_search_kernel(
     extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
-    WarpWS ws(smem + wid * L.total, L);
+    WarpWS ws(smem, wid, kSearchWarps, L);
     CounterTotals total;
     // persistent warps pull vertices from the batch; a slow search never holds
     // its CTA siblings' slots idle

@@ -12,7 +12,7 @@ __device__ __forceinline__ int64_t row_global(const Graph &g, int layer, int y) 
     return layer == 0 ? (int64_t)y : g.n + __ldg(g.uoff + y) + layer - 1;
 }
 
-// Per-warp workspace pointers.
+// Per-warp workspace pointers (WarpLayout): warp `wid` of a CTA of `warps`.
 struct WarpWS {
     uint8_t *adt;
     unsigned long long *T, *S;
@@ -20,14 +20,16 @@ struct WarpWS {
     int32_t *fresh;
     uint32_t *fdist;
     uint32_t *H;
-    __device__ WarpWS(uint8_t *base, const WarpLayout &L) {
-        adt = base + L.adt;
-        T = reinterpret_cast<unsigned long long *>(base + L.T);
-        S = reinterpret_cast<unsigned long long *>(base + L.S);
-        TQ = reinterpret_cast<int32_t *>(base + L.TQ);
-        fresh = reinterpret_cast<int32_t *>(base + L.fresh);
-        fdist = reinterpret_cast<uint32_t *>(base + L.fdist);
-        H = reinterpret_cast<uint32_t *>(base + L.hash);
+    __device__ WarpWS(uint8_t *smem, int wid, int warps, const WarpLayout &L) {
+        uint8_t *bg = smem + wid * L.big;
+        uint8_t *sm = smem + warps * L.big + wid * L.small;
+        adt = bg + L.adt;
+        H = reinterpret_cast<uint32_t *>(bg + L.hash);
+        T = reinterpret_cast<unsigned long long *>((L.t_big ? bg : sm) + L.T);
+        S = reinterpret_cast<unsigned long long *>(sm + L.S);
+        TQ = reinterpret_cast<int32_t *>(sm + L.TQ);
+        fresh = reinterpret_cast<int32_t *>(sm + L.fresh);
+        fdist = reinterpret_cast<uint32_t *>(sm + L.fdist);
     }
 };
 

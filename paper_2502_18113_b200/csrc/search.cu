@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     const int wid = threadIdx.x >> 5;
     const int q = blockIdx.x * kSearchWarps + wid;
     if (q >= nq) return;
-    WarpWS ws(smem + wid * L.total, L);
+    WarpWS ws(smem, wid, kSearchWarps, L);
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     const int wid = threadIdx.x >> 5;
     const int q = blockIdx.x * kSearchWarps + wid;
     if (q >= nq) return;
-    WarpWS ws(smem + wid * L.total, L);
+    WarpWS ws(smem, wid, kSearchWarps, L);
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_adt_smem(ws.adt, adt_q + (size_t)q * g.mpad * 16, g.mpad, lane);
     __syncwarp();

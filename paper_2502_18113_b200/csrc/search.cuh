@@ -73,8 +73,15 @@ __host__ __device__ inline int vis_bucket_slots(int hlog2) {
     return hlog2 >= 12 ? 8 : 1 << (hlog2 > 9 ? hlog2 - 9 : 0);
 }
 
+// Per-warp shared memory, in two blocks: a 256-aligned block (the ADT rows
+// and the visited table, both addressed by PRMT-merged byte offsets) and a
+// small block (candidate keys, tie queue, fresh ids/distances).  A CTA of w
+// warps holds w big blocks, then w small blocks: total = w * (big + small).
 struct WarpLayout {
-    int adt, T, S, TQ, fresh, fdist, hash, total;
+    int adt, hash, big;                  // offsets in the big block
+    int T, S, TQ, fresh, fdist, small;   // offsets in the small block (T: see t_big)
+    int t_big;                           // T lives at the end of the visited table
+    int total;
     int hash_log2;
     __host__ __device__ static int adt_bytes(int mpad) { return round_up(mpad * 16, 256); }
     // t_alias: the sorted results live at the end of the visited table (the
@@ -85,24 +92,26 @@ struct WarpLayout {
         hash_log2 = hlog2;
         const int nc = cand_capacity(expand, capmax);
         const int Wp = round_up(W, 32);
-        const bool alias = t_alias && W <= kRegSetMax;
         const int hbytes = 16 << vis_buckets_log2(hlog2);
+        t_big = t_alias && W <= kRegSetMax;
+        adt = 0;
+        hash = adt_bytes(mpad);
+        big = hash + hbytes;  // a multiple of 256
         int o = 0;
-        adt = o; o += adt_bytes(mpad);  // offset 0: 256-aligned chunks
-        // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
-        if (!alias) {
+        if (t_big) {
+            T = hash + hbytes - Wp * 8;
+        } else {
+            // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
             T = o;
             o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
             o = round_up(o, 16);
         }
-        S = o; o += 2 * nc * 4;                     // candidate keys (two buffers)
-        TQ = o; o += Wp * 4;                        // tie queue, then the final sort
+        S = o; o += 2 * nc * 4;  // candidate keys (two buffers)
+        TQ = o; o += Wp * 4;     // tie queue
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
-        o = round_up(o, 256);  // forward selection's tables are 256-aligned
-        hash = o; o += hbytes;
-        if (alias) T = hash + hbytes - Wp * 8;
-        total = round_up(o, 256);
+        small = round_up(o, 16);
+        total = big + small;
     }
 };
 
