@@ -18,6 +18,7 @@ from .flash import (FlashModel, FlashProvider, encode_and_adt, flash_train,  # n
                     sdt_distance)
 from .graph import BuildParams, GraphIndex, assign_layers, check_invariants  # noqa: F401
 from .pca import PCAModel, pca_train  # noqa: F401
+from .serialize import load_index, save_index  # noqa: F401
 
 HAVE_EXT = True
 
