@@ -97,17 +97,20 @@ __global__ void __maxnreg__(96) reverse_kernel(
         s = __shfl_sync(0xffffffffu, s, 0);
         if (s >= nseg) break;
         const int64_t h = heads[s];
-        const unsigned long long hk = keys[h];
+        // the segment's first 32 keys stay in registers (lane j: keys[h + j])
+        const unsigned long long kk = h + lane < N ? keys[h + lane] : KEY_MAX;
+        const unsigned long long hk = __shfl_sync(0xffffffffu, kk, 0);
         const int64_t rowg = (int64_t)(hk >> 32);
         int64_t e = -1;
-        for (int64_t b = h + 1;; b += 32) {
+        {
+            const unsigned nb = __ballot_sync(0xffffffffu, (kk >> 32) != (hk >> 32));
+            if (nb) e = h + __ffs(nb) - 1;
+        }
+        for (int64_t b = h + 32; e < 0; b += 32) {
             int64_t j = b + lane;
             bool same = j < N && (keys[j] >> 32) == (hk >> 32);
             unsigned nb = __ballot_sync(0xffffffffu, !same);
-            if (nb) {
-                e = b + __ffs(nb) - 1;
-                break;
-            }
+            if (nb) e = b + __ffs(nb) - 1;
         }
         const bool l0 = rowg < g.n;
         const int y = l0 ? (int)rowg : upper_owner[rowg - g.n];
@@ -126,7 +129,9 @@ __global__ void __maxnreg__(96) reverse_kernel(
         bool dirty = false;
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
-            const int x = (int)(keys[t] & 0xffffffffu);
+            const unsigned long long kt =
+                t - h < 32 ? __shfl_sync(0xffffffffu, kk, (int)(t - h)) : keys[t];
+            const int x = (int)(kt & 0xffffffffu);
             if (cnt < cap) {
                 if (lane == 0) row_s[cnt] = x;
                 ++cnt;
