@@ -122,15 +122,15 @@ template <int NR>
 __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
     const uint8_t *__restrict__ adt, int nq, const uint8_t *__restrict__ blocks,
     int64_t block_stride, int64_t codes_off, uint32_t copy_bytes, uint32_t stage_bytes, int cap,
-    int m, const int32_t *__restrict__ sel, int nsel, int slices,
+    int m, const int32_t *__restrict__ sel, int nsel, int slices, int stages,
     unsigned long long *__restrict__ out) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + wid * kScanStages;
-    uint8_t *ring = smem + 128 + (size_t)wid * kScanStages * stage_bytes;
+    uint8_t *ring = smem + 128 + (size_t)wid * stages * stage_bytes;
     if (lane == 0) {
-        for (int s = 0; s < kScanStages; ++s) mbar_init(bars + s, 1);
+        for (int s = 0; s < stages; ++s) mbar_init(bars + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -147,15 +147,15 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
     const int nblk = max(0, hi - lo);
     const int32_t *qsel = sel + (size_t)q * nsel + lo;
     if (lane == 0)
-        for (int s = 0; s < kScanStages && s < nblk; ++s) {
+        for (int s = 0; s < stages && s < nblk; ++s) {
             mbar_expect_tx(bars + s, copy_bytes);
             bulk_g2s(ring + (size_t)s * stage_bytes, blocks + (int64_t)__ldg(qsel + s) * block_stride,
                      copy_bytes, bars + s);
         }
     unsigned long long best = ~0ull;
     for (int i = 0; i < nblk; ++i) {
-        const int st = i % kScanStages;
-        mbar_wait(bars + st, (uint32_t)((i / kScanStages) & 1));
+        const int st = stages == 1 ? 0 : i & 1;
+        mbar_wait(bars + st, (uint32_t)((stages == 1 ? i : i >> 1) & 1));
         const uint8_t *blk = ring + (size_t)st * stage_bytes;
         const int cnt = min(*reinterpret_cast<const int32_t *>(blk), cap);
         const int32_t *ids = reinterpret_cast<const int32_t *>(blk + 16);
@@ -180,11 +180,11 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
             }
         }
         __syncwarp();
-        if (lane == 0 && i + kScanStages < nblk) {
+        if (lane == 0 && i + stages < nblk) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bars + st, copy_bytes);
             bulk_g2s(ring + (size_t)st * stage_bytes,
-                     blocks + (int64_t)__ldg(qsel + i + kScanStages) * block_stride, copy_bytes,
+                     blocks + (int64_t)__ldg(qsel + i + stages) * block_stride, copy_bytes,
                      bars + st);
         }
     }
@@ -215,7 +215,10 @@ extern "C" int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t 
     const uint32_t copy_bytes = (uint32_t)round_up64(codes_off + (int64_t)nb * m * 16, 16);
     FA_CHECK_ARG(copy_bytes <= (uint32_t)block_stride, "block stride smaller than its contents");
     const uint32_t stage_bytes = (uint32_t)round_up64(copy_bytes, 128);
-    const size_t smem = 128 + (size_t)kScanWarps * kScanStages * stage_bytes;
+    // two stages per warp while two CTAs still fit an SM, else one (large
+    // blocks: more warps beat deeper rings)
+    const int stages = 2 * ((size_t)kScanWarps * 2 * stage_bytes + 1024) * 2 <= 227 * 1024 ? 2 : 1;
+    const size_t smem = 128 + (size_t)kScanWarps * stages * stage_bytes;
     FA_CHECK_ARG(smem <= 227 * 1024, "block too large for the staged scan");
     int slices = 1;
     while ((int64_t)nq * slices < 148 * 96 && slices * 16 <= nsel) slices *= 2;
@@ -227,7 +230,7 @@ extern "C" int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t 
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         scan_select_tma_kernel<NR_><<<grid, kScanWarps * 32, smem, st>>>(                   \
             adt, nq, blocks, block_stride, codes_off, copy_bytes, stage_bytes, cap, m, sel,  \
-            nsel, slices, out);                                                             \
+            nsel, slices, stages, out);                                                     \
     } while (0)
     if (m <= 32) FA_TMA_LAUNCH(1);
     else if (m <= 64) FA_TMA_LAUNCH(2);
