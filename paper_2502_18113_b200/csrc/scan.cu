@@ -118,7 +118,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
 }
 
-template <int NR>
+// NR full table rows per lane (rows lane + 32 k); HALF: the m - 32 NR = 16
+// remaining rows are split in halves, lane t taking 8 slots (half t & 1) of
+// row 32 NR + t / 2 — no lane idles at m = 48, 80, 112.
+template <int NR, bool HALF>
 __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
     const uint8_t *__restrict__ adt, int nq, const uint8_t *__restrict__ blocks,
     int64_t block_stride, int64_t codes_off, uint32_t copy_bytes, uint32_t stage_bytes, int cap,
@@ -140,6 +143,13 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
     if (q >= nq) return;
     WarpTable<NR> tab;
     tab.load(adt + (size_t)q * m * 16, m, lane);
+    const int hrow = 32 * NR + (lane >> 1);
+    uint32_t th[4] = {0, 0, 0, 0};
+    if (HALF) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(adt + (size_t)q * m * 16 + hrow * 16);
+        th[0] = v.x; th[1] = v.y; th[2] = v.z; th[3] = v.w;
+    }
+    const bool hodd = lane & 1;
     const int nb = (cap + 15) >> 4;
     const int per = (nsel + slices - 1) / slices;
     const int lo = slice * per;
@@ -165,9 +175,22 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const int r = lane + 32 * k;
-                if (r < m)
+                if (HALF || r < m)
                     acc_row(tab.t[k], *reinterpret_cast<const uint4 *>(cod + (size_t)b * m * 16 + r * 16),
                             acc);
+            }
+            if (HALF) {
+                const uint2 c = *reinterpret_cast<const uint2 *>(cod + (size_t)b * m * 16 + hrow * 16 +
+                                                                 (hodd ? 8 : 0));
+                const uint32_t r0 = lut16x4(th[0], th[1], th[2], th[3], c.x);
+                const uint32_t r1 = lut16x4(th[0], th[1], th[2], th[3], c.y);
+                const uint32_t a[4] = {prmt(r0, 0u, 0x4240u), prmt(r0, 0u, 0x4341u),
+                                       prmt(r1, 0u, 0x4240u), prmt(r1, 0u, 0x4341u)};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (hodd) acc[4 + k] += a[k];
+                    else acc[k] += a[k];
+                }
             }
             const uint32_t v = reduce_batch(acc, lane);
             const int slot = b * 16 + slot_of_lane(lane);
@@ -224,18 +247,21 @@ extern "C" int fa_scan_select_tma_dev(const uint8_t *adt, int nq, const uint8_t 
     while ((int64_t)nq * slices < 148 * 96 && slices * 16 <= nsel) slices *= 2;
     const int64_t warps = (int64_t)nq * slices;
     const int grid = (int)((warps + kScanWarps - 1) / kScanWarps);
-#define FA_TMA_LAUNCH(NR_)                                                                  \
+#define FA_TMA_LAUNCH(NR_, HALF_)                                                           \
     do {                                                                                    \
-        FA_CUDA(cudaFuncSetAttribute(scan_select_tma_kernel<NR_>,                           \
+        FA_CUDA(cudaFuncSetAttribute(scan_select_tma_kernel<NR_, HALF_>,                    \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        scan_select_tma_kernel<NR_><<<grid, kScanWarps * 32, smem, st>>>(                   \
+        scan_select_tma_kernel<NR_, HALF_><<<grid, kScanWarps * 32, smem, st>>>(            \
             adt, nq, blocks, block_stride, codes_off, copy_bytes, stage_bytes, cap, m, sel,  \
             nsel, slices, stages, out);                                                     \
     } while (0)
-    if (m <= 32) FA_TMA_LAUNCH(1);
-    else if (m <= 64) FA_TMA_LAUNCH(2);
-    else if (m <= 96) FA_TMA_LAUNCH(3);
-    else FA_TMA_LAUNCH(4);
+    if (m == 48) FA_TMA_LAUNCH(1, true);
+    else if (m == 80) FA_TMA_LAUNCH(2, true);
+    else if (m == 112) FA_TMA_LAUNCH(3, true);
+    else if (m <= 32) FA_TMA_LAUNCH(1, false);
+    else if (m <= 64) FA_TMA_LAUNCH(2, false);
+    else if (m <= 96) FA_TMA_LAUNCH(3, false);
+    else FA_TMA_LAUNCH(4, false);
 #undef FA_TMA_LAUNCH
     FA_LAUNCH_CHECK();
     return FA_OK;

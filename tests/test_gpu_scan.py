@@ -34,7 +34,7 @@ def _expected(adt, blocks, sel, cap, m, codes_off):
     return out
 
 
-@pytest.mark.parametrize("cap,m", [(32, 32), (64, 64), (64, 48), (96, 96), (16, 8)])
+@pytest.mark.parametrize("cap,m", [(32, 32), (64, 64), (64, 48), (96, 96), (16, 8), (64, 80), (32, 112)])
 def test_scan_select_matches_oracle(cuda, cap, m):
     import ctypes
 
