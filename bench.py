@@ -400,6 +400,14 @@ def main():
 
     if rank == 0:
         out["scan"] = scan_benchmark(lib, torch, c["m_f"], cap0, peak)
+        # the same K1 scan at the other configs' block shapes (c1, c3, c5)
+        out["scan_other_shapes"] = {}
+        for cfg_o in (1, 3, 5):
+            co = dataset.CONFIGS[cfg_o]
+            r = scan_benchmark(lib, torch, co["m_f"], 2 * co["M"], peak, reps=3)
+            out["scan_other_shapes"][f"config{cfg_o}"] = {
+                "m": co["m_f"], "cap": 2 * co["M"], "kernel": r["kernel"],
+                "achieved": r["achieved"], "frac": r["frac"], "evals_per_s": r["evals_per_s"]}
         if not args.no_search:
             out["search"] = query_benchmark(torch, g, provider, data, queries)
         if not args.no_e2e:
