@@ -444,11 +444,35 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     void *cub_tmp = nullptr;
     size_t cub_bytes = 0;
     int rc = FA_OK;
+    // scratch is stream-ordered (cudaMallocAsync from the device's pool, kept
+    // cached across builds): no allocation or free synchronises the device
     auto cleanup = [&]() {
-        cudaFree(adt_batch); cudaFree(req); cudaFree(req_sorted); cudaFree(ctr);
-        cudaFree(req_off_d); cudaFree(err); cudaFree(cub_tmp); cudaFree(heads);
-        cudaFree(nheads); cudaFree(next_seg); cudaFree(sdtT);
+        for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
+                        (void *)req_off_d, (void *)err, cub_tmp, (void *)heads, (void *)nheads,
+                        (void *)next_seg, (void *)sdtT})
+            if (p) cudaFreeAsync(p, st);
     };
+    auto dev_alloc = [&](void **p, size_t bytes) -> int {
+        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+        if (e != cudaSuccess) {
+            set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+            return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
+        }
+        return FA_OK;
+    };
+    {
+        static bool pool_set = false;
+        if (!pool_set) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_set = true;
+        }
+    }
     int end_bit = 32;
     {
         int64_t rows = g.n + g.nU;

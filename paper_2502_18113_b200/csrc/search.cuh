@@ -180,7 +180,9 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
                 sum += b[0] + b[1] + b[2] + b[3];
             }
         }
-        for (int o = 1; o < G; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (G > 1) sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        if (G > 2) sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (G > 4) sum += __shfl_xor_sync(0xffffffffu, sum, 4);
         if (c == 0 && f < nf) out_s[f] = sum > 255u ? 255u : sum;
     }
     __syncwarp();
