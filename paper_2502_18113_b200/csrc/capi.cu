@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -121,6 +122,20 @@ using namespace fa;
 extern "C" const char *fa_last_error(void) { return g_err; }
 extern "C" int fa_version(void) { return 1; }
 
+// FLASHANN_B200_TIMING=1: per-phase wall times of the host drop-ins on stderr
+struct PhaseTimer {
+    bool on = getenv("FLASHANN_B200_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[fa timing] %-24s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dproj,
                                    const float *proj, uint8_t *codes, int m, const float *cent,
                                    int dmax, const int32_t *dims, const int32_t *offs,
@@ -138,8 +153,10 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
         res->max_layer = -1;
         return FA_OK;
     }
+    PhaseTimer tm;
     DevBuf dproj_b, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper;
     FA_TRY(dproj_b.upload(proj, sizeof(float) * n * dproj));
+    tm.mark("upload proj");
     FA_TRY(dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
     FA_TRY(ddims.upload(dims, sizeof(int32_t) * m));
     FA_TRY(doffs.upload(offs, sizeof(int32_t) * m));
@@ -153,22 +170,28 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     d.proj = dproj_b.as<float>(); d.cent = dcent.as<float>(); d.dims = ddims.as<int32_t>();
     d.offs = doffs.as<int32_t>(); d.sdt = dsdt.as<uint8_t>(); d.levels = dlev.as<int32_t>();
     d.uoff = duoff.as<int64_t>(); d.n_upper_rows = n_upper_rows;
+    tm.mark("upload model/levels");
     IndexGuard guard;
     FA_TRY(fa_index_create(&d, &guard.ix));
+    tm.mark("index create");
     FA_TRY(fa_index_encode(guard.ix, nullptr));
     FA_TRY(fa_index_build(guard.ix, opts, res, nullptr));
+    tm.mark("encode + build");
     // codes[x] as the compiled core leaves them (prep_qctx overwrite)
     int cs = 0;
     const uint8_t *dcodes = fa_index_codes(guard.ix, &cs);
     FA_CUDA(cudaMemcpy2D(codes, m, dcodes, cs, m, n, cudaMemcpyDeviceToHost));
+    tm.mark("codes D2H");
     FA_TRY(dbase.alloc((size_t)n * base_stride));
     FA_TRY(dupper.alloc((size_t)n_upper_rows * upper_stride));
     FA_TRY(fa_index_export_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
                                   upper_stride, nullptr));
     FA_CUDA(cudaDeviceSynchronize());
+    tm.mark("export");
     FA_TRY(staged_copy(base_blocks, dbase.p, (size_t)n * base_stride, true));
     if (n_upper_rows)
         FA_TRY(staged_copy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride, true));
+    tm.mark("blocks D2H");
     return FA_OK;
 }
 
