@@ -115,7 +115,9 @@ BuildSearchFn build_search_variant(int W, int expand) {
     switch (v) {
         case 2: return build_search_kernel<2, 1>;
         case 4: return build_search_kernel<4, 1>;
+        case 7: return build_search_kernel<7, 1>;
         case 8: return build_search_kernel<8, 1>;
+        case 10: return build_search_kernel<10, 1>;
         case 16: return build_search_kernel<16, 1>;
         default: return build_search_kernel<0, 1>;
     }

@@ -158,7 +158,9 @@ QuerySearchFn query_search_variant(int W) {
     switch (set_variant(W)) {
         case 2: return query_search_kernel<2>;
         case 4: return query_search_kernel<4>;
+        case 7: return query_search_kernel<7>;
         case 8: return query_search_kernel<8>;
+        case 10: return query_search_kernel<10>;
         case 16: return query_search_kernel<16>;
         default: return query_search_kernel<0>;
     }
@@ -168,7 +170,9 @@ LayerSearchFn layer_search_variant(int W) {
     switch (set_variant(W)) {
         case 2: return layer_search_kernel<2>;
         case 4: return layer_search_kernel<4>;
+        case 7: return layer_search_kernel<7>;
         case 8: return layer_search_kernel<8>;
+        case 10: return layer_search_kernel<10>;
         case 16: return layer_search_kernel<16>;
         default: return layer_search_kernel<0>;
     }

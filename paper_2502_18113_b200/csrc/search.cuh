@@ -852,14 +852,18 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     }
     // sort once: bitonic network over the 32 * J register slots (empty slots
     // hold the largest key and sort last), then the first ts go out
+    // (J not a power of two: the network runs over JP registers, the extra
+    // ones holding the largest key)
+    constexpr int JP = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : 16;
+    uint32_t ks[JP];
 #pragma unroll
-    for (int j = 0; j < J; ++j)
-        if (lane + 32 * j >= ts) rs.key[j] = 0xffffffffu;
-    warp_bitonic<J>(rs.key, lane);
+    for (int j = 0; j < JP; ++j)
+        ks[j] = (j < J && lane + 32 * j < ts) ? rs.key[j < J ? j : 0] : 0xffffffffu;
+    warp_bitonic<JP>(ks, lane);
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
+    for (int j = 0; j < JP; ++j) {
         const int e = 32 * j + lane;
-        if (e < ts) T[e] = make_key(rs.key[j] >> 24, (int)(rs.key[j] & 0xffffffu));
+        if (e < ts) T[e] = make_key(ks[j] >> 24, (int)(ks[j] & 0xffffffu));
     }
     __syncwarp();
     ts_out = ts;
@@ -1070,7 +1074,8 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
 
 // result-set variant for a search width W: register slots per lane, 0 = shared
 __host__ __device__ inline int set_variant(int W) {
-    return W <= 64 ? 2 : W <= 128 ? 4 : W <= 256 ? 8 : W <= kRegSetMax ? 16 : 0;
+    return W <= 64 ? 2 : W <= 128 ? 4 : W <= 224 ? 7 : W <= 256 ? 8 : W <= 320 ? 10
+           : W <= kRegSetMax ? 16 : 0;
 }
 
 // Width-1 greedy descent (hill_climb, _core.pyx:345-385): move to the first
