@@ -30,7 +30,8 @@ class Graph(C.Structure):
     _fields_ = [("n", i64), ("nU", i64), ("m", C.c_int), ("cs", C.c_int), ("cap0", C.c_int),
                 ("capU", C.c_int), ("adj0", vp), ("cnt0", vp), ("adjU", vp), ("cntU", vp),
                 ("codes", vp), ("levels", vp), ("uoff", vp), ("upper_owner", vp),
-                ("tie", C.c_int), ("expand", C.c_int)]
+                ("tie", C.c_int), ("expand", C.c_int), ("kind", C.c_int), ("vecs", vp),
+                ("dim", C.c_int)]
 
 
 class BuildResult(C.Structure):
@@ -67,6 +68,9 @@ def lib():
         L.or_layer_search.restype = C.c_int
         L.or_layer_search.argtypes = [C.POINTER(Graph), vp, C.c_int, C.c_int, C.c_int, vp, vp,
                                       C.POINTER(Counters)]
+        L.or_layer_search_exact.restype = C.c_int
+        L.or_layer_search_exact.argtypes = [C.POINTER(Graph), vp, C.c_int, C.c_int, C.c_int, vp,
+                                            vp, C.POINTER(Counters)]
         L.or_hill_climb.restype = C.c_int
         L.or_hill_climb.argtypes = [C.POINTER(Graph), vp, C.c_int, C.c_int, vp,
                                     C.POINTER(Counters)]
@@ -162,7 +166,10 @@ def schedule(levels, batch_max, batch_frac, seq_prefix):
 class HostGraph:
     """Host graph in the device's logical layout (exact-cap id rows + counts)."""
 
-    def __init__(self, levels, upper_offsets, R, m, codes=None, tie=0, expand=1):
+    def __init__(self, levels, upper_offsets, R, m, codes=None, tie=0, expand=1, kind=4,
+                 vecs=None):
+        """kind 4 = Flash (u8 tables over `codes`), kind 0 = exact (fp32 L2 over
+        `vecs`; m = 0)."""
         self.levels = _c(levels, np.int32)
         self.uoff = _c(upper_offsets, np.int64)
         self.n = self.levels.shape[0]
@@ -179,15 +186,24 @@ class HostGraph:
             o = self.uoff[v]
             owner[o : o + self.levels[v]] = v
         self.owner = owner
+        self.kind = int(kind)
+        self.vecs = None if vecs is None else _c(vecs, np.float32)
+        dim = 0 if self.vecs is None else self.vecs.shape[1]
+        if self.kind == 0 and self.vecs is None:
+            raise ValueError("the exact kind needs the vectors")
         self.s = Graph(self.n, self.nU, self.m, self.m, self.cap0, self.capU, _p(self.adj0),
                        _p(self.cnt0), _p(self.adjU), _p(self.cntU), _p(self.codes),
                        _p(self.levels), _p(self.uoff), _p(self.owner), int(tie),
-                       int(expand))
+                       int(expand), self.kind, _p(self.vecs), dim)
 
     @classmethod
-    def from_blocks(cls, levels, upper_offsets, base_blocks, upper_blocks, R, codes):
+    def from_blocks(cls, levels, upper_offsets, base_blocks, upper_blocks, R, codes, kind=4,
+                    vecs=None):
         """Import reference-layout rows (live ids compacted to a prefix)."""
-        g = cls(levels, upper_offsets, R, codes.shape[1], codes)
+        if kind == 0:
+            g = cls(levels, upper_offsets, R, 0, None, kind=0, vecs=vecs)
+        else:
+            g = cls(levels, upper_offsets, R, codes.shape[1], codes)
 
         def load(blocks, adj, cnt, cap):
             for r in range(blocks.shape[0]):
@@ -211,6 +227,15 @@ class HostGraph:
                                    _p(ids), _p(ds), C.byref(c))
         return ids[:ts].copy(), ds[:ts].copy(), c.as_dict()
 
+    def layer_search_exact(self, qvec, layer, entry, width):
+        """Exact kind: distances are returned as float32 values."""
+        ids = np.empty(width + 1, np.int32)
+        ds = np.empty(width + 1, np.int32)
+        c = Counters()
+        ts = lib().or_layer_search_exact(C.byref(self.s), _p(_c(qvec, np.float32)), layer, entry,
+                                         width, _p(ids), _p(ds), C.byref(c))
+        return ids[:ts].copy(), ds[:ts].view(np.float32).astype(np.float64), c.as_dict()
+
     def hill_climb(self, adt, layer, entry):
         d = C.c_int(0)
         c = Counters()
@@ -232,6 +257,19 @@ class HostGraph:
             raise MemoryError("oracle build failed")
         return {"entry_point": int(res.entry_point), "max_layer": int(res.max_layer),
                 "n_batches": int(res.n_batches), "counters": res.counters.as_dict()}
+
+    def build_exact(self, C_, batch_max=4096, batch_frac=0.02, seq_prefix=256):
+        """Exact kind: every distance is the fp32 L2 of the vectors."""
+        z = np.zeros((1, 16, 1), np.float32)
+        zi = np.zeros(1, np.int32)
+        return self.build(self.vecs, z, zi, zi, 0.0, 1.0, np.zeros((1, 16, 16), np.uint8), C_,
+                          batch_max, batch_frac, seq_prefix)
+
+    def search_exact(self, entry, max_layer, queries, ef, k):
+        z = np.zeros((1, 16, 1), np.float32)
+        zi = np.zeros(1, np.int32)
+        q = _c(queries, np.float32)
+        return self.search(self.vecs, z, zi, zi, 0.0, 1.0, entry, max_layer, q, q, ef, k, 0)
 
     def search(self, vecs, cent, dims, offs, dmin, delta, entry, max_layer, queries, qproj, ef,
                k, rerank_depth):

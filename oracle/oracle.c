@@ -23,6 +23,9 @@
  *                    deterministic insertion-batch schedule of the GPU build
  *                    (batch size 1 everywhere = the sequential reference)
  *   or_search        _kernels/_core.pyx:784-888
+ *   kind 0 (exact)   asym_one / sym_one _core.pyx:167-191: fp32 L2 for every
+ *                    distance, the same search / select / reverse rules; keys
+ *                    carry the fp32 bit pattern (monotone for d >= 0)
  *
  * Compile: gcc -O2 -ffp-contract=off (explicit fmaf where the tree fuses).
  */
@@ -149,6 +152,60 @@ int or_select(const uint8_t *sdt, int m, const uint8_t *codes, int cs, const int
     return nk;
 }
 
+/* ---- distance context (kind 4 Flash: u8 tables; kind 0 exact: fp32 L2) ---- */
+
+typedef struct {
+    const uint8_t *adt; /* Flash: the query's table (m x 16)   */
+    const float *vec;   /* exact: the query vector (dim)       */
+} qctx;
+
+static uint32_t fbits(double d) {
+    float f = (float)d;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+}
+static double bits_d(uint32_t u) {
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+/* distance query -> vertex u, as an order-preserving uint32 */
+static uint32_t qdist(const or_graph *g, const qctx *q, int u) {
+    if (g->kind == 0) return fbits(or_l2sq_f32(q->vec, g->vecs + (size_t)u * g->dim, g->dim));
+    return (uint32_t)adt_sum(q->adt, g->codes + (size_t)u * g->cs, g->m);
+}
+/* distance vertex a -> vertex b (sym_one) */
+static uint32_t pdist(const or_graph *g, const uint8_t *sdt, int a, int b) {
+    if (g->kind == 0)
+        return fbits(or_l2sq_f32(g->vecs + (size_t)a * g->dim, g->vecs + (size_t)b * g->dim,
+                                 g->dim));
+    return (uint32_t)or_sdt_sum(sdt, g->codes + (size_t)a * g->cs, g->codes + (size_t)b * g->cs,
+                                g->m);
+}
+static double dist_value(const or_graph *g, uint32_t d) {
+    return g->kind == 0 ? bits_d(d) : (double)d;
+}
+
+/* select_heur (_core.pyx:388-408) over uint32 distances */
+static int select_g(const or_graph *g, const uint8_t *sdt, const int32_t *ids, const uint32_t *d,
+                    int n, int cap, int32_t *out, int64_t *sym) {
+    int nk = 0;
+    for (int j = 0; j < n && nk < cap; ++j) {
+        int v = ids[j], ok = 1;
+        for (int t = 0; t < nk; ++t) {
+            if (sym) ++*sym;
+            if (pdist(g, sdt, out[t], v) < d[j]) {
+                ok = 0;
+                break;
+            }
+        }
+        if (ok) out[nk++] = v;
+    }
+    return nk;
+}
+
 /* ---- graph ---------------------------------------------------------------- */
 
 static int32_t *row_of(or_graph *g, int layer, int v) {
@@ -253,8 +310,8 @@ static uint32_t tie_back(int tie, uint32_t salt, uint32_t t) {
  * accept while the set is not full or d < worst distance (strict), evicting
  * the worst (largest d, smallest id on ties).  Returns |R|; out holds
  * (d << 32 | id) ascending. */
-static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int layer, int entry,
-                             int entry_d, int W, uint64_t *out, or_counters *c) {
+static int layer_search_impl(or_graph *g, scratch *s, const qctx *q, int layer, int entry,
+                             uint32_t entry_d, int W, uint64_t *out, or_counters *c) {
     int cap = layer == 0 ? g->cap0 : g->capU;
     s->epoch++;
     if (s->epoch == 0) {
@@ -293,7 +350,7 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
                 int u = ids[j];
                 if (u < 0 || s->visited[u] == ep) continue;
                 s->visited[u] = ep;
-                uint64_t du = (uint64_t)adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+                uint64_t du = (uint64_t)qdist(g, q, u);
                 s->fresh[nfresh++] = (du << 32) | tie_fwd(tie, s->salt, (uint32_t)u);
             }
         }
@@ -324,7 +381,7 @@ static int layer_search_impl(or_graph *g, scratch *s, const uint8_t *adt, int la
     return nr;
 }
 
-static void hill_climb_impl(or_graph *g, const uint8_t *adt, int layer, int *cur, int *curd,
+static void hill_climb_impl(or_graph *g, const qctx *q, int layer, int *cur, uint32_t *curd,
                             or_counters *c) {
     int cap = layer == 0 ? g->cap0 : g->capU;
     int improved = 1;
@@ -334,11 +391,12 @@ static void hill_climb_impl(or_graph *g, const uint8_t *adt, int layer, int *cur
         int cnt = *cnt_of(g, layer, *cur);
         if (cnt > cap) cnt = cap;
         if (c) c->kernel_calls += (cnt + 15) >> 4;
-        int bu = -1, bd = 0;
+        int bu = -1;
+        uint32_t bd = 0;
         for (int j = 0; j < cnt; ++j) {
             int u = ids[j];
             if (u < 0) continue;
-            int du = adt_sum(adt, g->codes + (size_t)u * g->cs, g->m);
+            uint32_t du = qdist(g, q, u);
             if (c) c->dist_comps++;
             if (bu < 0 || du < bd) {
                 bd = du;
@@ -370,15 +428,15 @@ static void scratch_free(scratch *s) {
     free(s->fresh);
 }
 
-int or_layer_search(or_graph *g, const uint8_t *adt, int layer, int entry, int W, int32_t *out_ids,
-                    int32_t *out_d, or_counters *c) {
+static int layer_search_q(or_graph *g, const qctx *q, int layer, int entry, int W,
+                          int32_t *out_ids, int32_t *out_d, or_counters *c) {
     scratch s;
     int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
     if (scratch_init(&s, g->n, W, capmax)) return -1;
     uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(W + 1));
-    int ed = adt_sum(adt, g->codes + (size_t)entry * g->cs, g->m);
+    uint32_t ed = qdist(g, q, entry);
     if (c) c->dist_comps++;
-    int ts = layer_search_impl(g, &s, adt, layer, entry, ed, W, keys, c);
+    int ts = layer_search_impl(g, &s, q, layer, entry, ed, W, keys, c);
     for (int i = 0; i < ts; ++i) {
         out_ids[i] = (int32_t)(keys[i] & 0xffffffffu);
         out_d[i] = (int32_t)(keys[i] >> 32);
@@ -388,18 +446,31 @@ int or_layer_search(or_graph *g, const uint8_t *adt, int layer, int entry, int W
     return ts;
 }
 
+int or_layer_search(or_graph *g, const uint8_t *adt, int layer, int entry, int W, int32_t *out_ids,
+                    int32_t *out_d, or_counters *c) {
+    qctx q = {adt, NULL};
+    return layer_search_q(g, &q, layer, entry, W, out_ids, out_d, c);
+}
+
+int or_layer_search_exact(or_graph *g, const float *qvec, int layer, int entry, int W,
+                          int32_t *out_ids, int32_t *out_d, or_counters *c) {
+    qctx q = {NULL, qvec};
+    return layer_search_q(g, &q, layer, entry, W, out_ids, out_d, c);
+}
+
 int or_hill_climb(or_graph *g, const uint8_t *adt, int layer, int entry, int *out_d,
                   or_counters *c) {
+    qctx q = {adt, NULL};
     int cur = entry;
-    int curd = adt_sum(adt, g->codes + (size_t)entry * g->cs, g->m);
-    hill_climb_impl(g, adt, layer, &cur, &curd, c);
-    if (out_d) *out_d = curd;
+    uint32_t curd = qdist(g, &q, entry);
+    hill_climb_impl(g, &q, layer, &cur, &curd, c);
+    if (out_d) *out_d = (int)curd;
     return cur;
 }
 
 /* reverse_add (_core.pyx:441-477) */
 static void reverse_add(or_graph *g, const uint8_t *sdt, int y, int x, int layer, uint64_t *pairs,
-                        int32_t *cid, double *cd, int32_t *sel, or_counters *c) {
+                        int32_t *cid, uint32_t *cd, int32_t *sel, or_counters *c) {
     int cap = layer == 0 ? g->cap0 : g->capU;
     int32_t *ids = row_of(g, layer, y);
     int32_t *cntp = cnt_of(g, layer, y);
@@ -411,20 +482,18 @@ static void reverse_add(or_graph *g, const uint8_t *sdt, int y, int x, int layer
         return;
     }
     if (c) c->reverse_prunes++;
-    const uint8_t *cy = g->codes + (size_t)y * g->cs;
     for (int j = 0; j <= cnt; ++j) {
         int u = j < cnt ? ids[j] : x;
-        uint64_t d = (uint64_t)or_sdt_sum(sdt, cy, g->codes + (size_t)u * g->cs, g->m);
+        uint64_t d = (uint64_t)pdist(g, sdt, y, u);
         pairs[j] = (d << 32) | (uint32_t)u; /* (d, id) order == fa_pair_cmp */
     }
     if (c) c->sym_comps += cnt + 1;
     qsort(pairs, (size_t)cnt + 1, sizeof(uint64_t), cmp_u64);
     for (int j = 0; j <= cnt; ++j) {
         cid[j] = (int32_t)(pairs[j] & 0xffffffffu);
-        cd[j] = (double)(pairs[j] >> 32);
+        cd[j] = (uint32_t)(pairs[j] >> 32);
     }
-    int nk = or_select(sdt, g->m, g->codes, g->cs, cid, cd, cnt + 1, cap, sel,
-                       c ? &c->sym_comps : NULL);
+    int nk = select_g(g, sdt, cid, cd, cnt + 1, cap, sel, c ? &c->sym_comps : NULL);
     for (int j = 0; j < cap; ++j) ids[j] = j < nk ? sel[j] : -1;
     *cntp = nk;
 }
@@ -481,24 +550,27 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
     or_reset(g);
     if (g->n == 0) return 0;
     int m = g->m;
-    /* codes are the fp32-tree codes (prep_qctx overwrite, _core.pyx:493-498) */
+    const int exact = g->kind == 0;
+    /* Flash: codes are the fp32-tree codes (prep_qctx overwrite,
+     * _core.pyx:493-498); exact: proj holds the vectors themselves */
     uint8_t *adts = NULL;
     int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
-    for (int64_t v = 0; v < g->n; ++v)
-        or_encode_adt(proj + (size_t)v * dproj, cent, dims, offs, m, dmax, dmin, delta,
-                      g->codes + (size_t)v * g->cs, NULL);
+    if (!exact)
+        for (int64_t v = 0; v < g->n; ++v)
+            or_encode_adt(proj + (size_t)v * dproj, cent, dims, offs, m, dmax, dmin, delta,
+                          g->codes + (size_t)v * g->cs, NULL);
     int32_t *starts = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
     int32_t *sizes = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
     int nb = or_schedule(g->levels, g->n, batch_max, batch_frac, seq_prefix, starts, sizes);
     int maxB = 1;
     for (int b = 0; b < nb; ++b)
         if (sizes[b] > maxB) maxB = sizes[b];
-    adts = (uint8_t *)malloc((size_t)m * 16);
+    adts = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
     scratch s;
     if (scratch_init(&s, g->n, C, capmax)) return -1;
     uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(C + 1));
     int32_t *cid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
-    double *cd = (double *)malloc(sizeof(double) * (size_t)(C + capmax + 2));
+    uint32_t *cd = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(C + capmax + 2));
     int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
     uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 2));
     int maxlev = 0;
@@ -514,23 +586,26 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
         for (int p = 0; p < sizes[b]; ++p) {
             int x = starts[b] + p;
             int level = g->levels[x];
-            uint8_t code_tmp[256];
-            or_encode_adt(proj + (size_t)x * dproj, cent, dims, offs, m, dmax, dmin, delta, code_tmp,
-                          adts);
+            qctx q = {adts, proj + (size_t)x * dproj};
+            if (!exact) {
+                uint8_t code_tmp[256];
+                or_encode_adt(proj + (size_t)x * dproj, cent, dims, offs, m, dmax, dmin, delta,
+                              code_tmp, adts);
+            }
             int cur = bep;
-            int curd = adt_sum(adts, g->codes + (size_t)cur * g->cs, m);
+            uint32_t curd = qdist(g, &q, cur);
             c->dist_comps++;
             for (int layer = bml; layer > level; --layer)
-                hill_climb_impl(g, adts, layer, &cur, &curd, c);
+                hill_climb_impl(g, &q, layer, &cur, &curd, c);
             int top = bml < level ? bml : level;
             for (int layer = top; layer >= 0; --layer) {
                 s.salt = tie_salt(g->tie, (uint32_t)x);
-                int ts = layer_search_impl(g, &s, adts, layer, cur, curd, C, T, c);
+                int ts = layer_search_impl(g, &s, &q, layer, cur, curd, C, T, c);
                 for (int j = 0; j < ts; ++j) {
                     cid[j] = (int32_t)(T[j] & 0xffffffffu);
-                    cd[j] = (double)(T[j] >> 32);
+                    cd[j] = (uint32_t)(T[j] >> 32);
                 }
-                int nsel = or_select(sdt, m, g->codes, g->cs, cid, cd, ts, R, sel, &c->sym_comps);
+                int nsel = select_g(g, sdt, cid, cd, ts, R, sel, &c->sym_comps);
                 int cap = layer == 0 ? g->cap0 : g->capU;
                 int32_t *row = row_of(g, layer, x);
                 for (int j = 0; j < cap; ++j) row[j] = j < nsel ? sel[j] : -1;
@@ -542,7 +617,7 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
                     req[nreq++] = (rowg << 32) | (uint32_t)x;
                 }
                 cur = (int)(T[0] & 0xffffffffu);
-                curd = (int)(T[0] >> 32);
+                curd = (uint32_t)(T[0] >> 32);
             }
             if (level > ml) {
                 ep = x;
@@ -583,7 +658,7 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
     int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
     scratch s;
     if (scratch_init(&s, g->n, ef, capmax)) return -1;
-    uint8_t *adt = (uint8_t *)malloc((size_t)m * 16);
+    uint8_t *adt = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
     uint8_t code[256];
     uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(ef + 1));
     typedef struct {
@@ -592,13 +667,17 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
     } pair;
     pair *pr = (pair *)malloc(sizeof(pair) * (size_t)(ef + 1));
     for (int q = 0; q < nq; ++q) {
-        or_encode_adt(qproj + (size_t)q * dproj, cent, dims, offs, m, dmax, dmin, delta, code, adt);
+        qctx qc = {adt, queries + (size_t)q * dim};
+        if (g->kind != 0)
+            or_encode_adt(qproj + (size_t)q * dproj, cent, dims, offs, m, dmax, dmin, delta, code,
+                          adt);
         int cur = entry;
-        int curd = adt_sum(adt, g->codes + (size_t)cur * g->cs, m);
+        uint32_t curd = qdist(g, &qc, cur);
         if (c) c->dist_comps++;
-        for (int layer = max_layer; layer > 0; --layer) hill_climb_impl(g, adt, layer, &cur, &curd, c);
+        for (int layer = max_layer; layer > 0; --layer)
+            hill_climb_impl(g, &qc, layer, &cur, &curd, c);
         s.salt = tie_salt(g->tie, (uint32_t)q);
-        int ts = layer_search_impl(g, &s, adt, 0, cur, curd, ef, T, c);
+        int ts = layer_search_impl(g, &s, &qc, 0, cur, curd, ef, T, c);
         int64_t *oi = out_ids + (size_t)q * k;
         double *od = out_d + (size_t)q * k;
         if (rerank_depth > 0) {
@@ -625,7 +704,7 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
         } else {
             for (int j = 0; j < k; ++j) {
                 oi[j] = j < ts ? (int64_t)(T[j] & 0xffffffffu) : -1;
-                od[j] = j < ts ? (double)(T[j] >> 32) : INFINITY;
+                od[j] = j < ts ? dist_value(g, (uint32_t)(T[j] >> 32)) : INFINITY;
             }
         }
     }

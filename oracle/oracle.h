@@ -23,6 +23,9 @@ typedef struct {
     const int32_t *upper_owner; /* nU: vertex owning each upper row */
     int tie;                    /* 0: ties by id; 1: by the scrambled id    */
     int expand;                 /* frontier entries expanded per step (<=1: 1) */
+    int kind;                   /* 4 Flash (u8 table distances), 0 exact (fp32 L2) */
+    const float *vecs;          /* exact: n x dim vectors                    */
+    int dim;
 } or_graph;
 
 typedef struct {
@@ -43,6 +46,9 @@ int or_select(const uint8_t *sdt, int m, const uint8_t *codes, int cs, const int
 void or_reset(or_graph *g);
 int or_layer_search(or_graph *g, const uint8_t *adt, int layer, int entry, int W, int32_t *out_ids,
                     int32_t *out_d, or_counters *c);
+/* exact kind: query vector instead of a table; out_d = fp32 distance bits */
+int or_layer_search_exact(or_graph *g, const float *qvec, int layer, int entry, int W,
+                          int32_t *out_ids, int32_t *out_d, or_counters *c);
 int or_hill_climb(or_graph *g, const uint8_t *adt, int layer, int entry, int *out_d,
                   or_counters *c);
 int or_schedule(const int32_t *levels, int64_t n, int batch_max, double batch_frac, int seq_prefix,
