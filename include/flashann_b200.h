@@ -253,6 +253,24 @@ int fa_search_batch_host(int64_t n, int dim, const float *vecs, int dproj, const
                          const float *queries, const float *qproj, int nq, int ef, int k,
                          int rerank_depth, int64_t *out_ids, double *out_d, int64_t *counters);
 
+/* The exact strategy (kind 0; asym_one / sym_one of K_EXACT, _core.pyx:
+ * 167-191): every distance is the fp32 L2 of the vectors (fa_l2sq_f32 tree),
+ * blocks carry no code region (code_subspaces = 0).  A device index created
+ * with m = 0 (and vecs, dim) is an exact-kind index; these are its host
+ * drop-ins for build_graph / search_batch with kind 0.  C, ef <= 512.        */
+int fa_build_graph_exact_host(int64_t n, int dim, const float *vecs, const int32_t *levels,
+                              uint8_t *base_blocks, int64_t base_stride, const int64_t *uoff,
+                              uint8_t *upper_blocks, int64_t n_upper_rows, int64_t upper_stride,
+                              int C, int R, const fa_build_opts *opts, fa_build_result *res);
+
+int fa_search_batch_exact_host(int64_t n, int dim, const float *vecs, const int32_t *levels,
+                               const uint8_t *base_blocks, int64_t base_stride,
+                               const int64_t *uoff, const uint8_t *upper_blocks,
+                               int64_t n_upper_rows, int64_t upper_stride, int R, int64_t entry,
+                               int max_layer, const float *queries, int nq, int ef, int k,
+                               int rerank_depth, int64_t *out_ids, double *out_d,
+                               int64_t *counters);
+
 #ifdef __cplusplus
 }
 #endif

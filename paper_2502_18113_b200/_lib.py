@@ -93,6 +93,11 @@ _SIGS = {
                                        vp, vp, f64, f64, vp, vp, i64, vp, vp, i64, i64, C.c_int,
                                        i64, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int,
                                        C.c_int, vp, vp, vp]),
+    "fa_build_graph_exact_host": (C.c_int, [i64, C.c_int, vp, vp, vp, i64, vp, vp, i64, i64,
+                                            C.c_int, C.c_int, vp, vp]),
+    "fa_search_batch_exact_host": (C.c_int, [i64, C.c_int, vp, vp, vp, i64, vp, vp, i64, i64,
+                                             C.c_int, i64, C.c_int, vp, C.c_int, C.c_int,
+                                             C.c_int, C.c_int, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

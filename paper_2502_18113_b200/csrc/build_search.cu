@@ -7,7 +7,10 @@ namespace fa {
 // One warp inserts one vertex of the batch: descent, per-layer beam search of
 // width C, forward selection (cap R), forward row write, reverse requests.
 // Mirrors insert_one (_core.pyx:501-536) against the graph as of batch start.
-template <int J, int EM>
+// P = FlashDist: the per-insertion query tables come in adt_batch and forward
+// selection uses the SDT (sdtT); P = ExactDist: the query is the inserted
+// vertex's own vector and every distance is fp32 L2.
+template <typename P, int J, int EM>
 __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
@@ -31,21 +34,26 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         const long long t_begin = clock64();
         const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
         __syncwarp();
-        load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
+        if constexpr (P::kExact) {
+            float *qv = reinterpret_cast<float *>(ws.adt);
+            for (int i = lane; i < g.dim; i += 32) qv[i] = __ldg(g.vecs + (size_t)x * g.dim + i);
+        } else {
+            load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
+        }
         __syncwarp();
         SearchCounters cnt = {};
         const int level = __ldg(g.levels + x);
         int cur = ep;
-        uint32_t curd = adt_one(ws.adt, g.codes + (size_t)ep * g.mpad, g.mpad, lane);
+        uint32_t curd = P::one(g, ws.adt, ep, lane);
         cnt.dist += 1;
         for (int layer = ml; layer > level; --layer)
-            hill_climb(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+            hill_climb<P>(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
         const int top = min(ml, level);
         unsigned long long *myreq = req + __ldg(req_off + p);
         long long sel_cycles = 0;
         for (int layer = top; layer >= 0; --layer) {
             int ts = 0;
-            bool ok = layer_search<J, EM>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
+            bool ok = layer_search<P, J, EM>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                                    ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
             if (!ok) {
                 if (lane == 0) atomicExch(err, 1);
@@ -57,14 +65,27 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
             const unsigned long long *T = ws.T;
             const long long t_sel = clock64();
             int32_t *kept;
-            int nsel = warp_select_tv(
-                sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
-                [&](int j, int &v, uint32_t &dv) {
-                    unsigned long long k = T[j];
-                    v = to.back((uint32_t)key_id(k));
-                    dv = key_d(k);
-                },
-                reinterpret_cast<uint8_t *>(ws.H), lane, &sym, kept);
+            int nsel;
+            if constexpr (P::kExact) {
+                kept = reinterpret_cast<int32_t *>(ws.H);
+                nsel = warp_select_exact(
+                    g, ts, R,
+                    [&](int j, int &v, uint32_t &dv) {
+                        unsigned long long k = T[j];
+                        v = to.back((uint32_t)key_id(k));
+                        dv = key_d(k);
+                    },
+                    kept, nullptr, lane, &sym);
+            } else {
+                nsel = warp_select_tv(
+                    sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,
+                    [&](int j, int &v, uint32_t &dv) {
+                        unsigned long long k = T[j];
+                        v = to.back((uint32_t)key_id(k));
+                        dv = key_d(k);
+                    },
+                    reinterpret_cast<uint8_t *>(ws.H), lane, &sym, kept);
+            }
             cnt.sym += sym;
             sel_cycles += clock64() - t_sel;
             // forward row of x (write_forward, _core.pyx:424-438); rows past the
@@ -109,17 +130,30 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
 BuildSearchFn build_search_variant(int W, int expand) {
     const int v = set_variant(W);
     if (expand > 1) {
-        if (v == 0) return build_search_kernel<0, 1>;
-        return v <= 8 ? build_search_kernel<8, kMaxExpand> : build_search_kernel<16, kMaxExpand>;
+        if (v == 0) return build_search_kernel<FlashDist, 0, 1>;
+        return v <= 8 ? build_search_kernel<FlashDist, 8, kMaxExpand>
+                      : build_search_kernel<FlashDist, 16, kMaxExpand>;
     }
     switch (v) {
-        case 2: return build_search_kernel<2, 1>;
-        case 4: return build_search_kernel<4, 1>;
-        case 7: return build_search_kernel<7, 1>;
-        case 8: return build_search_kernel<8, 1>;
-        case 10: return build_search_kernel<10, 1>;
-        case 16: return build_search_kernel<16, 1>;
-        default: return build_search_kernel<0, 1>;
+        case 2: return build_search_kernel<FlashDist, 2, 1>;
+        case 4: return build_search_kernel<FlashDist, 4, 1>;
+        case 7: return build_search_kernel<FlashDist, 7, 1>;
+        case 8: return build_search_kernel<FlashDist, 8, 1>;
+        case 10: return build_search_kernel<FlashDist, 10, 1>;
+        case 16: return build_search_kernel<FlashDist, 16, 1>;
+        default: return build_search_kernel<FlashDist, 0, 1>;
+    }
+}
+
+BuildSearchFn build_search_exact_variant(int W) {
+    switch (set_variant(W)) {
+        case 2: return build_search_kernel<ExactDist, 2, 1>;
+        case 4: return build_search_kernel<ExactDist, 4, 1>;
+        case 7: return build_search_kernel<ExactDist, 7, 1>;
+        case 8: return build_search_kernel<ExactDist, 8, 1>;
+        case 10: return build_search_kernel<ExactDist, 10, 1>;
+        case 16: return build_search_kernel<ExactDist, 16, 1>;
+        default: return nullptr;  // W > kRegSetMax: not served for the exact kind
     }
 }
 

@@ -250,3 +250,82 @@ extern "C" int fa_search_batch_host(int64_t n, int dim, const float *vecs, int d
     FA_CUDA(cudaMemcpy(out_d, dd.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToHost));
     return FA_OK;
 }
+
+extern "C" int fa_build_graph_exact_host(int64_t n, int dim, const float *vecs,
+                                         const int32_t *levels, uint8_t *base_blocks,
+                                         int64_t base_stride, const int64_t *uoff,
+                                         uint8_t *upper_blocks, int64_t n_upper_rows,
+                                         int64_t upper_stride, int C, int R,
+                                         const fa_build_opts *opts, fa_build_result *res) {
+    FA_CHECK_ARG(n >= 0 && dim >= 1 && R >= 1, "bad sizes");
+    if (n == 0) {
+        memset(res, 0, sizeof(*res));
+        res->entry_point = -1;
+        res->max_layer = -1;
+        return FA_OK;
+    }
+    DevBuf dvecs, dlev, duoff, dbase, dupper;
+    FA_TRY(dvecs.upload(vecs, sizeof(float) * n * dim));
+    FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
+    FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
+    fa_index_desc d;
+    memset(&d, 0, sizeof(d));
+    d.n = n; d.m = 0; d.R = R; d.dim = dim; d.dproj = dim;
+    d.vecs = dvecs.as<float>(); d.levels = dlev.as<int32_t>(); d.uoff = duoff.as<int64_t>();
+    d.n_upper_rows = n_upper_rows;
+    IndexGuard guard;
+    FA_TRY(fa_index_create(&d, &guard.ix));
+    FA_TRY(fa_index_build(guard.ix, opts, res, nullptr));
+    FA_TRY(dbase.alloc((size_t)n * base_stride));
+    FA_TRY(dupper.alloc((size_t)n_upper_rows * upper_stride));
+    FA_TRY(fa_index_export_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
+                                  upper_stride, nullptr));
+    FA_CUDA(cudaDeviceSynchronize());
+    FA_TRY(staged_copy(base_blocks, dbase.p, (size_t)n * base_stride, true));
+    if (n_upper_rows)
+        FA_TRY(staged_copy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride, true));
+    return FA_OK;
+}
+
+extern "C" int fa_search_batch_exact_host(int64_t n, int dim, const float *vecs,
+                                          const int32_t *levels, const uint8_t *base_blocks,
+                                          int64_t base_stride, const int64_t *uoff,
+                                          const uint8_t *upper_blocks, int64_t n_upper_rows,
+                                          int64_t upper_stride, int R, int64_t entry,
+                                          int max_layer, const float *queries, int nq, int ef,
+                                          int k, int rerank_depth, int64_t *out_ids,
+                                          double *out_d, int64_t *counters) {
+    if (entry < 0) {
+        set_error("cannot search an empty graph");
+        return FA_EEMPTY;
+    }
+    FA_CHECK_ARG(n > 0 && dim >= 1 && R >= 1 && k >= 1, "bad sizes");
+    if (nq == 0) {
+        if (counters) memset(counters, 0, 4 * sizeof(int64_t));
+        return FA_OK;
+    }
+    DevBuf dvecs, dlev, duoff, dbase, dupper, dq, did, dd;
+    FA_TRY(dvecs.upload(vecs, sizeof(float) * n * dim));
+    FA_TRY(dq.upload(queries, sizeof(float) * (size_t)nq * dim));
+    FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
+    FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
+    FA_TRY(dbase.upload(base_blocks, (size_t)n * base_stride));
+    FA_TRY(dupper.upload(upper_blocks, (size_t)n_upper_rows * upper_stride));
+    FA_TRY(did.alloc(sizeof(int64_t) * (size_t)nq * k));
+    FA_TRY(dd.alloc(sizeof(double) * (size_t)nq * k));
+    fa_index_desc d;
+    memset(&d, 0, sizeof(d));
+    d.n = n; d.m = 0; d.R = R; d.dim = dim; d.dproj = dim;
+    d.vecs = dvecs.as<float>(); d.levels = dlev.as<int32_t>(); d.uoff = duoff.as<int64_t>();
+    d.n_upper_rows = n_upper_rows;
+    IndexGuard guard;
+    FA_TRY(fa_index_create(&d, &guard.ix));
+    FA_TRY(fa_index_import_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
+                                  upper_stride, nullptr));
+    FA_TRY(fa_index_search(guard.ix, dq.as<float>(), dq.as<float>(), nq, ef, k, rerank_depth,
+                           entry, max_layer, did.as<int64_t>(), dd.as<double>(), counters,
+                           nullptr));
+    FA_CUDA(cudaMemcpy(out_ids, did.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToHost));
+    FA_CUDA(cudaMemcpy(out_d, dd.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToHost));
+    return FA_OK;
+}

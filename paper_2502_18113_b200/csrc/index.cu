@@ -190,7 +190,10 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     // search keys carry 24-bit vertex ids (d << 24 | tie id)
     FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 24), "n=%lld out of range [0, 2^24)",
                  (long long)desc->n);
-    FA_CHECK_ARG(desc->m >= 1 && desc->m <= 128, "m=%d outside [1,128]", desc->m);
+    // m = 0: the exact strategy (kind 0, code_subspaces = 0): fp32 L2 over vecs
+    FA_CHECK_ARG(desc->m >= 0 && desc->m <= 128, "m=%d outside [0,128]", desc->m);
+    FA_CHECK_ARG(desc->m > 0 || (desc->vecs && desc->dim >= 1),
+                 "the exact kind (m = 0) needs the vectors");
     FA_CHECK_ARG(desc->R >= 1, "R must be >= 1");
     FA_CHECK_ARG(2 * desc->R <= 127, "base capacity 2R=%d exceeds 127", 2 * desc->R);
     fa_index *ix = new fa_index();
@@ -206,6 +209,8 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.nU = desc->n_upper_rows;
     g.levels = desc->levels;
     g.uoff = desc->uoff;
+    g.vecs = desc->vecs;
+    g.dim = desc->dim;
     int rc = FA_OK;
     auto fail = [&](int r) {
         fa_index_destroy(ix);
@@ -294,6 +299,7 @@ extern "C" int fa_index_set_search_tie(fa_index *ix, int mode) {
 
 extern "C" int fa_index_encode(fa_index *ix, void *stream) {
     FA_CHECK_ARG(ix, "null index");
+    if (ix->g.m == 0) return FA_OK;  // exact kind: no codes
     FA_CHECK_ARG(ix->d.proj, "index has no projected vectors to encode");
     cudaStream_t st = as_stream(stream);
     FA_CUDA(cudaMemsetAsync(ix->codes, 0, (size_t)ix->g.n * ix->g.mpad, st));
@@ -304,7 +310,9 @@ extern "C" int fa_index_encode(fa_index *ix, void *stream) {
 
 extern "C" int fa_index_set_codes(fa_index *ix, const uint8_t *codes, int code_stride,
                                   void *stream) {
-    FA_CHECK_ARG(ix && codes, "null argument");
+    FA_CHECK_ARG(ix, "null index");
+    if (ix->g.m == 0) return FA_OK;  // exact kind: no codes
+    FA_CHECK_ARG(codes, "null codes");
     FA_CHECK_ARG(code_stride >= ix->g.m, "code_stride < m");
     cudaStream_t st = as_stream(stream);
     FA_CUDA(cudaMemsetAsync(ix->codes, 0, (size_t)ix->g.n * ix->g.mpad, st));
@@ -338,7 +346,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int C = opts->C;
     const int R = ix->d.R;
     FA_CHECK_ARG(C >= 1 && C <= 2048, "C=%d outside [1,2048]", C);
-    FA_CHECK_ARG(ix->d.sdt, "index has no SDT");
+    const bool exact = g.m == 0;  // kind 0: fp32 L2 everywhere
+    FA_CHECK_ARG(exact || ix->d.sdt, "index has no SDT");
+    FA_CHECK_ARG(!exact || C <= kRegSetMax, "the exact kind serves C <= %d", kRegSetMax);
     cudaStream_t st = as_stream(stream);
     memset(res, 0, sizeof(*res));
     res->entry_point = -1;
@@ -354,7 +364,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         ix->max_layer = -1;
         return FA_OK;
     }
-    FA_CHECK_ARG(ix->d.proj, "build needs the projected vectors (per-insertion tables)");
+    FA_CHECK_ARG(exact || ix->d.proj, "build needs the projected vectors (per-insertion tables)");
     const int Bmax = opts->batch_max > 0 ? opts->batch_max : 65536;
     const double frac = opts->batch_frac > 0 ? opts->batch_frac : 0.2;
     const int prefix = opts->seq_prefix >= 0 ? opts->seq_prefix : 256;
@@ -400,26 +410,30 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
 
     // ---- scratch ----
     const int capmax = std::max(g.cap0, g.capU);
+    if (exact) gb.expand = 1;
     WarpLayout L;
     L.init(g.mpad, C, capmax,
            pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2,
-                          (size_t)round_up(C, 32) * 8 + select_tv_bytes(g.m, g.mpad, R)),
-           gb.expand, true);
-    const size_t sdt_bytes = round_up(g.m * 256, 128);
+                          (size_t)round_up(C, 32) * 8 +
+                              (exact ? round_up(R * 4, 16) : select_tv_bytes(g.m, g.mpad, R))),
+           gb.expand, true, exact ? g.dim * 4 : -1, exact ? 8 : 4);
+    const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
     const size_t smem_search = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
                  smem_search);
-    const BuildSearchFn search_fn = build_search_variant(C, gb.expand);
+    const BuildSearchFn search_fn =
+        exact ? build_search_exact_variant(C) : build_search_variant(C, gb.expand);
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
     RL.init(capmax, g.m, g.mpad);
+    const void *rev_fn = exact ? (const void *)reverse_exact_kernel : (const void *)reverse_kernel;
     const size_t smem_rev = (size_t)kReverseWarps * RL.total;
-    FA_CUDA(cudaFuncSetAttribute(reverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FA_CUDA(cudaFuncSetAttribute(rev_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));
 
     int rev_per_sm = 0;
-    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, reverse_kernel,
+    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, rev_fn,
                                                           kReverseWarps * 32, smem_rev));
     const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * kNumSMs;
     int search_per_sm = 0;
@@ -510,8 +524,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }                                                                                \
     } while (0)
     FA_BUILD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 8, st));
-    transpose_sdt_kernel<<<1, 256, 0, st>>>(ix->d.sdt, g.m, sdtT);
-    FA_BUILD_CUDA(cudaGetLastError());
+    if (!exact) {
+        transpose_sdt_kernel<<<1, 256, 0, st>>>(ix->d.sdt, g.m, sdtT);
+        FA_BUILD_CUDA(cudaGetLastError());
+    }
     FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
                                   cudaMemcpyHostToDevice, st));
@@ -526,12 +542,15 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 0], st));
-        rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size, ix->d.dproj,
-                               ix->d.cent, ix->d.dims, ix->d.offs, g.m, ix->d.dmax,
-                               ix->d.dist_min, ix->d.delta, nullptr, g.mpad, adt_batch, g.mpad, st);
-        if (rc) {
-            cleanup();
-            return rc;
+        if (!exact) {
+            rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size,
+                                   ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs, g.m,
+                                   ix->d.dmax, ix->d.dist_min, ix->d.delta, nullptr, g.mpad,
+                                   adt_batch, g.mpad, st);
+            if (rc) {
+                cleanup();
+                return rc;
+            }
         }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
         // nheads[0]: reverse row heads, nheads[1]: the search's work counter
@@ -552,9 +571,13 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         // persistent warps pull row segments; never more warps than requests
         int rgrid = (int)std::min<int64_t>(rev_ctas, (b.nreq + 32 * kReverseWarps - 1) /
                                                           (32 * kReverseWarps) + 1);
-        reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
-            gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL,
-            ctr);
+        if (exact)
+            reverse_exact_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
+                gb, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
+        else
+            reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
+                gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg,
+                ix->upper_owner, RL, ctr);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
         launches += 4;
@@ -624,6 +647,9 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     FA_CHECK_ARG(entry < ix->g.n, "entry point out of range");
     FA_CHECK_ARG(ef >= 1 && ef <= 4096 && k >= 1, "need 1 <= k, 1 <= ef <= 4096");
     FA_CHECK_ARG(rerank_depth == 0 || (ix->d.vecs && queries), "rerank needs vectors and queries");
+    const bool exact = ix->g.m == 0;
+    FA_CHECK_ARG(!exact || queries, "the exact kind searches with the query vectors");
+    FA_CHECK_ARG(!exact || ef <= kRegSetMax, "the exact kind serves ef <= %d", kRegSetMax);
     cudaStream_t st = as_stream(stream);
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
@@ -633,14 +659,14 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     L.init(ix->g.mpad, ef, capmax,
            pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0,
                           (size_t)8 * std::min(std::max(rerank_depth, 0), ef)),
-           1);
+           1, false, exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
-    const QuerySearchFn qfn = query_search_variant(ef);
+    const QuerySearchFn qfn = query_search_variant(ef, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     uint8_t *adt_q = nullptr;
-    FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
+    if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
     int *err = nullptr;
     int rc = dev_alloc((void **)&ctr, 8 * sizeof(unsigned long long));
@@ -690,16 +716,20 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
     FA_TRY(ensure_gvis(ix));
+    // exact kind: qproj holds the query vectors (dim floats per row)
+    const bool exact = ix->g.m == 0;
+    FA_CHECK_ARG(!exact || width <= kRegSetMax, "the exact kind serves width <= %d", kRegSetMax);
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
-    L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1);
+    L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1, false,
+           exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
     size_t smem = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
-    const LayerSearchFn lfn = layer_search_variant(width);
+    const LayerSearchFn lfn = layer_search_variant(width, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     uint8_t *adt_q = nullptr;
-    FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
+    if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
     int *err = nullptr;
     int rc = dev_alloc((void **)&ctr, 8 * sizeof(unsigned long long));
@@ -714,7 +744,8 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
         gq.tie = ix->search_tie;
         gq.expand = 1;
         lfn<<<grid, kSearchWarps * 32, smem, st>>>(
-            gq, adt_q, nq, entries, width, layer, L, out_ids, out_d, out_n, ctr, err);
+            gq, exact ? reinterpret_cast<const uint8_t *>(qproj) : adt_q, nq, entries, width,
+            layer, L, out_ids, out_d, out_n, ctr, err);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -72,8 +72,10 @@ using LayerSearchFn = void (*)(Graph, const uint8_t *, int, const int64_t *, int
 // Kernel instantiations per result-set variant (set_variant(W)) and, for the
 // build, per expansion width (1 or kMaxExpand).
 BuildSearchFn build_search_variant(int W, int expand);
-QuerySearchFn query_search_variant(int W);
-LayerSearchFn layer_search_variant(int W);
+BuildSearchFn build_search_exact_variant(int W);  // null when W > kRegSetMax
+// exact = true: the exact-kind instantiations (null when W > kRegSetMax)
+QuerySearchFn query_search_variant(int W, bool exact);
+LayerSearchFn layer_search_variant(int W, bool exact);
 
 struct ReverseLayout {
     int tdom, tkeep, row, rowd, keptd, cand, sel, total;
@@ -101,6 +103,12 @@ __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                const int64_t *__restrict__ heads, const int *__restrict__ nheads,
                                int *__restrict__ next, const int32_t *__restrict__ upper_owner,
                                ReverseLayout L, unsigned long long *__restrict__ ctr);
+
+__global__ void reverse_exact_kernel(Graph g, const unsigned long long *__restrict__ keys,
+                                     int64_t N, const int64_t *__restrict__ heads,
+                                     const int *__restrict__ nheads, int *__restrict__ next,
+                                     const int32_t *__restrict__ upper_owner, ReverseLayout L,
+                                     unsigned long long *__restrict__ ctr);
 
 int launch_encode_adt(const float *red, int64_t n, int64_t red_stride, const float *cent,
                       const int32_t *dims, const int32_t *offs, int m, int dmax, double dmin,

@@ -288,4 +288,107 @@ __global__ void __maxnreg__(96) reverse_kernel(
     }
 }
 
+// Exact kind (kind 0): the same row segments; every prune is the reference's
+// full rule (reverse_add, _core.pyx:441-477) with fp32 L2 distances — d(y, u)
+// for the row and x, (d, id) sort, select_heur — lanes computing one
+// candidate's distance each.
+__global__ void __maxnreg__(96) reverse_exact_kernel(
+    Graph g, const unsigned long long *__restrict__ keys, int64_t N,
+    const int64_t *__restrict__ heads, const int *__restrict__ nheads, int *__restrict__ next,
+    const int32_t *__restrict__ upper_owner, ReverseLayout L, unsigned long long *__restrict__ ctr) {
+    extern __shared__ __align__(256) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    uint8_t *base = smem + wid * L.total;
+    int32_t *row_s = reinterpret_cast<int32_t *>(base + L.row);
+    unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
+    int32_t *kept = reinterpret_cast<int32_t *>(base + L.sel);
+    const int nseg = *nheads;
+    unsigned long long n_prune = 0, n_app = 0, n_sym = 0;
+    while (true) {
+        int s = 0;
+        if (lane == 0) s = atomicAdd(next, 1);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= nseg) break;
+        const int64_t h = heads[s];
+        const unsigned long long hk = keys[h];
+        const int64_t rowg = (int64_t)(hk >> 32);
+        int64_t e = -1;
+        for (int64_t b = h + 1; e < 0; b += 32) {
+            const int64_t j = b + lane;
+            const bool same = j < N && (keys[j] >> 32) == (hk >> 32);
+            const unsigned nb = __ballot_sync(0xffffffffu, !same);
+            if (nb) e = b + __ffs(nb) - 1;
+        }
+        const bool l0 = rowg < g.n;
+        const int y = l0 ? (int)rowg : upper_owner[rowg - g.n];
+        const int cap = l0 ? g.cap0 : g.capU;
+        int32_t *ids = l0 ? g.adj0 + rowg * g.cap0p : g.adjU + (rowg - g.n) * g.capUp;
+        int32_t *cntp = l0 ? g.cnt0 + rowg : g.cntU + (rowg - g.n);
+        int cnt = *cntp;
+        for (int j = lane; j < cap; j += 32) row_s[j] = ids[j];
+        const float *vy = g.vecs + (size_t)y * g.dim;
+        __syncwarp();
+        for (int64_t t = h; t < e; ++t) {
+            const int x = (int)(keys[t] & 0xffffffffu);
+            if (cnt < cap) {
+                if (lane == 0) row_s[cnt] = x;
+                ++cnt;
+                ++n_app;
+                __syncwarp();
+                continue;
+            }
+            ++n_prune;
+            for (int j = lane; j <= cap; j += 32) {
+                const int u = j < cap ? row_s[j] : x;
+                const float *vu = g.vecs + (size_t)u * g.dim;
+                const float d = l2_tree(g.dim, [&](int i) {
+                    return __fsub_rn(__ldg(vy + i), __ldg(vu + i));
+                });
+                cand[j] = ((unsigned long long)__float_as_uint(d) << 32) | (uint32_t)u;
+            }
+            __syncwarp();
+            unsigned long long mine[kRowChunks + 1];
+            int rk[kRowChunks + 1];
+#pragma unroll
+            for (int c = 0; c <= kRowChunks; ++c) {
+                const int j = c * 32 + lane;
+                rk[c] = -1;
+                if (j <= cap) {
+                    mine[c] = cand[j];
+                    rk[c] = count_less(cand, cap + 1, mine[c]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c <= kRowChunks; ++c)
+                if (rk[c] >= 0) cand[rk[c]] = mine[c];
+            __syncwarp();
+            unsigned long long sym = 0;
+            const int nk = warp_select_exact(
+                g, cap + 1, cap,
+                [&](int j, int &v, uint32_t &dv) {
+                    const unsigned long long k = cand[j];
+                    v = (int)(k & 0xffffffffu);
+                    dv = (uint32_t)(k >> 32);
+                },
+                kept, nullptr, lane, &sym);
+            n_sym += cap + 1 + sym;
+            __syncwarp();
+            for (int j = lane; j < cap; j += 32) row_s[j] = j < nk ? kept[j] : -1;
+            cnt = nk;
+            __syncwarp();
+        }
+        for (int j = lane; j < cap; j += 32) ids[j] = j < cnt ? row_s[j] : -1;
+        if (lane == 0) *cntp = cnt;
+        __syncwarp();
+    }
+    if (lane == 0 && (n_prune | n_app)) {
+        atomicAdd(ctr + 1, n_sym);
+        atomicAdd(ctr + 4, n_prune);
+        atomicAdd(ctr + 5, n_app);
+        atomicAdd(ctr + 6, n_prune);
+    }
+}
+
 }  // namespace fa

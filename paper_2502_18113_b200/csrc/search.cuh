@@ -39,6 +39,8 @@ struct Graph {
     int expand;  // frontier entries expanded per step (1 = semantic core)
     uint32_t *gvis;        // global visited tables, one per SM warp slot (or null)
     uint32_t *gvis_epoch;  // their epoch counters
+    const float *vecs;     // n x dim vectors (exact kind: every distance; rerank)
+    int dim;
 };
 
 constexpr int kMaxExpand = 8;
@@ -87,15 +89,17 @@ struct WarpLayout {
     // t_alias: the sorted results live at the end of the visited table (the
     // build: the table is dead once a layer search has sorted its results, and
     // forward selection's kept rows use only its start)
+    // ctx_bytes: the query context (default: the ADT, mpad x 16; the exact
+    // kind: the query vector, dim x 4); key_bytes: 4 (Flash) or 8 (exact)
     __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand,
-                                  bool t_alias = false) {
+                                  bool t_alias = false, int ctx_bytes = -1, int key_bytes = 4) {
         hash_log2 = hlog2;
         const int nc = cand_capacity(expand, capmax);
         const int Wp = round_up(W, 32);
         const int hbytes = 16 << vis_buckets_log2(hlog2);
         t_big = t_alias && W <= kRegSetMax;
         adt = 0;
-        hash = adt_bytes(mpad);
+        hash = ctx_bytes < 0 ? adt_bytes(mpad) : round_up(ctx_bytes, 256);
         big = hash + hbytes;  // a multiple of 256
         int o = 0;
         if (t_big) {
@@ -106,7 +110,7 @@ struct WarpLayout {
             o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
             o = round_up(o, 16);
         }
-        S = o; o += 2 * nc * 4;  // candidate keys (two buffers)
+        S = o; o += 2 * nc * key_bytes;  // candidate keys (two buffers)
         TQ = o; o += Wp * 4;     // tie queue
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
@@ -522,14 +526,102 @@ __device__ __forceinline__ uint32_t warp_maxd(const uint32_t *K, int n, int lane
     return __reduce_max_sync(0xffffffffu, mx);
 }
 
+// ---- distance policies -------------------------------------------------------
+// fp32 L2 (fa_l2sq_f32 tree, common.cuh l2_tree) of four (query, vector) pairs
+// at once: lane group g = lane / 8 handles pair g, lane k = lane % 8 owns
+// accumulator k of the 8-wide main loop.  q may live in shared memory.  The
+// result is valid in lane k == 0 of the group; null pointers = idle group.
+__device__ __forceinline__ float warp_l2_group8(const float *q, const float *__restrict__ v,
+                                                int d, int lane) {
+    const int k = lane & 7;
+    const int nfull = d >= 8 ? d / 8 : 0;
+    float acc = 0.f;
+    if (q && v)
+        for (int c = 0; c < nfull; ++c) {
+            const float e = __fsub_rn(q[8 * c + k], __ldg(v + 8 * c + k));
+            acc = __fadd_rn(acc, __fmul_rn(e, e));
+        }
+    const unsigned full = 0xffffffffu;
+    const float hi = __shfl_down_sync(full, acc, 4);
+    const float vk = (k < 4) ? __fadd_rn(acc, hi) : 0.f;  // v[k] = acc[k] + acc[k+4]
+    int i = 8 * nfull;
+    const bool four = (d - i) >= 4;
+    float wk = vk;
+    if (four && k < 4 && q && v) {
+        const float e = __fsub_rn(q[i + k], __ldg(v + i + k));
+        wk = __fmaf_rn(e, e, vk);
+    }
+    const float w2 = __shfl_down_sync(full, wk, 2);
+    const float t = __fadd_rn(wk, w2);  // lane0: w0+w2, lane1: w1+w3
+    const float t1 = __shfl_down_sync(full, t, 1);
+    float sum = __fadd_rn(t, t1);       // lane k == 0: (w0+w2)+(w1+w3)
+    if (!four && nfull == 0) sum = 0.f;
+    if (four) i += 4;
+    if (k == 0 && q && v)
+        for (; i < d; ++i) {
+            const float e = __fsub_rn(q[i], __ldg(v + i));
+            sum = __fmaf_rn(e, e, sum);
+        }
+    return sum;
+}
+
+// Flash (kind 4): keys (d << 24 | tie id) with the uint8 table distance d; the
+// query context is the query's ADT in shared memory.
+struct FlashDist {
+    using Key = uint32_t;
+    static constexpr bool kExact = false;
+    __device__ static __forceinline__ Key key(uint32_t d, uint32_t tie) { return (d << 24) | tie; }
+    __device__ static __forceinline__ void dists(const Graph &g, const uint8_t *qc,
+                                                 const int32_t *ids, int nf, uint32_t *out,
+                                                 int lane) {
+        dists_for(qc, g.codes, g.mpad, ids, nf, out, lane);
+    }
+    __device__ static __forceinline__ uint32_t one(const Graph &g, const uint8_t *qc, int v,
+                                                   int lane) {
+        return adt_one(qc, g.codes + (size_t)v * g.mpad, g.mpad, lane);
+    }
+};
+
+// Exact (kind 0, asym_one / sym_one of K_EXACT, _core.pyx:167-191): every
+// distance is the fp32 L2 of the vectors; keys (fp32 bits << 24 | tie id) —
+// the bit pattern of a non-negative float orders like its value.  The query
+// context is the query vector in shared memory.
+struct ExactDist {
+    using Key = uint64_t;
+    static constexpr bool kExact = true;
+    __device__ static __forceinline__ Key key(uint32_t d, uint32_t tie) {
+        return ((uint64_t)d << 24) | tie;
+    }
+    __device__ static __forceinline__ void dists(const Graph &g, const uint8_t *qc,
+                                                 const int32_t *ids, int nf, uint32_t *out,
+                                                 int lane) {
+        const float *q = reinterpret_cast<const float *>(qc);
+        for (int base = 0; base < nf; base += 4) {
+            const int j = base + (lane >> 3);
+            const float *v = j < nf ? g.vecs + (size_t)ids[j] * g.dim : nullptr;
+            const float s = warp_l2_group8(j < nf ? q : nullptr, v, g.dim, lane);
+            if ((lane & 7) == 0 && j < nf) out[j] = __float_as_uint(s);
+        }
+        __syncwarp();
+    }
+    __device__ static __forceinline__ uint32_t one(const Graph &g, const uint8_t *qc, int v,
+                                                   int lane) {
+        const float *q = reinterpret_cast<const float *>(qc);
+        const bool act = lane < 8;
+        const float s = warp_l2_group8(act ? q : nullptr, act ? g.vecs + (size_t)v * g.dim : nullptr,
+                                       g.dim, lane);
+        return __shfl_sync(0xffffffffu, __float_as_uint(s), 0);
+    }
+};
+
 // ---- register-resident result set (W <= kRegSetMax) -------------------------
 // Lane l owns slots l + 32 j (j < J); slot s is live iff s < ts.  Bit j of `fl`
 // marks slot j expanded.  Every loop over j is unrolled (no dynamic register
 // indexing), so pop / worst distance / eviction are register compares plus one
 // warp reduction instead of passes over shared memory.
-template <int J>
+template <int J, typename K = uint32_t>
 struct RegSet {
-    uint32_t key[J];
+    K key[J];
     uint32_t fl;
     // this lane's live slots when the set holds ts entries (a prefix of j)
     __device__ __forceinline__ static uint32_t live_mask(int ts, int lane) {
@@ -538,12 +630,12 @@ struct RegSet {
     }
     // smallest key (b1, slot j1; j1 = -1 if none) and second smallest key b2
     // over the slots of mask um
-    __device__ __forceinline__ void min2(uint32_t um, uint32_t &b1, int &j1, uint32_t &b2) const {
-        b1 = b2 = 0xffffffffu;
+    __device__ __forceinline__ void min2(uint32_t um, K &b1, int &j1, K &b2) const {
+        b1 = b2 = ~K(0);
         j1 = -1;
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const uint32_t k = key[j];
+            const K k = key[j];
             if ((um >> j) & 1u) {
                 if (j1 < 0 || k < b1) {
                     b2 = b1;
@@ -557,26 +649,27 @@ struct RegSet {
     }
     // eviction victim over the slots of mask lm: the largest distance, smallest
     // tie among those = the largest key ^ 0xFFFFFF (vf; vj = -1 if none)
-    __device__ __forceinline__ void victim(uint32_t lm, uint32_t &vf, int &vj) const {
+    __device__ __forceinline__ void victim(uint32_t lm, K &vf, int &vj) const {
         vf = 0;
         vj = -1;
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const uint32_t kf = key[j] ^ 0xffffffu;
+            const K kf = key[j] ^ K(0xffffffu);
             if (((lm >> j) & 1u) && (vj < 0 || kf > vf)) {
                 vf = kf;
                 vj = j;
             }
         }
     }
+    // largest distance (key >> 24) over the live slots
     __device__ __forceinline__ uint32_t maxd(int ts, int lane) const {
         uint32_t mx = 0;
 #pragma unroll
         for (int j = 0; j < J; ++j)
-            if (lane + 32 * j < ts) mx = max(mx, key[j] >> 24);
+            if (lane + 32 * j < ts) mx = max(mx, (uint32_t)(key[j] >> 24));
         return __reduce_max_sync(0xffffffffu, mx);
     }
-    __device__ __forceinline__ void put(int js, uint32_t k) {
+    __device__ __forceinline__ void put(int js, K k) {
 #pragma unroll
         for (int j = 0; j < J; ++j)
             if (j == js) key[j] = k;
@@ -600,11 +693,34 @@ __device__ __forceinline__ bool warp_pick_max(bool has, uint32_t best, uint32_t 
     owner = __ffs(__ballot_sync(0xffffffffu, has && best == m)) - 1;
     return true;
 }
+// 64-bit keys: the high word first, then the low word among its holders
+__device__ __forceinline__ bool warp_pick(bool has, uint64_t best, uint64_t &m, int &owner) {
+    const unsigned any = __ballot_sync(0xffffffffu, has);
+    if (!any) return false;
+    const uint32_t hi = (uint32_t)(best >> 32), lo = (uint32_t)best;
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, has ? hi : 0xffffffffu);
+    const bool cand = has && hi == mh;
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, cand ? lo : 0xffffffffu);
+    m = ((uint64_t)mh << 32) | ml;
+    owner = __ffs(__ballot_sync(0xffffffffu, cand && lo == ml)) - 1;
+    return true;
+}
+__device__ __forceinline__ bool warp_pick_max(bool has, uint64_t best, uint64_t &m, int &owner) {
+    const unsigned any = __ballot_sync(0xffffffffu, has);
+    if (!any) return false;
+    const uint32_t hi = (uint32_t)(best >> 32), lo = (uint32_t)best;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, has ? hi : 0u);
+    const bool cand = has && hi == mh;
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, cand ? lo : 0u);
+    m = ((uint64_t)mh << 32) | ml;
+    owner = __ffs(__ballot_sync(0xffffffffu, cand && lo == ml)) - 1;
+    return true;
+}
 
 // Ascending bitonic sort of the warp's 32 * J register keys; element
 // e = 32 j + lane lives in key[j] of lane `lane`.
-template <int J>
-__device__ __forceinline__ void warp_bitonic(uint32_t (&k)[J], int lane) {
+template <int J, typename K>
+__device__ __forceinline__ void warp_bitonic(K (&k)[J], int lane) {
     constexpr int N = 32 * J;
 #pragma unroll
     for (int size = 2; size <= N; size <<= 1) {
@@ -616,7 +732,7 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&k)[J], int lane) {
                 for (int j = 0; j < J; ++j) {
                     if ((j & rsd) == 0) {
                         const bool up = ((32 * j) & size) == 0;
-                        const uint32_t a = k[j], b = k[j | rsd];
+                        const K a = k[j], b = k[j | rsd];
                         k[j] = up ? min(a, b) : max(a, b);
                         k[j | rsd] = up ? max(a, b) : min(a, b);
                     }
@@ -624,7 +740,7 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&k)[J], int lane) {
             } else {
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
-                    const uint32_t o = __shfl_xor_sync(0xffffffffu, k[j], stride);
+                    const K o = __shfl_xor_sync(0xffffffffu, k[j], stride);
                     const bool up = ((32 * j + lane) & size) == 0;
                     const bool lower = (lane & stride) == 0;
                     k[j] = (up == lower) ? min(k[j], o) : max(k[j], o);
@@ -634,9 +750,9 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&k)[J], int lane) {
     }
 }
 
-template <int J, int EM>
+template <typename P, int J, int EM>
 __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int entry,
-                                                 uint32_t entry_d, int W, const uint8_t *adt_s,
+                                                 uint32_t entry_d, int W, const uint8_t *qc,
                                                  unsigned long long *T, int &ts_out,
                                                  unsigned long long *S, int32_t *TQ,
                                                  int32_t *fresh, uint32_t *fdist, uint32_t *H,
@@ -644,17 +760,18 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                                                  const TieOrder &to, int lane) {
     constexpr unsigned FULL = 0xffffffffu;
     const int cap = layer_cap(g, layer);
-    uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
-    uint32_t *Sb = Sa + cand_capacity(g);
+    using K = typename P::Key;
+    K *Sa = reinterpret_cast<K *>(S);
+    K *Sb = Sa + cand_capacity(g);
     const unsigned lt = (1u << lane) - 1u;
     VisitedSet vs;
     vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
     if (lane == 0) vs.visit(entry);
-    RegSet<J> rs;
+    RegSet<J, K> rs;
 #pragma unroll
-    for (int j = 0; j < J; ++j) rs.key[j] = 0u;
+    for (int j = 0; j < J; ++j) rs.key[j] = K(0);
     rs.fl = 0u;
-    if (lane == 0) rs.key[0] = k32(entry_d, to.fwd((uint32_t)entry));
+    if (lane == 0) rs.key[0] = P::key(entry_d, to.fwd((uint32_t)entry));
     int ts = 1;
     uint32_t wd = 0xffffffffu;  // worst distance once the set is full
     int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
@@ -670,19 +787,19 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         int npop = 0;
         int u[EM][kRowChunks];
         if (EM == 1) {
-            uint32_t b1, b2;
+            K b1, b2;
             int j1;
-            const uint32_t um = RegSet<J>::live_mask(ts, lane) & ~rs.fl;
+            const uint32_t um = RegSet<J, K>::live_mask(ts, lane) & ~rs.fl;
             rs.min2(um, b1, j1, b2);
             const int nl = __popc(um);
-            uint32_t m = 0;
+            K m = 0;
             int owner = -1;
             const bool anyT = warp_pick(nl > 0, b1, m, owner);
             const bool anyQ = tq_h < tq_t;
             if (!anyT && !anyQ) break;
-            const uint32_t kQ = anyQ ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
+            const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
             const bool fromT = anyT && (!anyQ || m < kQ);
-            pv[0] = to.back((fromT ? m : kQ) & 0xffffffu);
+            pv[0] = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
             npop = 1;
             if (fromT) {
                 if (lane == owner) rs.fl |= 1u << j1;
@@ -698,14 +815,14 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             // predict the next pop assuming nothing new enters: the popped
             // lane offers its second smallest key
             const bool h2 = fromT && lane == owner ? nl > 1 : nl > 0;
-            const uint32_t c2 = fromT && lane == owner ? b2 : b1;
-            uint32_t m2 = 0;
+            const K c2 = fromT && lane == owner ? b2 : b1;
+            K m2 = 0;
             int o2 = -1;
             const bool anyT2 = warp_pick(h2, c2, m2, o2);
             const bool anyQ2 = tq_h < tq_t;
             if (anyT2 || anyQ2) {
-                const uint32_t kQ2 = anyQ2 ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
-                pre_v = to.back((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu);
+                const K kQ2 = anyQ2 ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
+                pre_v = to.back((uint32_t)((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu));
                 load_row(row_ids(g, layer, pre_v), cap, lane, pre);
             } else {
                 pre_v = -1;
@@ -714,18 +831,18 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
 #pragma unroll
             for (int r = 0; r < EM; ++r) {
                 if (r >= E) break;
-                uint32_t best, b2;
+                K best, b2;
                 int bj;
-                rs.min2(RegSet<J>::live_mask(ts, lane) & ~rs.fl, best, bj, b2);
+                rs.min2(RegSet<J, K>::live_mask(ts, lane) & ~rs.fl, best, bj, b2);
                 const bool has = bj >= 0;
-                uint32_t m = 0;
+                K m = 0;
                 int owner = -1;
                 const bool anyT = warp_pick(has, best, m, owner);
                 const bool anyQ = tq_h < tq_t;
                 if (!anyT && !anyQ) break;
-                const uint32_t kQ = anyQ ? k32(wd, (uint32_t)TQ[tq_h]) : 0u;
+                const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
                 const bool fromT = anyT && (!anyQ || m < kQ);
-                pv[r] = to.back((fromT ? m : kQ) & 0xffffffu);
+                pv[r] = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
                 ++npop;
                 if (fromT) {
                     if (lane == owner) rs.fl |= 1u << bj;
@@ -771,7 +888,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         __syncwarp();
         phase_mark(cnt, 1, tph);
         if (nf == 0) continue;
-        dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
+        P::dists(g, qc, fresh, nf, fdist, lane);
         phase_mark(cnt, 2, tph);
         // candidates that can possibly enter: all while the set is not full,
         // else d < worst
@@ -780,17 +897,17 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             const int f = base + lane;
             const bool ok = f < nf && fdist[f] < wd;
             const unsigned b = __ballot_sync(FULL, ok);
-            if (ok) Sa[ns + __popc(b & lt)] = k32(fdist[f], to.fwd((uint32_t)fresh[f]));
+            if (ok) Sa[ns + __popc(b & lt)] = P::key(fdist[f], to.fwd((uint32_t)fresh[f]));
             ns += __popc(b);
         }
         __syncwarp();
         if (ns == 0) continue;
         const int nfill = min(ns, W - ts);
-        const uint32_t *src = Sa;
+        const K *src = Sa;
         if (nfill < ns) {
             // offers are processed in ascending order: rank-sort them
             for (int j = lane; j < ns; j += 32) {
-                const uint32_t k = Sa[j];
+                const K k = Sa[j];
                 int r = 0;
                 for (int t = 0; t < ns; ++t) r += Sa[t] < k;
                 Sb[r] = k;
@@ -812,18 +929,18 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         // stale = the set changed since wd was last known
         bool stale = ts == W && nfill > 0;
         if (nfill < ns) {
-            const uint32_t lm = RegSet<J>::live_mask(ts, lane);
+            const uint32_t lm = RegSet<J, K>::live_mask(ts, lane);
             for (int j = nfill; j < ns; ++j) {
-                const uint32_t s = src[j];
+                const K s = src[j];
                 // victim: largest distance, smallest tie; its distance is the
                 // current worst
-                uint32_t vf;
+                K vf;
                 int vj;
                 rs.victim(lm, vf, vj);
-                uint32_t m = 0;
+                K m = 0;
                 int owner = 0;
                 warp_pick_max(vj >= 0, vf, m, owner);
-                const uint32_t cur = m >> 24;
+                const uint32_t cur = (uint32_t)(m >> 24);
                 if (cur < wd) {
                     // the evicted ties are beyond the new worst (none before the
                     // set first fills)
@@ -831,7 +948,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                     wd = cur;
                 }
                 stale = false;
-                if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+                if ((uint32_t)(s >> 24) >= wd) break;  // sorted: later offers are rejected too
                 const uint32_t expd = __shfl_sync(FULL, (rs.fl >> vj) & 1u, owner);
                 if (!expd) {
                     if (lane == 0) TQ[tq_t] = (int32_t)((m ^ 0xffffffu) & 0xffffffu);
@@ -855,15 +972,15 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     // (J not a power of two: the network runs over JP registers, the extra
     // ones holding the largest key)
     constexpr int JP = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : 16;
-    uint32_t ks[JP];
+    K ks[JP];
 #pragma unroll
     for (int j = 0; j < JP; ++j)
-        ks[j] = (j < J && lane + 32 * j < ts) ? rs.key[j < J ? j : 0] : 0xffffffffu;
+        ks[j] = (j < J && lane + 32 * j < ts) ? rs.key[j < J ? j : 0] : ~K(0);
     warp_bitonic<JP>(ks, lane);
 #pragma unroll
     for (int j = 0; j < JP; ++j) {
         const int e = 32 * j + lane;
-        if (e < ts) T[e] = make_key(ks[j] >> 24, (int)(ks[j] & 0xffffffu));
+        if (e < ts) T[e] = make_key((uint32_t)(ks[j] >> 24), (int)(ks[j] & 0xffffffu));
     }
     __syncwarp();
     ts_out = ts;
@@ -1056,20 +1173,23 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
 
 
 // Best-first layer search with the result-set variant J chosen by the host
-// (set_variant): J slots per lane in registers, J = 0 the shared-memory set.
-template <int J, int EM>
+// (set_variant): J slots per lane in registers, J = 0 the shared-memory set
+// (Flash only).  P: the distance policy (FlashDist / ExactDist).
+template <typename P, int J, int EM>
 __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
-                                             int W, const uint8_t *adt_s, unsigned long long *T,
+                                             int W, const uint8_t *qc, unsigned long long *T,
                                              int &ts, unsigned long long *S, int32_t *TQ,
                                              int32_t *fresh, uint32_t *fdist, uint32_t *H,
                                              int hlog2, SearchCounters &cnt, const TieOrder &to,
                                              int lane) {
-    if constexpr (J == 0)
-        return layer_search_smem(g, layer, entry, entry_d, W, adt_s, T, ts, S, TQ, fresh, fdist, H,
+    if constexpr (J == 0) {
+        static_assert(!P::kExact, "the shared-memory result set serves the Flash kind only");
+        return layer_search_smem(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
                                  hlog2, cnt, to, lane);
-    else
-        return layer_search_reg<J, EM>(g, layer, entry, entry_d, W, adt_s, T, ts, S, TQ, fresh,
-                                       fdist, H, hlog2, cnt, to, lane);
+    } else {
+        return layer_search_reg<P, J, EM>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
+                                          fdist, H, hlog2, cnt, to, lane);
+    }
 }
 
 // result-set variant for a search width W: register slots per lane, 0 = shared
@@ -1078,10 +1198,45 @@ __host__ __device__ inline int set_variant(int W) {
            : W <= kRegSetMax ? 16 : 0;
 }
 
+// select_heur (_core.pyx:388-408) of the exact kind: candidate v (distance
+// bits dv) is kept iff no kept u has fp32 L2(u, v) < dv; lanes test kept[t]
+// in parallel, each with the fa_l2sq_f32 tree (symmetric in its arguments:
+// the squared differences are equal).
+template <class Get>
+__device__ int warp_select_exact(const Graph &g, int ncand, int cap, Get get, int32_t *kept,
+                                 uint32_t *kept_d, int lane, unsigned long long *sym_count) {
+    int nk = 0;
+    unsigned long long sym = 0;
+    for (int j = 0; j < ncand && nk < cap; ++j) {
+        int v;
+        uint32_t dv;
+        get(j, v, dv);
+        const float *b = g.vecs + (size_t)v * g.dim;
+        bool bad = false;
+        for (int t = lane; t < nk; t += 32) {
+            const float *a = g.vecs + (size_t)kept[t] * g.dim;
+            const float s = l2_tree(g.dim, [&](int i) { return __fsub_rn(__ldg(a + i), __ldg(b + i)); });
+            bad |= __float_as_uint(s) < dv;
+        }
+        sym += nk;
+        if (!__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) {
+                kept[nk] = v;
+                if (kept_d) kept_d[nk] = dv;
+            }
+            ++nk;
+        }
+        __syncwarp();
+    }
+    if (sym_count && lane == 0) *sym_count += sym;
+    return nk;
+}
+
 // Width-1 greedy descent (hill_climb, _core.pyx:345-385): move to the first
 // slot holding the minimum distance while it is strictly better.
+template <typename P>
 __device__ inline void hill_climb(const Graph &g, int layer, int &cur, uint32_t &curd,
-                           const uint8_t *adt_s, int32_t *ids_s, uint32_t *d_s,
+                           const uint8_t *qc, int32_t *ids_s, uint32_t *d_s,
                            SearchCounters &cnt, int lane) {
     const int cap = layer_cap(g, layer);
     while (true) {
@@ -1098,7 +1253,7 @@ __device__ inline void hill_climb(const Graph &g, int layer, int &cur, uint32_t 
         cnt.kcalls += (nlive + 15) >> 4;
         cnt.dist += nlive;
         if (nlive == 0) break;
-        dists_for(adt_s, g.codes, g.mpad, ids_s, nlive, d_s, lane);
+        P::dists(g, qc, ids_s, nlive, d_s, lane);
         unsigned long long best = KEY_MAX;
         for (int j = lane; j < nlive; j += 32) {
             unsigned long long k = ((unsigned long long)d_s[j] << 32) | (uint32_t)j;

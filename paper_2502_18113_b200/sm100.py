@@ -76,9 +76,13 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+KIND_EXACT = 0  # providers/base.py:23-29 KIND_IDS["exact"]
+
+
 def _require_flash(kind: int) -> None:
-    if kind != KIND_FLASH:
-        raise ValueError(f"the sm100 core serves the Flash strategy (kind 4), got kind {kind}")
+    if kind not in (KIND_FLASH, KIND_EXACT):
+        raise ValueError("the sm100 core serves the Flash (4) and exact (0) strategies, "
+                         f"got kind {kind}")
 
 
 def build_options(C_: int) -> _lib.BuildOpts:
@@ -112,17 +116,32 @@ def build_graph(kind, prov, levels, base_blocks, upper_offsets, upper_blocks, C,
     bb = np.ascontiguousarray(base_blocks)
     uo = _c(upper_offsets, np.int64)
     ub = np.ascontiguousarray(upper_blocks)
-    codes = np.ascontiguousarray(prov["codes"])
-    if codes.dtype != np.uint8:
-        raise TypeError("codes must be uint8")
     n = lv.shape[0]
+    codes = None
+    if kind != KIND_EXACT:
+        codes = np.ascontiguousarray(prov["codes"])
+        if codes.dtype != np.uint8:
+            raise TypeError("codes must be uint8")
     if n == 0:
         return {"entry_point": -1, "max_layer": -1,
                 "counters": {"dist_comps": 0, "sym_comps": 0, "kernel_calls": 0, "visited": 0}}
-    cent, dims, offs, sdt, proj = _prov_arrays(prov)
-    m = cent.shape[0]
     res = _lib.BuildResult()
     opts = build_options(int(C))
+    if kind == KIND_EXACT:
+        # exact strategy: fp32 L2 of the vectors, no codes (_core.pyx:167-191)
+        vecs = _c(prov["vecs"], np.float32)
+        check(lib.fa_build_graph_exact_host(
+            n, vecs.shape[1], ptr(vecs), ptr(lv), ptr(bb), bb.shape[1], ptr(uo), ptr(ub),
+            ub.shape[0], ub.shape[1] if ub.ndim == 2 else 0, int(C), int(R), C_byref(opts),
+            C_byref(res)))
+        if bb is not base_blocks:
+            base_blocks[...] = bb
+        if ub is not upper_blocks:
+            upper_blocks[...] = ub
+        return {"entry_point": int(res.entry_point), "max_layer": int(res.max_layer),
+                "counters": res.counters()}
+    cent, dims, offs, sdt, proj = _prov_arrays(prov)
+    m = cent.shape[0]
     check(lib.fa_build_graph_host(
         n, 0, None, proj.shape[1], ptr(proj), ptr(codes), m, ptr(cent), cent.shape[2], ptr(dims),
         ptr(offs), ptr(sdt), float(prov["dist_min"]), float(prov["delta"]), ptr(lv), ptr(bb),
@@ -156,6 +175,20 @@ def search_batch(kind, prov, levels, base_blocks, upper_offsets, upper_blocks, C
     uo = _c(upper_offsets, np.int64)
     ub = np.ascontiguousarray(upper_blocks)
     qs = _c(queries, np.float32)
+    if kind == KIND_EXACT:
+        vecs = _c(prov["vecs"], np.float32)
+        nq = qs.shape[0]
+        out_ids = np.full((nq, k), -1, dtype=np.int64)
+        out_d = np.full((nq, k), np.inf, dtype=np.float64)
+        ctr = np.zeros(4, dtype=np.int64)
+        if nq:
+            check(lib.fa_search_batch_exact_host(
+                lv.shape[0], vecs.shape[1], ptr(vecs), ptr(lv), ptr(bb), bb.shape[1], ptr(uo),
+                ptr(ub), ub.shape[0], ub.shape[1] if ub.ndim == 2 else 0, int(R), int(entry),
+                int(max_layer), ptr(qs), nq, int(ef), int(k), int(rerank_depth), ptr(out_ids),
+                ptr(out_d), ptr(ctr)))
+        return out_ids, out_d, {"dist_comps": int(ctr[0]), "sym_comps": int(ctr[1]),
+                                "kernel_calls": int(ctr[2]), "visited": int(ctr[3])}
     if qaux is None:
         raise ValueError("this strategy requires a prepared query payload (qaux)")
     qp = _c(qaux, np.float32)

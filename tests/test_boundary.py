@@ -70,8 +70,12 @@ def test_no_cpu_fallback_without_device():
 
     with pytest.raises(errors.DeviceError):
         sm100.quantize_distance(np.zeros(3), 0.0, 1.0)
-    with pytest.raises(ValueError):
-        sm100.build_graph(0, {}, np.zeros(1, np.int32), None, None, None, 8, 2)
+    with pytest.raises(ValueError):  # PQ (kind 1) is not served by this core
+        sm100.build_graph(1, {}, np.zeros(1, np.int32), None, None, None, 8, 2)
+    with pytest.raises(errors.DeviceError):  # the exact kind is, on a device only
+        sm100.build_graph(0, {"vecs": np.zeros((1, 4), np.float32), "dim": 4},
+                          np.zeros(1, np.int32), np.zeros((1, 36), np.uint8),
+                          np.zeros(1, np.int64), np.zeros((0, 36), np.uint8), 8, 2)
 
 
 def test_product_never_imports_oracle():
