@@ -67,7 +67,11 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
             int32_t *kept;
             int nsel;
             if constexpr (P::kExact) {
+                // kept ids, their distances to the candidate, the candidate's
+                // vector: the start of the (dead) visited table
                 kept = reinterpret_cast<int32_t *>(ws.H);
+                uint32_t *kd = reinterpret_cast<uint32_t *>(ws.H) + round_up(R, 4);
+                float *cv = reinterpret_cast<float *>(kd + round_up(R, 4));
                 nsel = warp_select_exact(
                     g, ts, R,
                     [&](int j, int &v, uint32_t &dv) {
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
                         v = to.back((uint32_t)key_id(k));
                         dv = key_d(k);
                     },
-                    kept, nullptr, lane, &sym);
+                    kept, cv, kd, lane, &sym);
             } else {
                 nsel = warp_select_tv(
                     sdtT, g.m, g.mpad, g.codes, g.mpad, ts, R,

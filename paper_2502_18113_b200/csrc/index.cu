@@ -415,7 +415,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     L.init(g.mpad, C, capmax,
            pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2,
                           (size_t)round_up(C, 32) * 8 +
-                              (exact ? round_up(R * 4, 16) : select_tv_bytes(g.m, g.mpad, R))),
+                              (exact ? (size_t)2 * round_up(R, 4) * 4 + (size_t)g.dim * 4
+                                     : select_tv_bytes(g.m, g.mpad, R))),
            gb.expand, true, exact ? g.dim * 4 : -1, exact ? 8 : 4);
     const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
     const size_t smem_search = (size_t)kSearchWarps * L.total;
@@ -426,7 +427,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
-    RL.init(capmax, g.m, g.mpad);
+    RL.init(capmax, g.m, g.mpad, exact ? g.dim : 0);
     const void *rev_fn = exact ? (const void *)reverse_exact_kernel : (const void *)reverse_kernel;
     const size_t smem_rev = (size_t)kReverseWarps * RL.total;
     FA_CUDA(cudaFuncSetAttribute(rev_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -79,7 +79,8 @@ LayerSearchFn layer_search_variant(int W, bool exact);
 
 struct ReverseLayout {
     int tdom, tkeep, row, rowd, keptd, cand, sel, total;
-    __host__ __device__ void init(int capmax, int m, int mpad) {
+    int qv, cv, cid, cd, kd;  // exact kind: y's and a candidate's vectors, ids, distances
+    __host__ __device__ void init(int capmax, int m, int mpad, int dim = 0) {
         int o = 0;
         tdom = o; o += round_up(mpad * 16, 256);   // x's row tables (256-aligned)
         tkeep = o; o += round_up(mpad * 16, 256);
@@ -89,6 +90,14 @@ struct ReverseLayout {
         cand = o; o += 128 * 8;
         o = round_up(o, 256);
         sel = o; o += select_tv_bytes(m, mpad, capmax);  // kept ids first
+        qv = cv = cid = cd = kd = 0;
+        if (dim > 0) {
+            qv = o; o += round_up(dim * 4, 16);
+            cv = o; o += round_up(dim * 4, 16);
+            cid = o; o += round_up(capmax + 1, 32) * 4;
+            cd = o; o += round_up(capmax + 1, 32) * 4;
+            kd = o; o += round_up(capmax, 32) * 4;
+        }
         total = round_up(o, 256);
     }
 };

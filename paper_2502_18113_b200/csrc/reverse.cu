@@ -290,8 +290,8 @@ __global__ void __maxnreg__(96) reverse_kernel(
 
 // Exact kind (kind 0): the same row segments; every prune is the reference's
 // full rule (reverse_add, _core.pyx:441-477) with fp32 L2 distances — d(y, u)
-// for the row and x, (d, id) sort, select_heur — lanes computing one
-// candidate's distance each.
+// for the row and x (8-lane groups against y's vector staged in shared
+// memory), (d, id) sort, select_heur.
 __global__ void __maxnreg__(96) reverse_exact_kernel(
     Graph g, const unsigned long long *__restrict__ keys, int64_t N,
     const int64_t *__restrict__ heads, const int *__restrict__ nheads, int *__restrict__ next,
@@ -303,6 +303,11 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
     int32_t *row_s = reinterpret_cast<int32_t *>(base + L.row);
     unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
     int32_t *kept = reinterpret_cast<int32_t *>(base + L.sel);
+    float *qv = reinterpret_cast<float *>(base + L.qv);
+    float *cv = reinterpret_cast<float *>(base + L.cv);
+    int32_t *cid = reinterpret_cast<int32_t *>(base + L.cid);
+    uint32_t *cd = reinterpret_cast<uint32_t *>(base + L.cd);
+    uint32_t *kd = reinterpret_cast<uint32_t *>(base + L.kd);
     const int nseg = *nheads;
     unsigned long long n_prune = 0, n_app = 0, n_sym = 0;
     while (true) {
@@ -327,7 +332,7 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         int32_t *cntp = l0 ? g.cnt0 + rowg : g.cntU + (rowg - g.n);
         int cnt = *cntp;
         for (int j = lane; j < cap; j += 32) row_s[j] = ids[j];
-        const float *vy = g.vecs + (size_t)y * g.dim;
+        bool have_y = false;
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
             const int x = (int)(keys[t] & 0xffffffffu);
@@ -339,14 +344,15 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
                 continue;
             }
             ++n_prune;
-            for (int j = lane; j <= cap; j += 32) {
-                const int u = j < cap ? row_s[j] : x;
-                const float *vu = g.vecs + (size_t)u * g.dim;
-                const float d = l2_tree(g.dim, [&](int i) {
-                    return __fsub_rn(__ldg(vy + i), __ldg(vu + i));
-                });
-                cand[j] = ((unsigned long long)__float_as_uint(d) << 32) | (uint32_t)u;
+            if (!have_y) {
+                for (int i = lane; i < g.dim; i += 32) qv[i] = __ldg(g.vecs + (size_t)y * g.dim + i);
+                have_y = true;
             }
+            for (int j = lane; j <= cap; j += 32) cid[j] = j < cap ? row_s[j] : x;
+            __syncwarp();
+            ExactDist::dists(g, reinterpret_cast<const uint8_t *>(qv), cid, cap + 1, cd, lane);
+            for (int j = lane; j <= cap; j += 32)
+                cand[j] = ((unsigned long long)cd[j] << 32) | (uint32_t)cid[j];
             __syncwarp();
             unsigned long long mine[kRowChunks + 1];
             int rk[kRowChunks + 1];
@@ -372,7 +378,7 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
                     v = (int)(k & 0xffffffffu);
                     dv = (uint32_t)(k >> 32);
                 },
-                kept, nullptr, lane, &sym);
+                kept, cv, kd, lane, &sym);
             n_sym += cap + 1 + sym;
             __syncwarp();
             for (int j = lane; j < cap; j += 32) row_s[j] = j < nk ? kept[j] : -1;

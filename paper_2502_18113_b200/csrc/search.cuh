@@ -1199,31 +1199,31 @@ __host__ __device__ inline int set_variant(int W) {
 }
 
 // select_heur (_core.pyx:388-408) of the exact kind: candidate v (distance
-// bits dv) is kept iff no kept u has fp32 L2(u, v) < dv; lanes test kept[t]
-// in parallel, each with the fa_l2sq_f32 tree (symmetric in its arguments:
-// the squared differences are equal).
+// bits dv) is kept iff no kept u has fp32 L2(u, v) < dv.  The candidate's
+// vector is staged in shared memory (cv, dim floats) and the kept set's
+// distances to it come four at a time from 8-lane groups (the fa_l2sq_f32
+// tree, symmetric in its arguments: the squared differences are equal).
 template <class Get>
 __device__ int warp_select_exact(const Graph &g, int ncand, int cap, Get get, int32_t *kept,
-                                 uint32_t *kept_d, int lane, unsigned long long *sym_count) {
+                                 float *cv, uint32_t *kd, int lane,
+                                 unsigned long long *sym_count) {
     int nk = 0;
     unsigned long long sym = 0;
     for (int j = 0; j < ncand && nk < cap; ++j) {
         int v;
         uint32_t dv;
         get(j, v, dv);
-        const float *b = g.vecs + (size_t)v * g.dim;
         bool bad = false;
-        for (int t = lane; t < nk; t += 32) {
-            const float *a = g.vecs + (size_t)kept[t] * g.dim;
-            const float s = l2_tree(g.dim, [&](int i) { return __fsub_rn(__ldg(a + i), __ldg(b + i)); });
-            bad |= __float_as_uint(s) < dv;
+        if (nk > 0) {
+            const float *b = g.vecs + (size_t)v * g.dim;
+            for (int i = lane; i < g.dim; i += 32) cv[i] = __ldg(b + i);
+            __syncwarp();
+            ExactDist::dists(g, reinterpret_cast<const uint8_t *>(cv), kept, nk, kd, lane);
+            for (int t = lane; t < nk; t += 32) bad |= kd[t] < dv;
         }
         sym += nk;
         if (!__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) {
-                kept[nk] = v;
-                if (kept_d) kept_d[nk] = dv;
-            }
+            if (lane == 0) kept[nk] = v;
             ++nk;
         }
         __syncwarp();
