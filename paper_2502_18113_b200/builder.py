@@ -62,9 +62,13 @@ def training_sample(dataset, sample_size: int, seed: int):
     return data[sel]
 
 
-def train_provider(strategy: str, sample, sp: StrategyParams, seed: int = 0) -> FlashProvider:
+def train_provider(strategy: str, sample, sp: StrategyParams, seed: int = 0):
+    if strategy == "exact":
+        from .exact import ExactProvider
+
+        return ExactProvider()
     if strategy != "flash":
-        raise ConfigError(f"strategy {strategy!r} is outside this GPU core (only 'flash')")
+        raise ConfigError(f"strategy {strategy!r} is outside this GPU core ('flash', 'exact')")
     d_f = sp.d_f
     if d_f is None:
         from .pca import pca_train

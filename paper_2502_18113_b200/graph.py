@@ -105,11 +105,23 @@ class GraphIndex:
 
         lib = _lib.load()
         dev = provider.dev
-        model = provider.model
         lv = torch.from_numpy(self.levels).cuda()
         uo = torch.from_numpy(np.ascontiguousarray(self.upper_offsets, np.int64)).cuda()
         self._keep = [lv, uo]
         d = _lib.IndexDesc()
+        if provider.kind_id == 0:  # exact strategy: m = 0, fp32 L2 over the vectors
+            d.n, d.m, d.R = self.n, 0, self.params.R
+            d.dim = d.dproj = int(dev["vecs"].shape[1])
+            d.vecs = dev["vecs"].data_ptr()
+            d.levels, d.uoff = lv.data_ptr(), uo.data_ptr()
+            d.n_upper_rows = self.n_upper_rows
+            self._desc = d
+            h = _lib.vp()
+            check(lib.fa_index_create(C.byref(d), C.byref(h)))
+            self.handle = h
+            self._provider = provider
+            return
+        model = provider.model
         d.n, d.m, d.R = self.n, model.m, self.params.R
         d.dim = int(dev["vecs"].shape[1])
         d.dproj = int(dev["proj"].shape[1])

@@ -10,7 +10,7 @@ here loads in the reference package and vice versa: the graph sections are the
 reference vertex-block layout (exported from / imported into the device
 index), the provider sections are FlashProvider.state_dict().
 
-Only the Flash strategy exists in this package; files of other strategies are
+The Flash and exact strategies are served; files of other strategies are
 rejected with FormatError.
 """
 
@@ -85,7 +85,8 @@ def save_index(path, g: GraphIndex, provider: FlashProvider, dataset) -> None:
                 "vectors": data}
     for k, v in arrays.items():
         sections[f"prov.{k}"] = v
-    sections["codes"] = provider.core_arrays()["codes"]
+    if provider.kind in ("pq", "sq", "flash"):
+        sections["codes"] = provider.core_arrays()["codes"]
     write_sections(path, meta, sections)
 
 
@@ -124,17 +125,23 @@ def load_index(path):
     import torch
 
     meta, sec = read_sections(path)
-    if meta["strategy"] != "flash":
+    if meta["strategy"] not in ("flash", "exact"):
         raise FormatError(f"{path}: strategy {meta['strategy']!r} is not served by this package")
     state = dict(meta["provider_scalars"])
     state.update({k[5:]: v for k, v in sec.items() if k.startswith("prov.")})
-    provider = FlashProvider.from_state(state)
     dataset = VectorDataset(sec["vectors"])
-    provider.attach(dataset)
-    codes = np.ascontiguousarray(sec["codes"], dtype=np.uint8)
-    provider.dev["codes"][:, : codes.shape[1]].copy_(torch.from_numpy(codes).cuda())
+    if meta["strategy"] == "exact":
+        from .exact import ExactProvider
+
+        provider = ExactProvider.from_state(state)
+        provider.attach(dataset)
+    else:
+        provider = FlashProvider.from_state(state)
+        provider.attach(dataset)
+        codes = np.ascontiguousarray(sec["codes"], dtype=np.uint8)
+        provider.dev["codes"][:, : codes.shape[1]].copy_(torch.from_numpy(codes).cuda())
     params = BuildParams(C=meta["C"], R=meta["R"], seed=meta["seed"], threads=meta["threads"])
-    g = GraphIndex(meta["n"], meta["dim"], params, "flash", meta["code_subspaces"],
+    g = GraphIndex(meta["n"], meta["dim"], params, meta["strategy"], meta["code_subspaces"],
                    sec["levels"])
     g.create_device(provider)
     base = np.ascontiguousarray(sec["base_blocks"])

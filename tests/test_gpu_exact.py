@@ -94,3 +94,25 @@ def test_exact_batched_build_matches_oracle(core, tie):
     hq = native.HostGraph.from_blocks(levels, uoff, base, upper, R, None, kind=0, vecs=x)
     oi, od, _ = hq.search_exact(res["entry_point"], res["max_layer"], q, 32, 10)
     assert np.array_equal(ids, oi) and np.array_equal(d, od)
+
+
+def test_exact_high_level_build_and_search(core):
+    """builder.build(..., "exact") on the device index == the host drop-in."""
+    from paper_2502_18113_b200 import builder, evaluation, graph, layout
+
+    rng = np.random.default_rng(8)
+    x = (rng.normal(size=(10, 32))[rng.integers(0, 10, 3000)]
+         + 0.3 * rng.normal(size=(3000, 32))).astype(np.float32)
+    params = graph.BuildParams(C=40, R=8, seed=2)
+    res = builder.build(x, "exact", params)
+    g = res.graph
+    out, base, upper = _build(core, x, g.levels, g.upper_offsets, 8, 40)
+    assert (g.entry_point, g.max_layer) == (out["entry_point"], out["max_layer"])
+    for v in range(3000):
+        assert np.array_equal(g.neighbors(v, 0), layout.row_ids(base, v, 16)), v
+    q = rng.normal(size=(25, 32)).astype(np.float32)
+    ids, d, _ = evaluation.search_batch(g, res.provider, q, evaluation.SearchParams(ef=24, k=6))
+    ids2, d2, _ = core.search_batch(0, {"vecs": x, "dim": 32}, g.levels, base, g.upper_offsets,
+                                    upper, 40, 8, out["entry_point"], out["max_layer"], q, None,
+                                    24, 6, 0)
+    assert np.array_equal(ids, ids2) and np.array_equal(d, d2)

@@ -11,16 +11,18 @@ from paper_2502_18113_b200 import layout, serialize
 from paper_2502_18113_b200.errors import FormatError
 
 GOLD = Path(__file__).resolve().parent / "golden" / "ref_index_small.fannidx"
+GOLD_EXACT = Path(__file__).resolve().parent / "golden" / "ref_index_exact.fannidx"
 
 
-def test_reader_and_writer_are_byte_exact(tmp_path):
-    meta, sec = serialize.read_sections(GOLD)
-    assert meta["strategy"] == "flash" and meta["n"] == 400 and meta["R"] == 8
+@pytest.mark.parametrize("path,strategy", [(GOLD, "flash"), (GOLD_EXACT, "exact")])
+def test_reader_and_writer_are_byte_exact(tmp_path, path, strategy):
+    meta, sec = serialize.read_sections(path)
+    assert meta["strategy"] == strategy and meta["n"] == 400 and meta["R"] == 8
     assert list(sec)[:5] == ["levels", "base_blocks", "upper_offsets", "upper_blocks", "vectors"]
     assert sec["base_blocks"].shape == (400, layout.block_stride(16, meta["code_subspaces"]))
     out = tmp_path / "copy.fannidx"
     serialize.write_sections(out, meta, sec)
-    assert out.read_bytes() == GOLD.read_bytes()
+    assert out.read_bytes() == path.read_bytes()
 
 
 def test_rejects_bad_files(tmp_path):
@@ -76,3 +78,33 @@ def test_device_round_trip(cuda, tmp_path):
     oid, od, _ = hq.search(p["vecs"], p["cent"], p["dims"], p["offs"], p["dist_min"],
                            p["delta"], g.entry_point, g.max_layer, q, prov.query_aux(q), 16, 5, 0)
     assert np.array_equal(ids, oid) and np.array_equal(ds_, od)
+
+
+@pytest.mark.gpu
+def test_exact_device_round_trip(cuda, tmp_path):
+    """An exact-strategy file written by the reference: load on the device,
+    write back identical sections, search like the oracle's exact searcher."""
+    meta, sec = serialize.read_sections(GOLD_EXACT)
+    g, prov, ds = serialize.load_index(GOLD_EXACT)
+    out = tmp_path / "rt.fannidx"
+    g.invalidate()
+    serialize.save_index(out, g, prov, ds)
+    meta2, sec2 = serialize.read_sections(out)
+    assert meta2 == meta and list(sec2) == list(sec)
+    for name in sec:
+        if name in ("base_blocks", "upper_blocks"):
+            cap = 2 * meta["R"] if name == "base_blocks" else meta["R"]
+            for r in range(sec[name].shape[0]):
+                assert np.array_equal(layout.row_ids(sec[name], r, cap),
+                                      layout.row_ids(sec2[name], r, cap)), (name, r)
+        else:
+            assert np.array_equal(sec2[name], sec[name]), name
+    from paper_2502_18113_b200 import evaluation
+
+    q = np.random.default_rng(5).normal(size=(20, 16)).astype(np.float32)
+    ids, d, _ = evaluation.search_batch(g, prov, q, evaluation.SearchParams(ef=16, k=5))
+    hq = native.HostGraph.from_blocks(sec["levels"], sec["upper_offsets"], sec["base_blocks"],
+                                      sec["upper_blocks"], meta["R"], None, kind=0,
+                                      vecs=sec["vectors"])
+    oi, od, _ = hq.search_exact(g.entry_point, g.max_layer, q, 16, 5)
+    assert np.array_equal(ids, oi) and np.array_equal(d, od)
