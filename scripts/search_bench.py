@@ -1,0 +1,78 @@
+#!/usr/bin/env python
+"""Query search: GPU search_batch vs the reference's
+compiled search_batch on the same built graph and queries.
+
+    python scripts/search_bench.py [--config 2] [--n N] [--threads 16]
+
+The graph is built on the GPU, exported to the reference layout, and searched
+by both cores (Flash kind, ef 64, k 10, with and without rerank 64): QPS and
+recall@10 against brute force.  The GPU leg runs on device-resident queries
+(evaluation.search_batch_dev) and through the host drop-in
+(sm100.search_batch, numpy in/out, including the block upload).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from oracle import refpkg  # noqa: E402
+from paper_2502_18113_b200 import (builder, dataset, evaluation, flash, graph,  # noqa: E402
+                                   sm100)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--threads", type=int, default=16)
+    args = ap.parse_args()
+    import torch
+
+    c = dataset.CONFIGS[args.config]
+    n = args.n or c["n"]
+    data, queries = dataset.baseline_config(args.config, n=n, nq=c["nq"])
+    gt = dataset.brute_force_knn(data, queries, 10)
+    res = builder.build(data, "flash", graph.BuildParams(C=c["efC"], R=c["M"], seed=0),
+                        builder.StrategyParams(m_f=c["m_f"], d_f=c["d_f"], kmeans_iters=10))
+    g, prov = res.graph, res.provider
+    pv = prov.core_arrays()
+    qaux = prov.query_aux(queries)
+    base, upper = g.base_blocks, g.upper_blocks
+    out = {"config": args.config, "n": n, "queries": len(queries), "ef": 64, "k": 10}
+    q_dev = torch.from_numpy(queries).cuda()
+    core = refpkg.load_ref_core()
+    for tag, rr in (("flash", 0), ("rerank64", 64)):
+        sp = evaluation.SearchParams(ef=64, k=10, rerank_depth=rr)
+        evaluation.search_batch_dev(g, prov, q_dev, sp)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ids, _, _ = evaluation.search_batch_dev(g, prov, q_dev, sp)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        r = {"gpu_qps": len(queries) / dt, "gpu_recall@10": evaluation.recall_at_k(
+            ids.cpu().numpy(), gt)}
+        t0 = time.perf_counter()
+        sm100.search_batch(4, pv, g.levels, base, g.upper_offsets, upper, c["efC"], c["M"],
+                           g.entry_point, g.max_layer, queries, qaux, 64, 10, rr)
+        r["gpu_host_api_qps"] = len(queries) / (time.perf_counter() - t0)
+        if core is not None:
+            t0 = time.perf_counter()
+            rids, _, _ = core.search_batch(4, pv, g.levels, base, g.upper_offsets, upper,
+                                           c["efC"], c["M"], g.entry_point, g.max_layer, queries,
+                                           qaux, 64, 10, rr, threads=args.threads,
+                                           kernel=len(core.available_kernels()) - 1)
+            r["reference_qps"] = len(queries) / (time.perf_counter() - t0)
+            r["reference_recall@10"] = evaluation.recall_at_k(rids, gt)
+        out[tag] = r
+    out["reference_threads"] = args.threads
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
