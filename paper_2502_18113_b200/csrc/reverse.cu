@@ -126,6 +126,13 @@ __global__ void __maxnreg__(96) reverse_kernel(
             if (cons) rowd_s[j] = distp[j];
         }
         const uint8_t *cy = g.codes + (size_t)y * g.mpad;
+        // y's code bytes of this lane's subspaces (lane + 32 k), packed
+        uint32_t cyl = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = lane + 32 * k;
+            if (i < g.m) cyl |= (uint32_t)__ldg(cy + i) << (8 * k);
+        }
         bool dirty = false;
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
@@ -143,7 +150,21 @@ __global__ void __maxnreg__(96) reverse_kernel(
             }
             ++n_prune;
             const uint8_t *cx = g.codes + (size_t)x * g.mpad;
-            const uint32_t dx = sdt_sum_warp(sdt, g.m, cy, cx, lane);
+            // Tdom[i][c] = sdt[i][c][x_i]: d(L_j, x) = sum_i Tdom[i][L_j,i] and
+            // d(y, x) = sum_i Tdom[i][y_i]
+            build_row_table(sdtT, g.m, g.mpad, cx, tdom, lane);
+            __syncwarp();
+            uint32_t dx;
+            {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = lane + 32 * k;
+                    if (i < g.m) acc += tdom[(i << 4) + ((cyl >> (8 * k)) & 0xffu)];
+                }
+                acc = __reduce_add_sync(0xffffffffu, acc);
+                dx = acc > 255u ? 255u : acc;
+            }
             const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
             int nk = 0;
             if (cons) {
@@ -164,11 +185,6 @@ __global__ void __maxnreg__(96) reverse_kernel(
                 // domination of x, one 32-member chunk at a time: the first
                 // dominating member settles it
                 bool xkept = true;
-                if (p > 0) {
-                    // Tdom[i][c] = sdt[i][c][x_i]: d(L_j, x) = sum_i Tdom[i][L_j,i]
-                    build_row_table(sdtT, g.m, g.mpad, cx, tdom, lane);
-                    __syncwarp();
-                }
 #pragma unroll
                 for (int c = 0; c < kRowChunks; ++c) {
                     if (c * 32 >= p) break;
