@@ -41,16 +41,6 @@ __device__ __forceinline__ uint32_t sdt_sum16(const uint8_t *tab, int m,
     return acc > 255u ? 255u : acc;
 }
 
-// The same sum for one pair, split across the warp (same value in every lane).
-__device__ __forceinline__ uint32_t sdt_sum_warp(const uint8_t *tab, int m,
-                                                 const uint8_t *__restrict__ p,
-                                                 const uint8_t *__restrict__ q, int lane) {
-    uint32_t acc = 0;
-    for (int i = lane; i < m; i += 32) acc += tab[(i << 8) + (__ldg(p + i) << 4) + __ldg(q + i)];
-    acc = __reduce_add_sync(0xffffffffu, acc);
-    return acc > 255u ? 255u : acc;
-}
-
 // Segment heads of the sorted request keys (first key of every row).
 __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys, int64_t N,
                                      int64_t *__restrict__ heads, int *__restrict__ nheads,
