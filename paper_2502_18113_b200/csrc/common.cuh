@@ -43,7 +43,21 @@ void set_error(const char *fmt, ...);
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 constexpr int kWarp = 32;
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // B200; grids use num_sms() (the device's own count)
+
+// SM count of the current device (cached per process; B200: 148)
+inline int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+            n = v;
+        else
+            n = kNumSMs;
+    }
+    return n;
+}
 
 __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
 __host__ __device__ inline int64_t round_up64(int64_t x, int64_t a) { return (x + a - 1) / a * a; }

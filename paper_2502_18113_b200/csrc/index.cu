@@ -436,11 +436,11 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     int rev_per_sm = 0;
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, rev_fn,
                                                           kReverseWarps * 32, smem_rev));
-    const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * kNumSMs;
+    const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * num_sms();
     int search_per_sm = 0;
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, search_fn,
                                                           kSearchWarps * 32, smem_search));
-    const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * kNumSMs;
+    const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * num_sms();
     // carve out only the shared memory the resident CTAs use: the rest stays
     // L1, which holds the transposed SDT and the hot code rows
     {
