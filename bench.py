@@ -130,15 +130,15 @@ def ref_cpu_build(prov_full, levels_fn, n_sub, C, R, threads):
 
 
 def size_cpu_sample(build, n_max, target_s, n0=20_000):
-    """Grow a prefix by doubling until one reference build takes about
-    target_s / 3 (the CPU rate falls steeply with n once the graph leaves the
+    """Grow a prefix by doubling until one reference build takes at least
+    target_s / 2 (the CPU rate falls steeply with n once the graph leaves the
     caches, so a small calibration cannot be extrapolated).  Returns
     (n, seconds, vec/s) of the last build, or None."""
     n = min(n_max, n0)
     r = build(n)
     if r is None:
         return None
-    while r[0] < target_s / 3.0 and n < n_max:
+    while r[0] < target_s / 2.0 and n < n_max:
         n = min(n_max, 2 * n)
         r = build(n)
     return n, r[0], r[1]
