@@ -20,6 +20,26 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
+def device_config5(n, seed=0, chunk=1 << 19):
+    """Config 5's law (rank-64 signal + isotropic noise at power SNR 3, unit
+    norm, bf16-rounded) generated on the device in chunks: 5M x 768 would need
+    ~100 GB of float64 host temporaries through dataset.baseline_config."""
+    import torch
+
+    d = 768
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    basis = torch.randn(64, d, device="cuda", generator=g, dtype=torch.float64) / d ** 0.5
+    out = torch.empty((n, d), device="cuda", dtype=torch.float32)
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        sig = torch.randn(hi - lo, 64, device="cuda", generator=g, dtype=torch.float64) @ basis
+        noise = torch.randn(hi - lo, d, device="cuda", generator=g, dtype=torch.float64)
+        x = sig + noise * torch.sqrt((sig * sig).mean() / 3.0)
+        x /= torch.linalg.norm(x, dim=1, keepdim=True)
+        out[lo:hi] = x.to(torch.bfloat16).to(torch.float32)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="+", default=[3, 4, 5])
@@ -34,9 +54,13 @@ def main():
         c = dataset.CONFIGS[cfg]
         n = args.n or c["n"]
         t0 = time.perf_counter()
-        data, _ = dataset.baseline_config(cfg, n=n, nq=0)
+        if cfg == 5 and n > 1_000_000:
+            data = x_dev = device_config5(n)
+        else:
+            data, _ = dataset.baseline_config(cfg, n=n, nq=0)
+            x_dev = torch.from_numpy(data).cuda()
+        torch.cuda.synchronize()
         gen_s = time.perf_counter() - t0
-        x_dev = torch.from_numpy(data).cuda()
         sample = builder.training_sample(data, builder.DEFAULT_SAMPLE, 0)
         t0 = time.perf_counter()
         model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=10)
