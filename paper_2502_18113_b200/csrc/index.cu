@@ -411,13 +411,18 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // ---- scratch ----
     const int capmax = std::max(g.cap0, g.capU);
     if (exact) gb.expand = 1;
+    // Visited table: 2^12 16-bit slots (8 KB) unless requested — a larger one
+    // costs occupancy (the ids it cannot hold go to the global tier).  The
+    // forward selection's workspace always lives in the dead table; the
+    // sorted results join it when both fit, else they take their own space.
+    const size_t sel_bytes = exact ? (size_t)2 * round_up(R, 4) * 4 + (size_t)g.dim * 4
+                                   : (size_t)select_tv_bytes(g.m, g.mpad, R);
+    int hl = opts->hash_log2 > 0 ? std::max(opts->hash_log2, 9) : 12;
+    while (((size_t)16 << vis_buckets_log2(hl)) < sel_bytes) ++hl;
+    const bool t_alias =
+        sel_bytes + (size_t)round_up(C, 32) * 8 <= ((size_t)16 << vis_buckets_log2(hl));
     WarpLayout L;
-    L.init(g.mpad, C, capmax,
-           pick_hash_log2(C, cand_capacity(gb.expand, capmax), R, g.mpad, opts->hash_log2,
-                          (size_t)round_up(C, 32) * 8 +
-                              (exact ? (size_t)2 * round_up(R, 4) * 4 + (size_t)g.dim * 4
-                                     : select_tv_bytes(g.m, g.mpad, R))),
-           gb.expand, true, exact ? g.dim * 4 : -1, exact ? 8 : 4);
+    L.init(g.mpad, C, capmax, hl, gb.expand, t_alias, exact ? g.dim * 4 : -1, exact ? 8 : 4);
     const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
     const size_t smem_search = (size_t)kSearchWarps * L.total;
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
