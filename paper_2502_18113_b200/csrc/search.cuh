@@ -1218,8 +1218,15 @@ __device__ int warp_select_exact(const Graph &g, int ncand, int cap, Get get, in
             const float *b = g.vecs + (size_t)v * g.dim;
             for (int i = lane; i < g.dim; i += 32) cv[i] = __ldg(b + i);
             __syncwarp();
-            ExactDist::dists(g, reinterpret_cast<const uint8_t *>(cv), kept, nk, kd, lane);
-            for (int t = lane; t < nk; t += 32) bad |= kd[t] < dv;
+            // four kept vectors per pass; the first dominating one settles it
+            for (int base = 0; base < nk; base += 4) {
+                const int t = base + (lane >> 3);
+                const float *a = t < nk ? g.vecs + (size_t)kept[t] * g.dim : nullptr;
+                const float d = warp_l2_group8(t < nk ? cv : nullptr, a, g.dim, lane);
+                if ((lane & 7) == 0 && t < nk && __float_as_uint(d) < dv) bad = true;
+                if (__any_sync(0xffffffffu, bad)) break;
+            }
+            __syncwarp();
         }
         sym += nk;
         if (!__any_sync(0xffffffffu, bad)) {
