@@ -223,8 +223,10 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     if ((rc = dev_alloc((void **)&ix->adjU, sizeof(int32_t) * g.nU * g.capUp))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->cntU, sizeof(int32_t) * g.nU))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->consU, g.nU))) return fail(rc);
-    if ((rc = dev_alloc((void **)&ix->dist0, (size_t)g.n * g.cap0p))) return fail(rc);
-    if ((rc = dev_alloc((void **)&ix->distU, (size_t)g.nU * g.capUp))) return fail(rc);
+    // prune-distance caches: u8 per slot (Flash), fp32 bits per slot (exact)
+    const size_t dbytes = desc->m == 0 ? 4 : 1;
+    if ((rc = dev_alloc((void **)&ix->dist0, (size_t)g.n * g.cap0p * dbytes))) return fail(rc);
+    if ((rc = dev_alloc((void **)&ix->distU, (size_t)g.nU * g.capUp * dbytes))) return fail(rc);
     if ((rc = dev_alloc((void **)&ix->upper_owner, sizeof(int32_t) * g.nU))) return fail(rc);
     g.codes = ix->codes;
     g.adj0 = ix->adj0; g.cnt0 = ix->cnt0; g.cons0 = ix->cons0;

@@ -80,6 +80,7 @@ LayerSearchFn layer_search_variant(int W, bool exact);
 struct ReverseLayout {
     int tdom, tkeep, row, rowd, keptd, cand, sel, total;
     int qv, cv, cid, cd, kd;  // exact kind: y's and a candidate's vectors, ids, distances
+    int rowd32, keptd32, kflag;  // exact kind: the row's cached fp32 distances, survivors
     __host__ __device__ void init(int capmax, int m, int mpad, int dim = 0) {
         int o = 0;
         tdom = o; o += round_up(mpad * 16, 256);   // x's row tables (256-aligned)
@@ -90,13 +91,16 @@ struct ReverseLayout {
         cand = o; o += 128 * 8;
         o = round_up(o, 256);
         sel = o; o += select_tv_bytes(m, mpad, capmax);  // kept ids first
-        qv = cv = cid = cd = kd = 0;
+        qv = cv = cid = cd = kd = rowd32 = keptd32 = kflag = 0;
         if (dim > 0) {
             qv = o; o += round_up(dim * 4, 16);
             cv = o; o += round_up(dim * 4, 16);
             cid = o; o += round_up(capmax + 1, 32) * 4;
             cd = o; o += round_up(capmax + 1, 32) * 4;
             kd = o; o += round_up(capmax, 32) * 4;
+            rowd32 = o; o += round_up(capmax, 32) * 4;
+            keptd32 = o; o += round_up(capmax, 32) * 4;
+            kflag = o; o += round_up(capmax, 32);
         }
         total = round_up(o, 256);
     }

@@ -294,10 +294,14 @@ __global__ void __maxnreg__(96) reverse_kernel(
     }
 }
 
-// Exact kind (kind 0): the same row segments; every prune is the reference's
-// full rule (reverse_add, _core.pyx:441-477) with fp32 L2 distances — d(y, u)
-// for the row and x (8-lane groups against y's vector staged in shared
-// memory), (d, id) sort, select_heur.
+// Exact kind (kind 0): the same row segments and the same two prune paths as
+// reverse_kernel, with fp32 L2 distances (symmetric: d(a, b) = d(b, a) bit
+// for bit) computed four pairs at a time by 8-lane groups.  Fast path (the row
+// is a prune output, its owner distances cached as fp32 bits): d(y, x), then
+// d(L_j, x) for the members closer than x until one dominates, then the keep
+// test of the rest.  Full path (rows written by appends / forward writes):
+// d(y, u) for the row and x, (d, id) sort, select_heur (reverse_add,
+// _core.pyx:441-477).
 __global__ void __maxnreg__(96) reverse_exact_kernel(
     Graph g, const unsigned long long *__restrict__ keys, int64_t N,
     const int64_t *__restrict__ heads, const int *__restrict__ nheads, int *__restrict__ next,
@@ -314,8 +318,11 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
     int32_t *cid = reinterpret_cast<int32_t *>(base + L.cid);
     uint32_t *cd = reinterpret_cast<uint32_t *>(base + L.cd);
     uint32_t *kd = reinterpret_cast<uint32_t *>(base + L.kd);
+    uint32_t *rowd = reinterpret_cast<uint32_t *>(base + L.rowd32);
+    uint32_t *keptd = reinterpret_cast<uint32_t *>(base + L.keptd32);
+    uint8_t *kflag = base + L.kflag;
     const int nseg = *nheads;
-    unsigned long long n_prune = 0, n_app = 0, n_sym = 0;
+    unsigned long long n_prune = 0, n_app = 0, n_sym = 0, n_full = 0;
     while (true) {
         int s = 0;
         if (lane == 0) s = atomicAdd(next, 1);
@@ -336,70 +343,156 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         const int cap = l0 ? g.cap0 : g.capU;
         int32_t *ids = l0 ? g.adj0 + rowg * g.cap0p : g.adjU + (rowg - g.n) * g.capUp;
         int32_t *cntp = l0 ? g.cnt0 + rowg : g.cntU + (rowg - g.n);
+        uint8_t *consp = l0 ? g.cons0 + rowg : g.consU + (rowg - g.n);
+        uint32_t *distp = reinterpret_cast<uint32_t *>(l0 ? g.dist0 : g.distU) +
+                          (l0 ? rowg * g.cap0p : (rowg - g.n) * g.capUp);
         int cnt = *cntp;
-        for (int j = lane; j < cap; j += 32) row_s[j] = ids[j];
-        bool have_y = false;
+        int cons = *consp;
+        for (int j = lane; j < cap; j += 32) {
+            row_s[j] = ids[j];
+            if (cons) rowd[j] = distp[j];
+        }
+        const float *vy = g.vecs + (size_t)y * g.dim;
+        bool have_y = false, dirty = false;
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
             const int x = (int)(keys[t] & 0xffffffffu);
             if (cnt < cap) {
                 if (lane == 0) row_s[cnt] = x;
                 ++cnt;
+                cons = 0;
+                dirty = true;
                 ++n_app;
                 __syncwarp();
                 continue;
             }
             ++n_prune;
-            if (!have_y) {
-                for (int i = lane; i < g.dim; i += 32) qv[i] = __ldg(g.vecs + (size_t)y * g.dim + i);
-                have_y = true;
-            }
-            for (int j = lane; j <= cap; j += 32) cid[j] = j < cap ? row_s[j] : x;
-            __syncwarp();
-            ExactDist::dists(g, reinterpret_cast<const uint8_t *>(qv), cid, cap + 1, cd, lane);
-            for (int j = lane; j <= cap; j += 32)
-                cand[j] = ((unsigned long long)cd[j] << 32) | (uint32_t)cid[j];
-            __syncwarp();
-            unsigned long long mine[kRowChunks + 1];
-            int rk[kRowChunks + 1];
-#pragma unroll
-            for (int c = 0; c <= kRowChunks; ++c) {
-                const int j = c * 32 + lane;
-                rk[c] = -1;
-                if (j <= cap) {
-                    mine[c] = cand[j];
-                    rk[c] = count_less(cand, cap + 1, mine[c]);
+            int nk = 0;
+            if (cons) {
+                // x's vector staged; d(y, x) from lane group 0
+                for (int i = lane; i < g.dim; i += 32) cv[i] = __ldg(g.vecs + (size_t)x * g.dim + i);
+                __syncwarp();
+                const uint32_t dx = __shfl_sync(
+                    0xffffffffu,
+                    __float_as_uint(warp_l2_group8(lane < 8 ? cv : nullptr,
+                                                   lane < 8 ? vy : nullptr, g.dim, lane)),
+                    0);
+                const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
+                int p = 0;
+                for (int j = lane; j < cap; j += 32) {
+                    const unsigned long long kj =
+                        ((unsigned long long)rowd[j] << 32) | (uint32_t)row_s[j];
+                    p += __popc(__ballot_sync(__activemask(), kj < kx));
                 }
+                p = __reduce_max_sync(0xffffffffu, p);  // lanes beyond cap saw no chunk
+                n_sym += cap + 1 + p;
+                // domination of x by a closer member, four at a time
+                bool xkept = true;
+                for (int b0 = 0; b0 < p; b0 += 4) {
+                    const int j = b0 + (lane >> 3);
+                    const float *a = j < p ? g.vecs + (size_t)row_s[j] * g.dim : nullptr;
+                    const float d = warp_l2_group8(j < p ? cv : nullptr, a, g.dim, lane);
+                    const bool dom = (lane & 7) == 0 && j < p && __float_as_uint(d) < dx;
+                    if (__any_sync(0xffffffffu, dom)) {
+                        xkept = false;
+                        break;
+                    }
+                }
+                if (!xkept) continue;  // the row is unchanged (and still consistent)
+                n_sym += cap - p;
+                // the farther members stay unless x dominates them
+                for (int b0 = p; b0 < cap; b0 += 4) {
+                    const int j = b0 + (lane >> 3);
+                    const float *a = j < cap ? g.vecs + (size_t)row_s[j] * g.dim : nullptr;
+                    const float d = warp_l2_group8(j < cap ? cv : nullptr, a, g.dim, lane);
+                    if ((lane & 7) == 0 && j < cap) kflag[j] = __float_as_uint(d) >= rowd[j];
+                }
+                __syncwarp();
+                // survivors in candidate order: L_0..L_{p-1}, x, L_p..
+                for (int c0 = 0; c0 < cap; c0 += 32) {
+                    const int j = c0 + lane;
+                    const bool keep = j < cap && (j < p || kflag[j]);
+                    const unsigned bk = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        int pos = nk + __popc(bk & ((1u << lane) - 1u)) + (j >= p ? 1 : 0);
+                        if (pos < cap) {
+                            kept[pos] = row_s[j];
+                            keptd[pos] = rowd[j];
+                        }
+                    }
+                    nk += __popc(bk);
+                }
+                if (lane == 0 && p < cap) {
+                    kept[p] = x;
+                    keptd[p] = dx;
+                }
+                nk = min(nk + 1, cap);
+            } else {
+                ++n_full;
+                if (!have_y) {
+                    for (int i = lane; i < g.dim; i += 32) qv[i] = __ldg(vy + i);
+                    have_y = true;
+                }
+                for (int j = lane; j <= cap; j += 32) cid[j] = j < cap ? row_s[j] : x;
+                __syncwarp();
+                ExactDist::dists(g, reinterpret_cast<const uint8_t *>(qv), cid, cap + 1, cd, lane);
+                for (int j = lane; j <= cap; j += 32)
+                    cand[j] = ((unsigned long long)cd[j] << 32) | (uint32_t)cid[j];
+                __syncwarp();
+                unsigned long long mine[kRowChunks + 1];
+                int rk[kRowChunks + 1];
+#pragma unroll
+                for (int c = 0; c <= kRowChunks; ++c) {
+                    const int j = c * 32 + lane;
+                    rk[c] = -1;
+                    if (j <= cap) {
+                        mine[c] = cand[j];
+                        rk[c] = count_less(cand, cap + 1, mine[c]);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c <= kRowChunks; ++c)
+                    if (rk[c] >= 0) cand[rk[c]] = mine[c];
+                __syncwarp();
+                unsigned long long sym = 0;
+                nk = warp_select_exact(
+                    g, cap + 1, cap,
+                    [&](int j, int &v, uint32_t &dv) {
+                        const unsigned long long k = cand[j];
+                        v = (int)(k & 0xffffffffu);
+                        dv = (uint32_t)(k >> 32);
+                    },
+                    kept, cv, kd, lane, &sym, keptd);
+                n_sym += cap + 1 + sym;
             }
             __syncwarp();
-#pragma unroll
-            for (int c = 0; c <= kRowChunks; ++c)
-                if (rk[c] >= 0) cand[rk[c]] = mine[c];
-            __syncwarp();
-            unsigned long long sym = 0;
-            const int nk = warp_select_exact(
-                g, cap + 1, cap,
-                [&](int j, int &v, uint32_t &dv) {
-                    const unsigned long long k = cand[j];
-                    v = (int)(k & 0xffffffffu);
-                    dv = (uint32_t)(k >> 32);
-                },
-                kept, cv, kd, lane, &sym);
-            n_sym += cap + 1 + sym;
-            __syncwarp();
-            for (int j = lane; j < cap; j += 32) row_s[j] = j < nk ? kept[j] : -1;
+            for (int j = lane; j < cap; j += 32) {
+                row_s[j] = j < nk ? kept[j] : -1;
+                rowd[j] = j < nk ? keptd[j] : 0u;
+            }
             cnt = nk;
+            cons = 1;
+            dirty = true;
             __syncwarp();
         }
-        for (int j = lane; j < cap; j += 32) ids[j] = j < cnt ? row_s[j] : -1;
-        if (lane == 0) *cntp = cnt;
+        if (dirty) {
+            for (int j = lane; j < cap; j += 32) {
+                ids[j] = j < cnt ? row_s[j] : -1;
+                if (cons) distp[j] = rowd[j];
+            }
+            if (lane == 0) {
+                *cntp = cnt;
+                *consp = (uint8_t)cons;
+            }
+        }
         __syncwarp();
     }
     if (lane == 0 && (n_prune | n_app)) {
         atomicAdd(ctr + 1, n_sym);
         atomicAdd(ctr + 4, n_prune);
         atomicAdd(ctr + 5, n_app);
-        atomicAdd(ctr + 6, n_prune);
+        atomicAdd(ctr + 6, n_full);
     }
 }
 

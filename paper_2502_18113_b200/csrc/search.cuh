@@ -1206,7 +1206,7 @@ __host__ __device__ inline int set_variant(int W) {
 template <class Get>
 __device__ int warp_select_exact(const Graph &g, int ncand, int cap, Get get, int32_t *kept,
                                  float *cv, uint32_t *kd, int lane,
-                                 unsigned long long *sym_count) {
+                                 unsigned long long *sym_count, uint32_t *kept_d = nullptr) {
     int nk = 0;
     unsigned long long sym = 0;
     for (int j = 0; j < ncand && nk < cap; ++j) {
@@ -1230,7 +1230,10 @@ __device__ int warp_select_exact(const Graph &g, int ncand, int cap, Get get, in
         }
         sym += nk;
         if (!__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) kept[nk] = v;
+            if (lane == 0) {
+                kept[nk] = v;
+                if (kept_d) kept_d[nk] = dv;
+            }
             ++nk;
         }
         __syncwarp();
