@@ -340,85 +340,12 @@ struct TieOrder {
     }
 };
 
-// number of entries of sorted a[0..n) strictly less than x
-__device__ __forceinline__ int lower_rank(const unsigned long long *a, int n, unsigned long long x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// Warp-cooperative rank (entries of a[0..n) below x, same result in every
-// lane): independent loads + ballots instead of a chain of dependent loads.
-__device__ __forceinline__ int warp_rank(const unsigned long long *a, int n, unsigned long long x,
-                                         int lane) {
-    int r = 0;
-#pragma unroll 4
-    for (int c = 0; c < n; c += 32) {
-        const int i = c + lane;
-        r += __popc(__ballot_sync(0xffffffffu, i < n && a[i] < x));
-    }
-    return r;
-}
-
 // number of entries of the unsorted (small) a[0..n) strictly less than x;
 // every lane reads the same word: shared-memory broadcast
 __device__ __forceinline__ int count_less(const unsigned long long *a, int n, unsigned long long x) {
     int c = 0;
     for (int j = 0; j < n; ++j) c += a[j] < x;
     return c;
-}
-
-// Merge the sorted keys S[0..ns) into the sorted T[0..ts) (ts + ns <= capacity)
-// in place: T's entries only move right, so 32-entry chunks are processed from
-// the top; the new keys land last.  Returns the lowest position written.
-__device__ __forceinline__ int merge_sorted_into(unsigned long long *T, int &ts,
-                                                 const unsigned long long *S, int ns, int lane) {
-    if (ns == 0) return ts;
-    int spos[4];  // final slots of S[lane + 32c] (ns <= 128), from the original T
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int j = lane + 32 * c;
-        spos[c] = j < ns ? j + lower_rank(T, ts, S[j]) : -1;
-    }
-    const int p0 = __shfl_sync(0xffffffffu, spos[0], 0);  // S[0] is the smallest
-    if (ts > p0) {
-        for (int base = p0 + ((ts - 1 - p0) & ~31); base >= p0; base -= 32) {
-            const int i = base + lane;
-            unsigned long long t = 0;
-            int np = -1;
-            if (i < ts) {
-                t = T[i];
-                np = i + count_less(S, ns, t);
-            }
-            __syncwarp();
-            if (np >= 0) T[np] = t;
-            __syncwarp();
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-        if (spos[c] >= 0) T[spos[c]] = S[lane + 32 * c];
-    __syncwarp();
-    ts += ns;
-    return p0;
-}
-
-// Move T[lo..hi) one slot right (T[hi] is overwritten), highest 32-entry chunk
-// first, so no entry is overwritten before it is read.
-__device__ __forceinline__ void shift_right1(unsigned long long *T, int lo, int hi, int lane) {
-    if (hi <= lo) return;
-    for (int base = lo + ((hi - 1 - lo) & ~31); base >= lo; base -= 32) {
-        const int i = base + lane;
-        unsigned long long t = 0;
-        if (i < hi) t = T[i];
-        __syncwarp();
-        if (i < hi) T[i + 1] = t;
-        __syncwarp();
-    }
 }
 
 // Per-search counters (32-bit: one search never reaches 2^32 of anything);
@@ -449,18 +376,6 @@ __device__ __forceinline__ void phase_mark(SearchCounters &, int, long long &) {
 // On return T[0..ts) holds the result ascending by (d, id).
 // Returns false on visited-hash overflow.
 constexpr int kRowChunks = 4;  // id rows up to 128 slots (cap = 2R <= 127)
-
-// First unexpanded member of T at or after `from` (-1 if none).
-__device__ __forceinline__ int next_unexpanded(const unsigned long long *T, int ts, int from,
-                                               int lane) {
-    for (int c = from; c < ts; c += 32) {
-        int idx = c + lane;
-        bool f = idx < ts && ((T[idx] & 1ull) == 0ull);
-        unsigned b = __ballot_sync(0xffffffffu, f);
-        if (b) return c + __ffs(b) - 1;
-    }
-    return -1;
-}
 
 __device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane,
                                          int (&u)[kRowChunks]) {
