@@ -265,8 +265,8 @@ struct VisitedSet {
         const uint32_t r = (h & ((1u << (24 - kb)) - 1u)) + 1u;
         uint4 *bk = B + (h >> (24 - kb));
         const uint32_t rr = r | (r << 16);
+        uint4 v = *bk;  // the common case (a visited id) needs this one read
         while (true) {
-            const uint4 v = lds128_volatile(bk);
             if ((__vcmpeq2(v.x, rr) | __vcmpeq2(v.y, rr) | __vcmpeq2(v.z, rr) |
                  __vcmpeq2(v.w, rr)) != 0u)
                 return 0;
@@ -280,6 +280,7 @@ struct VisitedSet {
             const uint32_t nw = ow | (r << (16 * (e & 1)));
             if (atomicCAS(reinterpret_cast<uint32_t *>(bk) + wi, ow, nw) == ow) return 1;
             // another lane took the slot: re-read the bucket
+            v = lds128_volatile(bk);
         }
         if (G == nullptr) return 3;
         const uint32_t key = (uint32_t)id + 1u;
