@@ -367,10 +367,16 @@ def main():
     kernel_ms = {"encode": prof["ms_encode"], "search": prof["ms_search"],
                  "sort": prof["ms_sort"], "reverse": prof["ms_reverse"]}
     cap0, mpad = 2 * c["M"], (c["m_f"] + 15) // 16 * 16
-    # algorithmic bytes of the search kernel: one id row per expansion + the
-    # code row of every evaluated vertex
-    search_bytes = prof["visited"] * cap0 * 4 + prof["dist_comps"] * c["m_f"]
+    # algorithmic bytes per SURVEY §8(d): one unit = one 16-lane batch
+    # evaluation of a neighbour block = 16 (m + 4) B, plus 4 B of count per
+    # block; units = 16 x the reference's kernel_calls counter (the build
+    # counts it exactly as the reference does, ceil(live / 16) per expansion)
+    evals = 16 * prof["kernel_calls"]
+    search_bytes = evals * (c["m_f"] + 4) + prof["visited"] * 4
     search_gbs = search_bytes / (prof["ms_search"] * 1e-3) / 1e9
+    # what this kernel actually has to read: an id row per expansion and the
+    # code row of each fresh (unvisited) neighbour only
+    touched = prof["visited"] * cap0 * 4 + prof["dist_comps"] * c["m_f"]
     # DRAM bytes per build at the captured launch's bytes per inserted vector
     tr = load_traffic().get("build_search_kernel")
     search_traffic = int(tr["dram_bytes"] / tr["vectors"] * n) if tr else None
@@ -378,6 +384,10 @@ def main():
                 "achieved": search_gbs, "peak": peak, "unit": "GB/s",
                 "frac": search_gbs / peak, "traffic": search_traffic, "peak_kind": peak_kind,
                 "bytes_per_build": search_bytes,
+                "evals_per_s": evals / (prof["ms_search"] * 1e-3),
+                "bytes_basis": "SURVEY 8(d): 16 x kernel_calls x (m + 4) B + 4 B per block",
+                "touched_bytes_per_build": touched,
+                "touched_frac": touched / (prof["ms_search"] * 1e-3) / 1e9 / peak,
                 "traffic_basis": "per build: ncu DRAM bytes per inserted vector of one captured "
                                  "launch x n (profiles/*_traffic.json)",
                 "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}
