@@ -10,7 +10,7 @@ namespace fa {
 // P = FlashDist: the per-insertion query tables come in adt_batch and forward
 // selection uses the SDT (sdtT); P = ExactDist: the query is the inserted
 // vertex's own vector and every distance is fp32 L2.
-template <typename P, int J, int EM>
+template <typename P, int J, int EM, int RC>
 __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         long long sel_cycles = 0;
         for (int layer = top; layer >= 0; --layer) {
             int ts = 0;
-            bool ok = layer_search<P, J, EM>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
+            bool ok = layer_search<P, J, EM, RC>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                                    ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
             if (!ok) {
                 if (lane == 0) atomicExch(err, 1);
@@ -131,34 +131,43 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     flush_counters(total, ctr, lane);
 }
 
-BuildSearchFn build_search_variant(int W, int expand) {
+// RC: id-row chunks compiled into the hot loop (2 when the base rows hold
+// <= 64 slots: the common R <= 32; else 4)
+#define FA_BUILD_J(P, EM, RC)                                 \
+    switch (v) {                                              \
+        case 2: return build_search_kernel<P, 2, EM, RC>;     \
+        case 4: return build_search_kernel<P, 4, EM, RC>;     \
+        case 7: return build_search_kernel<P, 7, EM, RC>;     \
+        case 8: return build_search_kernel<P, 8, EM, RC>;     \
+        case 10: return build_search_kernel<P, 10, EM, RC>;   \
+        case 16: return build_search_kernel<P, 16, EM, RC>;   \
+        default: break;                                       \
+    }
+
+BuildSearchFn build_search_variant(int W, int expand, int cap0) {
     const int v = set_variant(W);
     if (expand > 1) {
-        if (v == 0) return build_search_kernel<FlashDist, 0, 1>;
-        return v <= 8 ? build_search_kernel<FlashDist, 8, kMaxExpand>
-                      : build_search_kernel<FlashDist, 16, kMaxExpand>;
+        if (v == 0) return build_search_kernel<FlashDist, 0, 1, kRowChunks>;
+        return v <= 8 ? build_search_kernel<FlashDist, 8, kMaxExpand, kRowChunks>
+                      : build_search_kernel<FlashDist, 16, kMaxExpand, kRowChunks>;
     }
-    switch (v) {
-        case 2: return build_search_kernel<FlashDist, 2, 1>;
-        case 4: return build_search_kernel<FlashDist, 4, 1>;
-        case 7: return build_search_kernel<FlashDist, 7, 1>;
-        case 8: return build_search_kernel<FlashDist, 8, 1>;
-        case 10: return build_search_kernel<FlashDist, 10, 1>;
-        case 16: return build_search_kernel<FlashDist, 16, 1>;
-        default: return build_search_kernel<FlashDist, 0, 1>;
+    if (cap0 <= 64) {
+        FA_BUILD_J(FlashDist, 1, 2)
+    } else {
+        FA_BUILD_J(FlashDist, 1, kRowChunks)
     }
+    return build_search_kernel<FlashDist, 0, 1, kRowChunks>;
 }
 
-BuildSearchFn build_search_exact_variant(int W) {
-    switch (set_variant(W)) {
-        case 2: return build_search_kernel<ExactDist, 2, 1>;
-        case 4: return build_search_kernel<ExactDist, 4, 1>;
-        case 7: return build_search_kernel<ExactDist, 7, 1>;
-        case 8: return build_search_kernel<ExactDist, 8, 1>;
-        case 10: return build_search_kernel<ExactDist, 10, 1>;
-        case 16: return build_search_kernel<ExactDist, 16, 1>;
-        default: return nullptr;  // W > kRegSetMax: not served for the exact kind
+BuildSearchFn build_search_exact_variant(int W, int cap0) {
+    const int v = set_variant(W);
+    if (cap0 <= 64) {
+        FA_BUILD_J(ExactDist, 1, 2)
+    } else {
+        FA_BUILD_J(ExactDist, 1, kRowChunks)
     }
+    return nullptr;  // W > kRegSetMax: not served for the exact kind
 }
+#undef FA_BUILD_J
 
 }  // namespace fa

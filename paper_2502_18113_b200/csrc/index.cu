@@ -430,7 +430,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
                  smem_search);
     const BuildSearchFn search_fn =
-        exact ? build_search_exact_variant(C) : build_search_variant(C, gb.expand);
+        exact ? build_search_exact_variant(C, g.cap0) : build_search_variant(C, gb.expand, g.cap0);
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;

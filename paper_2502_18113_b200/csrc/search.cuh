@@ -378,10 +378,10 @@ __device__ __forceinline__ void phase_mark(SearchCounters &, int, long long &) {
 // Returns false on visited-hash overflow.
 constexpr int kRowChunks = 4;  // id rows up to 128 slots (cap = 2R <= 127)
 
-__device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane,
-                                         int (&u)[kRowChunks]) {
+template <int RC = kRowChunks>
+__device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane, int (&u)[RC]) {
 #pragma unroll
-    for (int k = 0; k < kRowChunks; ++k) {
+    for (int k = 0; k < RC; ++k) {
         int j = k * 32 + lane;
         u[k] = j < cap ? __ldg(ids + j) : -1;
     }
@@ -666,7 +666,8 @@ __device__ __forceinline__ void warp_bitonic(K (&k)[J], int lane) {
     }
 }
 
-template <typename P, int J, int EM>
+// RC: id-row chunks of 32 slots compiled in (cap <= 32 RC)
+template <typename P, int J, int EM, int RC = kRowChunks>
 __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int entry,
                                                  uint32_t entry_d, int W, const uint8_t *qc,
                                                  unsigned long long *T, int &ts_out,
@@ -692,7 +693,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     uint32_t wd = 0xffffffffu;  // worst distance once the set is full
     int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
     int pre_v = -1;             // speculative id row of the most likely next pop (EM == 1)
-    int pre[kRowChunks];
+    int pre[RC];
     const int E = EM > 1 ? min(max(g.expand, 1), EM) : 1;
     long long tph = phase_clock();
     __syncwarp();
@@ -701,7 +702,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         // ---- pop up to E frontier minima: unexpanded set members vs tie queue
         int pv[EM];
         int npop = 0;
-        int u[EM][kRowChunks];
+        int u[EM][RC];
         if (EM == 1) {
             K b1, b2;
             int j1;
@@ -724,7 +725,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             }
             if (pv[0] == pre_v) {
 #pragma unroll
-                for (int k = 0; k < kRowChunks; ++k) u[0][k] = pre[k];
+                for (int k = 0; k < RC; ++k) u[0][k] = pre[k];
             } else {
                 load_row(row_ids(g, layer, pv[0]), cap, lane, u[0]);
             }
@@ -783,7 +784,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             if (r >= npop) break;
             int nlive = 0;
 #pragma unroll
-            for (int k = 0; k < kRowChunks; ++k) {
+            for (int k = 0; k < RC; ++k) {
                 if (k * 32 >= cap) break;
                 const int x = u[r][k];
                 const bool live = x >= 0;
@@ -1091,7 +1092,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
 // Best-first layer search with the result-set variant J chosen by the host
 // (set_variant): J slots per lane in registers, J = 0 the shared-memory set
 // (Flash only).  P: the distance policy (FlashDist / ExactDist).
-template <typename P, int J, int EM>
+template <typename P, int J, int EM, int RC = kRowChunks>
 __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
                                              int W, const uint8_t *qc, unsigned long long *T,
                                              int &ts, unsigned long long *S, int32_t *TQ,
@@ -1103,7 +1104,7 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
         return layer_search_smem(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
                                  hlog2, cnt, to, lane);
     } else {
-        return layer_search_reg<P, J, EM>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
+        return layer_search_reg<P, J, EM, RC>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
                                           fdist, H, hlog2, cnt, to, lane);
     }
 }
