@@ -214,6 +214,27 @@ __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
     return v;
 }
 
+// The global tier's probe (ids whose shared bucket is full: the cold path,
+// kept out of line so the hot loop stays compact).  0 = already visited,
+// 2 = inserted.
+static __device__ __noinline__ int global_visit(uint32_t *G, uint32_t epoch, int id) {
+    const uint32_t key = (uint32_t)id + 1u;
+    const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
+    const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
+    uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
+    while (true) {
+        const uint32_t v = G[p];
+        if (v == gk) return 0;
+        if ((v >> 24) != epoch) {
+            const uint32_t old = atomicCAS(G + p, v, gk);
+            if (old == v) return 2;
+            if (old == gk) return 0;
+            continue;
+        }
+        p = (p + 1u) & gmask;
+    }
+}
+
 struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
@@ -282,22 +303,7 @@ struct VisitedSet {
             // another lane took the slot: re-read the bucket
             v = lds128_volatile(bk);
         }
-        if (G == nullptr) return 3;
-        const uint32_t key = (uint32_t)id + 1u;
-        const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
-        const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
-        uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
-        while (true) {
-            uint32_t v = G[p];
-            if (v == gk) return 0;
-            if ((v >> 24) != epoch) {
-                uint32_t old = atomicCAS(G + p, v, gk);
-                if (old == v) return 2;
-                if (old == gk) return 0;
-                continue;
-            }
-            p = (p + 1u) & gmask;
-        }
+        return G == nullptr ? 3 : global_visit(G, epoch, id);
     }
 };
 
