@@ -435,7 +435,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
     RL.init(capmax, g.m, g.mpad, exact ? g.dim : 0);
-    const void *rev_fn = exact ? (const void *)reverse_exact_kernel : (const void *)reverse_kernel;
+    const bool rc2 = g.cap0 <= 64;  // base rows of <= 64 slots: two 32-slot chunks
+    const void *rev_fn = exact ? (const void *)reverse_exact_kernel
+                         : rc2 ? (const void *)reverse_kernel<2>
+                               : (const void *)reverse_kernel<kRowChunks>;
     const size_t smem_rev = (size_t)kReverseWarps * RL.total;
     FA_CUDA(cudaFuncSetAttribute(rev_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));
@@ -582,8 +585,12 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         if (exact)
             reverse_exact_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
                 gb, req_sorted, b.nreq, heads, nheads, next_seg, ix->upper_owner, RL, ctr);
+        else if (rc2)
+            reverse_kernel<2><<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
+                gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg,
+                ix->upper_owner, RL, ctr);
         else
-            reverse_kernel<<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
+            reverse_kernel<kRowChunks><<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
                 gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg,
                 ix->upper_owner, RL, ctr);
         FA_BUILD_CUDA(cudaGetLastError());

@@ -110,6 +110,7 @@ __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys
                                      int64_t *__restrict__ heads, int *__restrict__ nheads,
                                      int *__restrict__ next);
 
+template <int RC>
 __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                const uint8_t *__restrict__ sdtT,
                                const unsigned long long *__restrict__ keys, int64_t N,

@@ -59,6 +59,8 @@ __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys
     if (h) heads[base + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = i;
 }
 
+// RC: row chunks of 32 slots compiled in (cap <= 32 RC)
+template <int RC>
 __global__ void __maxnreg__(96) reverse_kernel(
     Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ sdtT,
     const unsigned long long *__restrict__ keys, int64_t N, const int64_t *__restrict__ heads,
@@ -163,9 +165,9 @@ __global__ void __maxnreg__(96) reverse_kernel(
                 // the candidates; x survives iff no L_j (j < p) dominates it;
                 // L_j (j >= p) drops iff x survives and dominates it.
                 int p = 0;
-                unsigned long long kj[kRowChunks];
+                unsigned long long kj[RC];
 #pragma unroll
-                for (int c = 0; c < kRowChunks; ++c) {
+                for (int c = 0; c < RC; ++c) {
                     const int j = c * 32 + lane;
                     kj[c] = KEY_MAX;
                     if (j < cap) kj[c] = ((unsigned long long)rowd_s[j] << 32) | (uint32_t)row_s[j];
@@ -176,7 +178,7 @@ __global__ void __maxnreg__(96) reverse_kernel(
                 // dominating member settles it
                 bool xkept = true;
 #pragma unroll
-                for (int c = 0; c < kRowChunks; ++c) {
+                for (int c = 0; c < RC; ++c) {
                     if (c * 32 >= p) break;
                     bool domx = false;
                     if (kj[c] < kx)
@@ -196,7 +198,7 @@ __global__ void __maxnreg__(96) reverse_kernel(
                 }
                 // survivors in candidate order: L_0..L_{p-1}, x, L_p..
 #pragma unroll
-                for (int c = 0; c < kRowChunks; ++c) {
+                for (int c = 0; c < RC; ++c) {
                     const int j = c * 32 + lane;
                     bool keep = false;
                     int uj = -1;
@@ -236,10 +238,10 @@ __global__ void __maxnreg__(96) reverse_kernel(
                     }
                 }
                 __syncwarp();
-                unsigned long long mine[kRowChunks + 1];
-                int rk[kRowChunks + 1];
+                unsigned long long mine[RC + 1];
+                int rk[RC + 1];
 #pragma unroll
-                for (int c = 0; c <= kRowChunks; ++c) {
+                for (int c = 0; c <= RC; ++c) {
                     const int j = c * 32 + lane;
                     rk[c] = -1;
                     if (j <= cap) {
@@ -249,7 +251,7 @@ __global__ void __maxnreg__(96) reverse_kernel(
                 }
                 __syncwarp();
 #pragma unroll
-                for (int c = 0; c <= kRowChunks; ++c)
+                for (int c = 0; c <= RC; ++c)
                     if (rk[c] >= 0) cand[rk[c]] = mine[c];
                 __syncwarp();
                 unsigned long long sym = 0;
@@ -495,5 +497,15 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         atomicAdd(ctr + 6, n_full);
     }
 }
+
+template __global__ void reverse_kernel<2>(Graph, const uint8_t *, const uint8_t *,
+                                           const unsigned long long *, int64_t, const int64_t *,
+                                           const int *, int *, const int32_t *, ReverseLayout,
+                                           unsigned long long *);
+template __global__ void reverse_kernel<kRowChunks>(Graph, const uint8_t *, const uint8_t *,
+                                                    const unsigned long long *, int64_t,
+                                                    const int64_t *, const int *, int *,
+                                                    const int32_t *, ReverseLayout,
+                                                    unsigned long long *);
 
 }  // namespace fa
