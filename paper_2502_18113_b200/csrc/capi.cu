@@ -2,6 +2,7 @@
 // mirror the reference core's blocking Cython entry points
 // (build_graph _core.pyx:711-764, search_batch _core.pyx:817-888).
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -46,7 +47,15 @@ struct DevBuf {
 // overlaps the host copies of the others and the host side runs on several
 // cores.  The pinned pool is allocated once per process.
 constexpr size_t kStageBytes = size_t(32) << 20;
-constexpr int kStageWorkers = 8;
+// worker threads (FLASHANN_B200_STAGE_WORKERS, default 8, at most 32)
+static int stage_workers() {
+    static int w = 0;
+    if (w == 0) {
+        const char *e = getenv("FLASHANN_B200_STAGE_WORKERS");
+        w = e ? std::min(32, std::max(1, atoi(e))) : 8;
+    }
+    return w;
+}
 static std::mutex g_stage_mu;
 static std::vector<void *> g_stage;
 
@@ -59,7 +68,7 @@ static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
         return FA_OK;
     }
     std::lock_guard<std::mutex> lk(g_stage_mu);  // one staged copy at a time
-    const int T = (int)std::min<size_t>(kStageWorkers, nchunk);
+    const int T = (int)std::min<size_t>(stage_workers(), nchunk);
     while ((int)g_stage.size() < T) {
         void *p = nullptr;
         cudaError_t e = cudaHostAlloc(&p, kStageBytes, cudaHostAllocDefault);
