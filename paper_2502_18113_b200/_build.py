@@ -30,6 +30,8 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
 # diagnostics build: per-phase SM cycles of the layer search in point_stats
 if os.environ.get("FLASHANN_B200_PHASE_PROFILE") == "1":
     NVCC_FLAGS.append("-DFA_PHASE_PROFILE=1")
+# experiment builds: extra -D flags (e.g. "-DFA_PIPE=0")
+NVCC_FLAGS += os.environ.get("FLASHANN_B200_NVCC_DEFS", "").split()
 
 
 def nvcc() -> str:

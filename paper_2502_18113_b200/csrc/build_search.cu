@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         long long sel_cycles = 0;
         for (int layer = top; layer >= 0; --layer) {
             int ts = 0;
-            bool ok = layer_search<P, J, EM, RC>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
+            bool ok = layer_search<P, J, EM, RC, 9>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
                                    ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
             if (!ok) {
                 if (lane == 0) atomicExch(err, 1);

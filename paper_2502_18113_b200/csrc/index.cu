@@ -419,7 +419,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // sorted results join it when both fit, else they take their own space.
     const size_t sel_bytes = exact ? (size_t)2 * round_up(R, 4) * 4 + (size_t)g.dim * 4
                                    : (size_t)select_tv_bytes(g.m, g.mpad, R);
-    int hl = opts->hash_log2 > 0 ? std::max(opts->hash_log2, 9) : 12;
+    // (the build kernels compile the table's 2^9 buckets in: requests above
+    // 2^12 slots are clamped; growing hl below only makes room for the
+    // selection workspace)
+    int hl = opts->hash_log2 > 0 ? std::min(std::max(opts->hash_log2, 9), 12) : 12;
     while (((size_t)16 << vis_buckets_log2(hl)) < sel_bytes) ++hl;
     const bool t_alias =
         sel_bytes + (size_t)round_up(C, 32) * 8 <= ((size_t)16 << vis_buckets_log2(hl));

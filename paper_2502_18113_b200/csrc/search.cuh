@@ -19,6 +19,10 @@
 #ifndef FA_PHASE_PROFILE
 #define FA_PHASE_PROFILE 0
 #endif
+// 1: Flash searches with one expansion per step take layer_search_pipe
+#ifndef FA_PIPE
+#define FA_PIPE 1
+#endif
 
 namespace fa {
 
@@ -149,11 +153,20 @@ __device__ __forceinline__ uint32_t adt_one(const uint8_t *adt_s, const uint8_t 
 // Distances of the nf ids in ids_s[] (shared) into out_s[] (shared).  G lanes
 // per id (G = chunks rounded up to a power of two), each summing one
 // 16-subspace chunk gathered with a 16-byte load.
+// Lanes per id of dists_for: the id's 16-byte code chunks rounded up to a
+// power of two (log2); a pass covers 32 >> lg ids.
+__device__ __forceinline__ int dist_lanes_log2(int mpad) {
+    const int chunks = mpad >> 4;
+    return chunks <= 1 ? 0 : 32 - __clz(chunks - 1);
+}
+
+// pre: the first pass's code chunk of this lane is already loaded (w0)
 __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *__restrict__ codes,
                                           int mpad, const int32_t *ids_s, int nf,
-                                          uint32_t *out_s, int lane) {
+                                          uint32_t *out_s, int lane, bool pre = false,
+                                          uint4 w0 = make_uint4(0, 0, 0, 0)) {
     const int chunks = mpad >> 4;
-    const int lg = chunks <= 1 ? 0 : 32 - __clz(chunks - 1);
+    const int lg = dist_lanes_log2(mpad);
     const int G = 1 << lg;
     const int gi = lane >> lg, c = lane & (G - 1);
     const bool active = c < chunks;
@@ -169,8 +182,13 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
         const int f = base + gi;
         uint32_t sum = 0;
         if (f < nf && active) {
-            const int id = ids_s[f];
-            const uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
+            uint4 w;
+            if (pre && base == 0) {
+                w = w0;
+            } else {
+                const int id = ids_s[f];
+                w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
+            }
             const uint32_t W[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -235,6 +253,23 @@ static __device__ __noinline__ int global_visit(uint32_t *G, uint32_t epoch, int
     }
 }
 
+// Read-only membership test of the global tier (L2 reads, no insertion).
+static __device__ __noinline__ bool global_seen(const uint32_t *G, uint32_t epoch, int id) {
+    const uint32_t key = (uint32_t)id + 1u;
+    const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
+    const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
+    uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
+    while (true) {
+        const uint32_t v = *reinterpret_cast<const volatile uint32_t *>(G + p);
+        if (v == gk) return true;
+        if ((v >> 24) != epoch) return false;
+        p = (p + 1u) & gmask;
+    }
+}
+
+// KB: log2 of the shared tier's bucket count compiled in (0 = from hlog2 at
+// run time); the build kernels fix it at 9 (the 8 KB table).
+template <int KB = 0>
 struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
@@ -253,7 +288,7 @@ struct VisitedSet {
 
     __device__ void begin(void *H, int hlog2, uint32_t *gtables, uint32_t *gepochs, int lane) {
         B = reinterpret_cast<uint4 *>(H);
-        kb = vis_buckets_log2(hlog2);
+        kb = KB ? KB : vis_buckets_log2(hlog2);
         nslots = vis_bucket_slots(hlog2);
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
@@ -279,31 +314,56 @@ struct VisitedSet {
         __syncwarp();
     }
 
+    // bucket of id and its remainder r (1 .. 2^(24 - kb))
+    __device__ __forceinline__ uint4 *bucket(int id, uint32_t &r) const {
+        const int k = KB ? KB : kb;
+        const uint32_t h = ((uint32_t)id * kVisMul) & 0xffffffu;
+        r = (h & ((1u << (24 - k)) - 1u)) + 1u;
+        return B + (h >> (24 - k));
+    }
+    // some 16-bit slot of v equals the remainder (rr = r in both halves):
+    // unsigned 16x2 minimum of v ^ rr (VIMNMX) has a zero half
+    __device__ static __forceinline__ bool holds(const uint4 &v, uint32_t rr) {
+        const uint32_t m = __vminu2(__vminu2(v.x ^ rr, v.y ^ rr), __vminu2(v.z ^ rr, v.w ^ rr));
+        return ((m & 0xffffu) == 0u) | (m < 0x10000u);
+    }
+    // filled slots (they fill in order, so also the first free one)
+    __device__ static __forceinline__ int filled(const uint4 &v) {
+        const uint32_t o = 0x00010001u;
+        const uint32_t f = __vminu2(v.x, o) + __vminu2(v.y, o) + __vminu2(v.z, o) + __vminu2(v.w, o);
+        return (int)((f & 0xffffu) + (f >> 16));
+    }
+
     // 0 = already visited, 1 = new (shared tier), 2 = new (global tier),
     // 3 = the global tier is unavailable (overflow)
     __device__ int visit(int id) {
-        const uint32_t h = ((uint32_t)id * kVisMul) & 0xffffffu;
-        const uint32_t r = (h & ((1u << (24 - kb)) - 1u)) + 1u;
-        uint4 *bk = B + (h >> (24 - kb));
-        const uint32_t rr = r | (r << 16);
+        uint32_t r;
+        uint4 *bk = bucket(id, r);
+        const uint32_t rr = r * 0x10001u;
         uint4 v = *bk;  // the common case (a visited id) needs this one read
         while (true) {
-            if ((__vcmpeq2(v.x, rr) | __vcmpeq2(v.y, rr) | __vcmpeq2(v.z, rr) |
-                 __vcmpeq2(v.w, rr)) != 0u)
-                return 0;
-            // slots fill in order: the first empty slot = the number of filled ones
-            const uint32_t f = __vsetne2(v.x, 0u) + __vsetne2(v.y, 0u) + __vsetne2(v.z, 0u) +
-                               __vsetne2(v.w, 0u);
-            const int e = (int)((f & 0xffffu) + (f >> 16));
+            if (holds(v, rr)) return 0;
+            const int e = filled(v);
             if (e >= nslots) break;
             const int wi = e >> 1;
-            const uint32_t ow = wi == 0 ? v.x : wi == 1 ? v.y : wi == 2 ? v.z : v.w;
+            const uint32_t ow = (wi & 2) ? ((wi & 1) ? v.w : v.z) : ((wi & 1) ? v.y : v.x);
             const uint32_t nw = ow | (r << (16 * (e & 1)));
             if (atomicCAS(reinterpret_cast<uint32_t *>(bk) + wi, ow, nw) == ow) return 1;
             // another lane took the slot: re-read the bucket
             v = lds128_volatile(bk);
         }
         return G == nullptr ? 3 : global_visit(G, epoch, id);
+    }
+
+    // Read-only test (no insertion): true iff visit(id) would insert now.
+    // Callers keep inserts and probes in separate __syncwarp-ed phases.
+    __device__ __forceinline__ bool probe(int id) const {
+        uint32_t r;
+        const uint4 *bk = bucket(id, r);
+        const uint4 v = *bk;
+        if (holds(v, r * 0x10001u)) return false;
+        if (filled(v) < nslots || G == nullptr) return true;
+        return !global_seen(G, epoch, id);
     }
 };
 
@@ -672,8 +732,122 @@ __device__ __forceinline__ void warp_bitonic(K (&k)[J], int lane) {
     }
 }
 
-// RC: id-row chunks of 32 slots compiled in (cap <= 32 RC)
-template <typename P, int J, int EM, int RC = kRowChunks>
+// Offer the nf fresh candidates (ids[f], distances fd[f]) of one expansion
+// to the register result set (layer_search_reg's acceptance rules): those
+// with d < worst (all while the set is not full) are taken in ascending
+// (d, tie) order, filling free slots first, then each evicting the current
+// victim (largest d, smallest tie) while it is still below the worst.
+template <typename P, int J>
+__device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, int &ts, int W,
+                                              uint32_t &wd, int &tq_h, int &tq_t, int32_t *TQ,
+                                              typename P::Key *Sa, typename P::Key *Sb,
+                                              const int32_t *fresh, const uint32_t *fdist, int nf,
+                                              const TieOrder &to, int lane) {
+    using K = typename P::Key;
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned lt = (1u << lane) - 1u;
+    // candidates that can possibly enter: all while the set is not full,
+    // else d < worst
+    int ns = 0;
+    for (int base = 0; base < nf; base += 32) {
+        const int f = base + lane;
+        const bool ok = f < nf && fdist[f] < wd;
+        const unsigned b = __ballot_sync(FULL, ok);
+        if (ok) Sa[ns + __popc(b & lt)] = P::key(fdist[f], to.fwd((uint32_t)fresh[f]));
+        ns += __popc(b);
+    }
+    __syncwarp();
+    if (ns == 0) return;
+    const int nfill = min(ns, W - ts);
+    const K *src = Sa;
+    if (nfill < ns) {
+        // offers are processed in ascending order: rank-sort them
+        for (int j = lane; j < ns; j += 32) {
+            const K k = Sa[j];
+            int r = 0;
+            for (int t = 0; t < ns; ++t) r += Sa[t] < k;
+            Sb[r] = k;
+        }
+        __syncwarp();
+        src = Sb;
+    }
+    // the first nfill offers fill slots ts .. ts + nfill
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int o = lane + 32 * j - ts;
+        if (o >= 0 && o < nfill) {
+            rs.key[j] = src[o];
+            rs.fl &= ~(1u << j);
+        }
+    }
+    ts += nfill;
+    // worst distance wd: recomputed lazily (as the next victim's distance);
+    // stale = the set changed since wd was last known
+    bool stale = ts == W && nfill > 0;
+    if (nfill < ns) {
+        const uint32_t lm = RegSet<J, K>::live_mask(ts, lane);
+        for (int j = nfill; j < ns; ++j) {
+            const K s = src[j];
+            // victim: largest distance, smallest tie; its distance is the
+            // current worst
+            K vf;
+            int vj;
+            rs.victim(lm, vf, vj);
+            K m = 0;
+            int owner = 0;
+            warp_pick_max(vj >= 0, vf, m, owner);
+            const uint32_t cur = (uint32_t)(m >> 24);
+            if (cur < wd) {
+                // the evicted ties are beyond the new worst (none before the
+                // set first fills)
+                if (wd != 0xffffffffu) tq_h = tq_t = 0;
+                wd = cur;
+            }
+            stale = false;
+            if ((uint32_t)(s >> 24) >= wd) break;  // sorted: later offers are rejected too
+            const uint32_t expd = __shfl_sync(FULL, (rs.fl >> vj) & 1u, owner);
+            if (!expd) {
+                if (lane == 0) TQ[tq_t] = (int32_t)((m ^ 0xffffffu) & 0xffffffu);
+                ++tq_t;
+            }
+            if (lane == owner) rs.put(vj, s);
+            stale = true;
+        }
+    }
+    if (stale) {
+        const uint32_t nwd = rs.maxd(ts, lane);
+        if (nwd < wd) {
+            if (wd != 0xffffffffu) tq_h = tq_t = 0;
+            wd = nwd;
+        }
+    }
+    __syncwarp();
+}
+
+// The result set out, ascending, as 64-bit keys: T[0..ts).
+template <int J, typename K>
+__device__ __forceinline__ void sort_out(const RegSet<J, K> &rs, int ts, unsigned long long *T,
+                                         int lane) {
+    // sort once: bitonic network over the 32 * J register slots (empty slots
+    // hold the largest key and sort last), then the first ts go out
+    // (J not a power of two: the network runs over JP registers, the extra
+    // ones holding the largest key)
+    constexpr int JP = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : 16;
+    K ks[JP];
+#pragma unroll
+    for (int j = 0; j < JP; ++j)
+        ks[j] = (j < J && lane + 32 * j < ts) ? rs.key[j < J ? j : 0] : ~K(0);
+    warp_bitonic<JP>(ks, lane);
+#pragma unroll
+    for (int j = 0; j < JP; ++j) {
+        const int e = 32 * j + lane;
+        if (e < ts) T[e] = make_key((uint32_t)(ks[j] >> 24), (int)(ks[j] & 0xffffffu));
+    }
+    __syncwarp();
+}
+
+// RC: id-row chunks of 32 slots compiled in (cap <= 32 RC); KB: VisitedSet
+template <typename P, int J, int EM, int RC = kRowChunks, int KB = 0>
 __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int entry,
                                                  uint32_t entry_d, int W, const uint8_t *qc,
                                                  unsigned long long *T, int &ts_out,
@@ -687,7 +861,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     K *Sa = reinterpret_cast<K *>(S);
     K *Sb = Sa + cand_capacity(g);
     const unsigned lt = (1u << lane) - 1u;
-    VisitedSet vs;
+    VisitedSet<KB> vs;
     vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
     if (lane == 0) vs.visit(entry);
     RegSet<J, K> rs;
@@ -813,99 +987,9 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         if (nf == 0) continue;
         P::dists(g, qc, fresh, nf, fdist, lane);
         phase_mark(cnt, 2, tph);
-        // candidates that can possibly enter: all while the set is not full,
-        // else d < worst
-        int ns = 0;
-        for (int base = 0; base < nf; base += 32) {
-            const int f = base + lane;
-            const bool ok = f < nf && fdist[f] < wd;
-            const unsigned b = __ballot_sync(FULL, ok);
-            if (ok) Sa[ns + __popc(b & lt)] = P::key(fdist[f], to.fwd((uint32_t)fresh[f]));
-            ns += __popc(b);
-        }
-        __syncwarp();
-        if (ns == 0) continue;
-        const int nfill = min(ns, W - ts);
-        const K *src = Sa;
-        if (nfill < ns) {
-            // offers are processed in ascending order: rank-sort them
-            for (int j = lane; j < ns; j += 32) {
-                const K k = Sa[j];
-                int r = 0;
-                for (int t = 0; t < ns; ++t) r += Sa[t] < k;
-                Sb[r] = k;
-            }
-            __syncwarp();
-            src = Sb;
-        }
-        // the first nfill offers fill slots ts .. ts + nfill
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int o = lane + 32 * j - ts;
-            if (o >= 0 && o < nfill) {
-                rs.key[j] = src[o];
-                rs.fl &= ~(1u << j);
-            }
-        }
-        ts += nfill;
-        // worst distance wd: recomputed lazily (as the next victim's distance);
-        // stale = the set changed since wd was last known
-        bool stale = ts == W && nfill > 0;
-        if (nfill < ns) {
-            const uint32_t lm = RegSet<J, K>::live_mask(ts, lane);
-            for (int j = nfill; j < ns; ++j) {
-                const K s = src[j];
-                // victim: largest distance, smallest tie; its distance is the
-                // current worst
-                K vf;
-                int vj;
-                rs.victim(lm, vf, vj);
-                K m = 0;
-                int owner = 0;
-                warp_pick_max(vj >= 0, vf, m, owner);
-                const uint32_t cur = (uint32_t)(m >> 24);
-                if (cur < wd) {
-                    // the evicted ties are beyond the new worst (none before the
-                    // set first fills)
-                    if (wd != 0xffffffffu) tq_h = tq_t = 0;
-                    wd = cur;
-                }
-                stale = false;
-                if ((uint32_t)(s >> 24) >= wd) break;  // sorted: later offers are rejected too
-                const uint32_t expd = __shfl_sync(FULL, (rs.fl >> vj) & 1u, owner);
-                if (!expd) {
-                    if (lane == 0) TQ[tq_t] = (int32_t)((m ^ 0xffffffu) & 0xffffffu);
-                    ++tq_t;
-                }
-                if (lane == owner) rs.put(vj, s);
-                stale = true;
-            }
-        }
-        if (stale) {
-            const uint32_t nwd = rs.maxd(ts, lane);
-            if (nwd < wd) {
-                if (wd != 0xffffffffu) tq_h = tq_t = 0;
-                wd = nwd;
-            }
-        }
-        __syncwarp();
+        accept_offers<P, J>(rs, ts, W, wd, tq_h, tq_t, TQ, Sa, Sb, fresh, fdist, nf, to, lane);
     }
-    // sort once: bitonic network over the 32 * J register slots (empty slots
-    // hold the largest key and sort last), then the first ts go out
-    // (J not a power of two: the network runs over JP registers, the extra
-    // ones holding the largest key)
-    constexpr int JP = J <= 2 ? 2 : J <= 4 ? 4 : J <= 8 ? 8 : 16;
-    K ks[JP];
-#pragma unroll
-    for (int j = 0; j < JP; ++j)
-        ks[j] = (j < J && lane + 32 * j < ts) ? rs.key[j < J ? j : 0] : ~K(0);
-    warp_bitonic<JP>(ks, lane);
-#pragma unroll
-    for (int j = 0; j < JP; ++j) {
-        const int e = 32 * j + lane;
-        if (e < ts) T[e] = make_key((uint32_t)(ks[j] >> 24), (int)(ks[j] & 0xffffffu));
-    }
-    __syncwarp();
+    sort_out<J>(rs, ts, T, lane);
     ts_out = ts;
     return true;
 }
@@ -924,7 +1008,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
     uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
     uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
     uint32_t *Sb = Sa + cand_capacity(g);
-    VisitedSet vs;
+    VisitedSet<> vs;
     vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
     if (lane == 0) {
         vs.visit(entry);
@@ -1098,7 +1182,175 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
 // Best-first layer search with the result-set variant J chosen by the host
 // (set_variant): J slots per lane in registers, J = 0 the shared-memory set
 // (Flash only).  P: the distance policy (FlashDist / ExactDist).
-template <typename P, int J, int EM, int RC = kRowChunks>
+// Flash, one expansion per step (the build's and the query search's common
+// case): layer_search_reg's rules with the next expansion's work started one
+// step early.  The row of the predicted next pop (the unexpanded minimum
+// assuming no offer enters; right for ~98 % of the pops at config 2) is
+// loaded during the current step; at the top of the next step, before the
+// pop, its ids are tested against the visited set read-only (no insertion
+// happens between that test and the pop's own visit, so the test is exact),
+// the not-yet-visited ones compacted into PF, and the first pass of their
+// code rows issued into registers.  When the pop confirms the prediction only
+// the PF ids are inserted (one compacted pass instead of the whole row) and
+// their distances start from registers that were loaded during the pop;
+// otherwise the step takes the plain path.  Results, counters and visit
+// order are those of layer_search_reg.
+template <int J, int RC, int KB>
+__device__ __forceinline__ bool layer_search_pipe(const Graph &g, int layer, int entry,
+                                                  uint32_t entry_d, int W, const uint8_t *qc,
+                                                  unsigned long long *T, int &ts_out,
+                                                  unsigned long long *S, int32_t *TQ,
+                                                  int32_t *fresh, uint32_t *fdist, uint32_t *H,
+                                                  int hlog2, SearchCounters &cnt,
+                                                  const TieOrder &to, int lane) {
+    using P = FlashDist;
+    using K = uint32_t;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int cap = layer_cap(g, layer);
+    K *Sa = reinterpret_cast<K *>(S);
+    K *Sb = Sa + cand_capacity(g);
+    // PF: the predicted row's not-yet-visited ids (Sb is free between the
+    // acceptance of one step and the next step's offers)
+    int32_t *PF = reinterpret_cast<int32_t *>(Sb);
+    const unsigned lt = (1u << lane) - 1u;
+    const int lg = dist_lanes_log2(g.mpad);
+    const int pgi = lane >> lg, pc = lane & ((1 << lg) - 1);
+    const bool pact = pc < (g.mpad >> 4);
+    VisitedSet<KB> vs;
+    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
+    if (lane == 0) vs.visit(entry);
+    RegSet<J, K> rs;
+#pragma unroll
+    for (int j = 0; j < J; ++j) rs.key[j] = K(0);
+    rs.fl = 0u;
+    if (lane == 0) rs.key[0] = P::key(entry_d, to.fwd((uint32_t)entry));
+    int ts = 1;
+    uint32_t wd = 0xffffffffu;  // worst distance once the set is full
+    int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
+    int pre_v = -1;             // predicted next pop; its id row in pre[]
+    int pre[RC];
+    long long tph = phase_clock();
+    __syncwarp();
+    while (true) {
+        phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
+        // ---- early work for the predicted pop: read-only visited test of its
+        // row, compaction into PF, first pass of their code rows
+        int pf_nf = 0, pf_live = 0;
+        uint4 pfw = make_uint4(0, 0, 0, 0);
+        if (pre_v >= 0) {
+#pragma unroll
+            for (int k = 0; k < RC; ++k) {
+                if (k * 32 >= cap) break;
+                const int x = pre[k];
+                const bool live = x >= 0;
+                const bool fr = live && vs.probe(x);
+                const unsigned bf = __ballot_sync(FULL, fr);
+                if (fr) PF[pf_nf + __popc(bf & lt)] = x;
+                pf_nf += __popc(bf);
+                pf_live += __popc(__ballot_sync(FULL, live));
+            }
+            __syncwarp();
+            if (pgi < pf_nf && pact)
+                pfw = __ldg(reinterpret_cast<const uint4 *>(g.codes + (size_t)PF[pgi] * g.mpad +
+                                                            pc * 16));
+        }
+        // ---- pop the frontier minimum: unexpanded set members vs tie queue
+        K b1, b2;
+        int j1;
+        const uint32_t um = RegSet<J, K>::live_mask(ts, lane) & ~rs.fl;
+        rs.min2(um, b1, j1, b2);
+        const int nl = __popc(um);
+        K m = 0;
+        int owner = -1;
+        const bool anyT = warp_pick(nl > 0, b1, m, owner);
+        const bool anyQ = tq_h < tq_t;
+        if (!anyT && !anyQ) break;
+        const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
+        const bool fromT = anyT && (!anyQ || m < kQ);
+        const int pv = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
+        if (fromT) {
+            if (lane == owner) rs.fl |= 1u << j1;
+        } else {
+            ++tq_h;
+        }
+        const bool hit = pv == pre_v;
+        int u[RC];
+        if (!hit) load_row(row_ids(g, layer, pv), cap, lane, u);
+        // predict the next pop assuming nothing new enters: the popped lane
+        // offers its second smallest key
+        {
+            const bool h2 = fromT && lane == owner ? nl > 1 : nl > 0;
+            const K c2 = fromT && lane == owner ? b2 : b1;
+            K m2 = 0;
+            int o2 = -1;
+            const bool anyT2 = warp_pick(h2, c2, m2, o2);
+            const bool anyQ2 = tq_h < tq_t;
+            if (anyT2 || anyQ2) {
+                const K kQ2 = anyQ2 ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
+                pre_v = to.back(
+                    (uint32_t)((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu));
+                load_row(row_ids(g, layer, pre_v), cap, lane, pre);
+            } else {
+                pre_v = -1;
+            }
+        }
+        cnt.visited += 1;
+        phase_mark(cnt, 0, tph);
+        if (vs.gcount + cap > vs.glimit) return false;
+        bool over = false;
+        int nf = 0;
+        bool pre_ok = false;
+        if (hit) {
+            // insert the PF ids; they are all new unless the row repeats an id
+            // (never in a graph built here), in which case the compaction
+            // drops the repeats and the preloaded codes are not used
+            bool lost = false;
+            for (int base = 0; base < pf_nf; base += 32) {
+                const int f = base + lane;
+                const int x = f < pf_nf ? PF[f] : -1;
+                const int rr = x >= 0 ? vs.visit(x) : 0;
+                over |= rr == 3;
+                lost |= x >= 0 && rr == 0;
+                const bool fr = rr == 1 || rr == 2;
+                const unsigned bf = __ballot_sync(FULL, fr);
+                if (fr) fresh[nf + __popc(bf & lt)] = x;
+                nf += __popc(bf);
+                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
+            }
+            pre_ok = !__any_sync(FULL, lost);
+        } else {
+            pf_live = 0;
+#pragma unroll
+            for (int k = 0; k < RC; ++k) {
+                if (k * 32 >= cap) break;
+                const int x = u[k];
+                const bool live = x >= 0;
+                const int rr = live ? vs.visit(x) : 0;
+                over |= rr == 3;
+                const bool fr = rr == 1 || rr == 2;
+                const unsigned bf = __ballot_sync(FULL, fr);
+                if (fr) fresh[nf + __popc(bf & lt)] = x;
+                nf += __popc(bf);
+                pf_live += __popc(__ballot_sync(FULL, live));
+                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
+            }
+        }
+        cnt.kcalls += (pf_live + 15) >> 4;
+        if (__any_sync(FULL, over)) return false;
+        cnt.dist += nf;
+        __syncwarp();
+        phase_mark(cnt, 1, tph);
+        if (nf == 0) continue;
+        dists_for(qc, g.codes, g.mpad, fresh, nf, fdist, lane, pre_ok, pfw);
+        phase_mark(cnt, 2, tph);
+        accept_offers<P, J>(rs, ts, W, wd, tq_h, tq_t, TQ, Sa, Sb, fresh, fdist, nf, to, lane);
+    }
+    sort_out<J>(rs, ts, T, lane);
+    ts_out = ts;
+    return true;
+}
+
+template <typename P, int J, int EM, int RC = kRowChunks, int KB = 0>
 __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
                                              int W, const uint8_t *qc, unsigned long long *T,
                                              int &ts, unsigned long long *S, int32_t *TQ,
@@ -1109,9 +1361,12 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
         static_assert(!P::kExact, "the shared-memory result set serves the Flash kind only");
         return layer_search_smem(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
                                  hlog2, cnt, to, lane);
+    } else if constexpr (FA_PIPE && EM == 1 && !P::kExact) {
+        return layer_search_pipe<J, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
+                                            fdist, H, hlog2, cnt, to, lane);
     } else {
-        return layer_search_reg<P, J, EM, RC>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
-                                          fdist, H, hlog2, cnt, to, lane);
+        return layer_search_reg<P, J, EM, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ,
+                                                  fresh, fdist, H, hlog2, cnt, to, lane);
     }
 }
 
