@@ -19,10 +19,6 @@
 #ifndef FA_PHASE_PROFILE
 #define FA_PHASE_PROFILE 0
 #endif
-// 1: Flash searches with one expansion per step take layer_search_pipe
-#ifndef FA_PIPE
-#define FA_PIPE 1
-#endif
 
 namespace fa {
 
@@ -160,11 +156,9 @@ __device__ __forceinline__ int dist_lanes_log2(int mpad) {
     return chunks <= 1 ? 0 : 32 - __clz(chunks - 1);
 }
 
-// pre: the first pass's code chunk of this lane is already loaded (w0)
 __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *__restrict__ codes,
                                           int mpad, const int32_t *ids_s, int nf,
-                                          uint32_t *out_s, int lane, bool pre = false,
-                                          uint4 w0 = make_uint4(0, 0, 0, 0)) {
+                                          uint32_t *out_s, int lane) {
     const int chunks = mpad >> 4;
     const int lg = dist_lanes_log2(mpad);
     const int G = 1 << lg;
@@ -182,13 +176,8 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
         const int f = base + gi;
         uint32_t sum = 0;
         if (f < nf && active) {
-            uint4 w;
-            if (pre && base == 0) {
-                w = w0;
-            } else {
-                const int id = ids_s[f];
-                w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
-            }
+            const int id = ids_s[f];
+            const uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
             const uint32_t W[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -249,20 +238,6 @@ static __device__ __noinline__ int global_visit(uint32_t *G, uint32_t epoch, int
             if (old == gk) return 0;
             continue;
         }
-        p = (p + 1u) & gmask;
-    }
-}
-
-// Read-only membership test of the global tier (L2 reads, no insertion).
-static __device__ __noinline__ bool global_seen(const uint32_t *G, uint32_t epoch, int id) {
-    const uint32_t key = (uint32_t)id + 1u;
-    const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
-    const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
-    uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
-    while (true) {
-        const uint32_t v = *reinterpret_cast<const volatile uint32_t *>(G + p);
-        if (v == gk) return true;
-        if ((v >> 24) != epoch) return false;
         p = (p + 1u) & gmask;
     }
 }
@@ -353,17 +328,6 @@ struct VisitedSet {
             v = lds128_volatile(bk);
         }
         return G == nullptr ? 3 : global_visit(G, epoch, id);
-    }
-
-    // Read-only test (no insertion): true iff visit(id) would insert now.
-    // Callers keep inserts and probes in separate __syncwarp-ed phases.
-    __device__ __forceinline__ bool probe(int id) const {
-        uint32_t r;
-        const uint4 *bk = bucket(id, r);
-        const uint4 v = *bk;
-        if (holds(v, r * 0x10001u)) return false;
-        if (filled(v) < nslots || G == nullptr) return true;
-        return !global_seen(G, epoch, id);
     }
 };
 
@@ -1182,174 +1146,6 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
 // Best-first layer search with the result-set variant J chosen by the host
 // (set_variant): J slots per lane in registers, J = 0 the shared-memory set
 // (Flash only).  P: the distance policy (FlashDist / ExactDist).
-// Flash, one expansion per step (the build's and the query search's common
-// case): layer_search_reg's rules with the next expansion's work started one
-// step early.  The row of the predicted next pop (the unexpanded minimum
-// assuming no offer enters; right for ~98 % of the pops at config 2) is
-// loaded during the current step; at the top of the next step, before the
-// pop, its ids are tested against the visited set read-only (no insertion
-// happens between that test and the pop's own visit, so the test is exact),
-// the not-yet-visited ones compacted into PF, and the first pass of their
-// code rows issued into registers.  When the pop confirms the prediction only
-// the PF ids are inserted (one compacted pass instead of the whole row) and
-// their distances start from registers that were loaded during the pop;
-// otherwise the step takes the plain path.  Results, counters and visit
-// order are those of layer_search_reg.
-template <int J, int RC, int KB>
-__device__ __forceinline__ bool layer_search_pipe(const Graph &g, int layer, int entry,
-                                                  uint32_t entry_d, int W, const uint8_t *qc,
-                                                  unsigned long long *T, int &ts_out,
-                                                  unsigned long long *S, int32_t *TQ,
-                                                  int32_t *fresh, uint32_t *fdist, uint32_t *H,
-                                                  int hlog2, SearchCounters &cnt,
-                                                  const TieOrder &to, int lane) {
-    using P = FlashDist;
-    using K = uint32_t;
-    constexpr unsigned FULL = 0xffffffffu;
-    const int cap = layer_cap(g, layer);
-    K *Sa = reinterpret_cast<K *>(S);
-    K *Sb = Sa + cand_capacity(g);
-    // PF: the predicted row's not-yet-visited ids (Sb is free between the
-    // acceptance of one step and the next step's offers)
-    int32_t *PF = reinterpret_cast<int32_t *>(Sb);
-    const unsigned lt = (1u << lane) - 1u;
-    const int lg = dist_lanes_log2(g.mpad);
-    const int pgi = lane >> lg, pc = lane & ((1 << lg) - 1);
-    const bool pact = pc < (g.mpad >> 4);
-    VisitedSet<KB> vs;
-    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
-    if (lane == 0) vs.visit(entry);
-    RegSet<J, K> rs;
-#pragma unroll
-    for (int j = 0; j < J; ++j) rs.key[j] = K(0);
-    rs.fl = 0u;
-    if (lane == 0) rs.key[0] = P::key(entry_d, to.fwd((uint32_t)entry));
-    int ts = 1;
-    uint32_t wd = 0xffffffffu;  // worst distance once the set is full
-    int tq_h = 0, tq_t = 0;     // tie queue TQ[tq_h..tq_t), distance == wd
-    int pre_v = -1;             // predicted next pop; its id row in pre[]
-    int pre[RC];
-    long long tph = phase_clock();
-    __syncwarp();
-    while (true) {
-        phase_mark(cnt, 3, tph);  // the previous iteration's acceptance
-        // ---- early work for the predicted pop: read-only visited test of its
-        // row, compaction into PF, first pass of their code rows
-        int pf_nf = 0, pf_live = 0;
-        uint4 pfw = make_uint4(0, 0, 0, 0);
-        if (pre_v >= 0) {
-#pragma unroll
-            for (int k = 0; k < RC; ++k) {
-                if (k * 32 >= cap) break;
-                const int x = pre[k];
-                const bool live = x >= 0;
-                const bool fr = live && vs.probe(x);
-                const unsigned bf = __ballot_sync(FULL, fr);
-                if (fr) PF[pf_nf + __popc(bf & lt)] = x;
-                pf_nf += __popc(bf);
-                pf_live += __popc(__ballot_sync(FULL, live));
-            }
-            __syncwarp();
-            if (pgi < pf_nf && pact)
-                pfw = __ldg(reinterpret_cast<const uint4 *>(g.codes + (size_t)PF[pgi] * g.mpad +
-                                                            pc * 16));
-        }
-        // ---- pop the frontier minimum: unexpanded set members vs tie queue
-        K b1, b2;
-        int j1;
-        const uint32_t um = RegSet<J, K>::live_mask(ts, lane) & ~rs.fl;
-        rs.min2(um, b1, j1, b2);
-        const int nl = __popc(um);
-        K m = 0;
-        int owner = -1;
-        const bool anyT = warp_pick(nl > 0, b1, m, owner);
-        const bool anyQ = tq_h < tq_t;
-        if (!anyT && !anyQ) break;
-        const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
-        const bool fromT = anyT && (!anyQ || m < kQ);
-        const int pv = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
-        if (fromT) {
-            if (lane == owner) rs.fl |= 1u << j1;
-        } else {
-            ++tq_h;
-        }
-        const bool hit = pv == pre_v;
-        int u[RC];
-        if (!hit) load_row(row_ids(g, layer, pv), cap, lane, u);
-        // predict the next pop assuming nothing new enters: the popped lane
-        // offers its second smallest key
-        {
-            const bool h2 = fromT && lane == owner ? nl > 1 : nl > 0;
-            const K c2 = fromT && lane == owner ? b2 : b1;
-            K m2 = 0;
-            int o2 = -1;
-            const bool anyT2 = warp_pick(h2, c2, m2, o2);
-            const bool anyQ2 = tq_h < tq_t;
-            if (anyT2 || anyQ2) {
-                const K kQ2 = anyQ2 ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
-                pre_v = to.back(
-                    (uint32_t)((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu));
-                load_row(row_ids(g, layer, pre_v), cap, lane, pre);
-            } else {
-                pre_v = -1;
-            }
-        }
-        cnt.visited += 1;
-        phase_mark(cnt, 0, tph);
-        if (vs.gcount + cap > vs.glimit) return false;
-        bool over = false;
-        int nf = 0;
-        bool pre_ok = false;
-        if (hit) {
-            // insert the PF ids; they are all new unless the row repeats an id
-            // (never in a graph built here), in which case the compaction
-            // drops the repeats and the preloaded codes are not used
-            bool lost = false;
-            for (int base = 0; base < pf_nf; base += 32) {
-                const int f = base + lane;
-                const int x = f < pf_nf ? PF[f] : -1;
-                const int rr = x >= 0 ? vs.visit(x) : 0;
-                over |= rr == 3;
-                lost |= x >= 0 && rr == 0;
-                const bool fr = rr == 1 || rr == 2;
-                const unsigned bf = __ballot_sync(FULL, fr);
-                if (fr) fresh[nf + __popc(bf & lt)] = x;
-                nf += __popc(bf);
-                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
-            }
-            pre_ok = !__any_sync(FULL, lost);
-        } else {
-            pf_live = 0;
-#pragma unroll
-            for (int k = 0; k < RC; ++k) {
-                if (k * 32 >= cap) break;
-                const int x = u[k];
-                const bool live = x >= 0;
-                const int rr = live ? vs.visit(x) : 0;
-                over |= rr == 3;
-                const bool fr = rr == 1 || rr == 2;
-                const unsigned bf = __ballot_sync(FULL, fr);
-                if (fr) fresh[nf + __popc(bf & lt)] = x;
-                nf += __popc(bf);
-                pf_live += __popc(__ballot_sync(FULL, live));
-                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
-            }
-        }
-        cnt.kcalls += (pf_live + 15) >> 4;
-        if (__any_sync(FULL, over)) return false;
-        cnt.dist += nf;
-        __syncwarp();
-        phase_mark(cnt, 1, tph);
-        if (nf == 0) continue;
-        dists_for(qc, g.codes, g.mpad, fresh, nf, fdist, lane, pre_ok, pfw);
-        phase_mark(cnt, 2, tph);
-        accept_offers<P, J>(rs, ts, W, wd, tq_h, tq_t, TQ, Sa, Sb, fresh, fdist, nf, to, lane);
-    }
-    sort_out<J>(rs, ts, T, lane);
-    ts_out = ts;
-    return true;
-}
-
 template <typename P, int J, int EM, int RC = kRowChunks, int KB = 0>
 __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
                                              int W, const uint8_t *qc, unsigned long long *T,
@@ -1361,9 +1157,6 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
         static_assert(!P::kExact, "the shared-memory result set serves the Flash kind only");
         return layer_search_smem(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
                                  hlog2, cnt, to, lane);
-    } else if constexpr (FA_PIPE && EM == 1 && !P::kExact) {
-        return layer_search_pipe<J, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh,
-                                            fdist, H, hlog2, cnt, to, lane);
     } else {
         return layer_search_reg<P, J, EM, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ,
                                                   fresh, fdist, H, hlog2, cnt, to, lane);
