@@ -607,12 +607,19 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_BUILD_CUDA(cudaStreamSynchronize(st));
     if (prof) {
         double acc[4] = {0, 0, 0, 0};
-        for (size_t bi = 0; bi < batches.size(); ++bi)
+        // FLASHANN_B200_BATCH_LOG=1: one stderr line per batch (diagnostics)
+        const bool blog = getenv("FLASHANN_B200_BATCH_LOG") != nullptr;
+        for (size_t bi = 0; bi < batches.size(); ++bi) {
+            float bms[4] = {0.f, 0.f, 0.f, 0.f};
             for (int k = 0; k < 4; ++k) {
-                float ms = 0.f;
-                FA_BUILD_CUDA(cudaEventElapsedTime(&ms, ev[bi * 5 + k], ev[bi * 5 + k + 1]));
-                acc[k] += ms;
+                FA_BUILD_CUDA(cudaEventElapsedTime(&bms[k], ev[bi * 5 + k], ev[bi * 5 + k + 1]));
+                acc[k] += bms[k];
             }
+            if (blog)
+                fprintf(stderr, "[fa batch] %zu start %lld size %d nreq %lld ms %.4f %.4f %.4f %.4f\n",
+                        bi, (long long)batches[bi].start, batches[bi].size,
+                        (long long)batches[bi].nreq, bms[0], bms[1], bms[2], bms[3]);
+        }
         for (auto &e : ev) cudaEventDestroy(e);
         res->ms_encode = acc[0];
         res->ms_search = acc[1];

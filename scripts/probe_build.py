@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--bmax", type=int, default=None)
     ap.add_argument("--hash-log2", type=int, default=0)
     ap.add_argument("--tie", type=int, default=None)
+    ap.add_argument("--expand", type=int, default=None)
     ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     import torch
@@ -48,6 +49,8 @@ def main():
         over["batch_max"] = args.bmax
     if args.tie is not None:
         over["tie"] = args.tie
+    if args.expand is not None:
+        over["expand"] = args.expand
     stats = torch.zeros((args.n, 8), dtype=torch.int64, device="cuda")
     for r in range(args.reps):
         torch.cuda.synchronize()
