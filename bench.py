@@ -321,13 +321,18 @@ def main():
     data, queries = dataset.baseline_config(CFG, n=n, nq=0 if args.no_search else c["nq"])
     x_dev = torch.from_numpy(data).cuda()
 
-    # coder training on the GPU (coding_seconds)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    sample = builder.training_sample(data, builder.DEFAULT_SAMPLE, 0)
-    model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=10)
-    torch.cuda.synchronize()
-    coding_s = time.perf_counter() - t0
+    # coder training on the GPU (coding_seconds).  The first call in a process
+    # also pays the cuBLAS / cuSOLVER handle set-up (coding_seconds_cold); the
+    # reported figure is the second, identical call.
+    coding = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sample = builder.training_sample(data, builder.DEFAULT_SAMPLE, 0)
+        model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=10)
+        torch.cuda.synchronize()
+        coding.append(time.perf_counter() - t0)
+    coding_s = coding[-1]
 
     params = graph.BuildParams(C=c["efC"], R=c["M"], seed=0)
     levels = graph.assign_layers(n, 0, c["M"])
@@ -401,7 +406,8 @@ def main():
                       "parallelism": f"replicas x{world}",
                       "l2": "inputs larger than L2 (no flush)",
                       "batch": {k: v for k, v in sm100.BUILD_OPTIONS.items() if k != "profile"}},
-           "coding_seconds": coding_s, "kernel_ms_per_build": kernel_ms,
+           "coding_seconds": coding_s, "coding_seconds_cold": coding[0],
+           "kernel_ms_per_build": kernel_ms,
            "counters": {k: ctrs[-1][k] for k in ("dist_comps", "sym_comps", "visited",
                                                   "kernel_calls", "reverse_prunes",
                                                   "reverse_appends", "n_batches")},

@@ -108,6 +108,12 @@ typedef struct {
     unsigned int has_uint32, uinteger;
 } fa_pcg64_state;
 
+/* k-means subsamples on the host: sel[i] = np.sort(rng_i.permutation(ns)[:cap])
+ * for rng_i = default_rng(seed + i) given as its PCG64 state (kmeans.py:50-54);
+ * states are advanced exactly as numpy advances them.  Host pointers; runs
+ * the m subspaces on parallel threads; needs no device.                      */
+int fa_kmeans_subsample(int64_t ns, int cap, int m, void *states, int32_t *sel);
+
 /* Scratch bytes needed by fa_kmeans_subspaces_dev.                           */
 size_t fa_kmeans_scratch_bytes(int m, int nsub);
 

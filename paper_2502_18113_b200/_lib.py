@@ -66,6 +66,7 @@ _SIGS = {
     "fa_sdt_sum_dev": (C.c_int, [vp, C.c_int, vp, i64, vp, i64, i64, vp, vp]),
     "fa_select_dev": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
     "fa_kmeans_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "fa_kmeans_subsample": (C.c_int, [i64, C.c_int, C.c_int, vp, vp]),
     "fa_kmeans_subspaces_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp,
                                           C.c_int, vp, C.c_int, vp, vp, vp]),
     "fa_flash_range_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp, vp,

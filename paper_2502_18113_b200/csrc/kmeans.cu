@@ -12,6 +12,10 @@
 // numpy's float64 summation order is reproduced where it decides a value:
 // np.sum is pairwise (n < 8 sequential from 0; 8..128 eight strided
 // accumulators; recursive halving above), which `pw_sum` restates.
+#include <algorithm>
+#include <thread>
+#include <vector>
+
 #include "common.cuh"
 
 namespace fa {
@@ -25,13 +29,13 @@ struct Pcg64 {
     unsigned __int128 s, inc;
     bool has;
     uint32_t u;
-    __device__ explicit Pcg64(const Pcg64State &st) {
+    __host__ __device__ explicit Pcg64(const Pcg64State &st) {
         s = ((unsigned __int128)st.s_hi << 64) | st.s_lo;
         inc = ((unsigned __int128)st.inc_hi << 64) | st.inc_lo;
         has = st.has_uint32 != 0;
         u = st.uinteger;
     }
-    __device__ uint64_t next64() {
+    __host__ __device__ uint64_t next64() {
         const unsigned __int128 mult =
             ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
         s = s * mult + inc;
@@ -39,7 +43,7 @@ struct Pcg64 {
         unsigned rot = (unsigned)(s >> 122);
         return (x >> rot) | (x << ((64 - rot) & 63));
     }
-    __device__ uint32_t next32() {
+    __host__ __device__ uint32_t next32() {
         if (has) {
             has = false;
             return u;
@@ -48,6 +52,28 @@ struct Pcg64 {
         has = true;
         u = (uint32_t)(v >> 32);
         return (uint32_t)v;
+    }
+    __host__ void store(Pcg64State &st) const {
+        st.s_hi = (unsigned long long)(s >> 64);
+        st.s_lo = (unsigned long long)s;
+        st.inc_hi = (unsigned long long)(inc >> 64);
+        st.inc_lo = (unsigned long long)inc;
+        st.has_uint32 = has ? 1u : 0u;
+        st.uinteger = u;
+    }
+    // random_interval (numpy distributions.c): a draw in [0, mx] by masked
+    // rejection, 32-bit draws while mx fits
+    __host__ uint64_t interval(uint64_t mx) {
+        if (mx == 0) return 0;
+        uint64_t mask = mx;
+        for (int k = 1; k < 64; k <<= 1) mask |= mask >> k;
+        uint64_t v;
+        if (mx <= 0xffffffffull) {
+            do v = next32() & mask; while (v > mx);
+        } else {
+            do v = next64() & mask; while (v > mx);
+        }
+        return v;
     }
     // Generator.random(): 53-bit double
     __device__ double random() { return (double)(next64() >> 11) * (1.0 / 9007199254740992.0); }
@@ -389,6 +415,35 @@ extern "C" int fa_kmeans_subspaces_dev(const float *xs, int64_t ns, int ld, cons
                                          reinterpret_cast<const Pcg64State *>(states), iters, xbuf,
                                          d2, asg, cent_out, dmax, hist_out);
     FA_LAUNCH_CHECK();
+    return FA_OK;
+}
+
+// k-means subsample rows of every subspace on the host cores:
+// np.sort(default_rng(seed + i).permutation(ns)[:cap]) (kmeans.py:50-54) —
+// numpy's shuffle of arange(ns) (Fisher-Yates from the top, j =
+// random_interval(i)) replayed from the generator's state, which is left as
+// numpy leaves it.  The subspaces run on parallel threads.
+extern "C" int fa_kmeans_subsample(int64_t ns, int cap, int m, void *states, int32_t *sel) {
+    FA_CHECK_ARG(ns >= 1 && cap >= 1 && cap <= ns && m >= 1 && states && sel,
+                 "bad subsample arguments");
+    FA_CHECK_ARG(ns <= 0x7fffffffll, "sample of %lld rows too large", (long long)ns);
+    Pcg64State *st = reinterpret_cast<Pcg64State *>(states);
+    const int T = std::max(1, std::min<int>(m, (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([=]() {
+            std::vector<int32_t> a((size_t)ns);
+            for (int i = t; i < m; i += T) {
+                Pcg64 rng(st[i]);
+                for (int64_t k = 0; k < ns; ++k) a[k] = (int32_t)k;
+                for (int64_t k = ns - 1; k > 0; --k) std::swap(a[k], a[rng.interval((uint64_t)k)]);
+                int32_t *out = sel + (size_t)i * cap;
+                std::copy(a.begin(), a.begin() + cap, out);
+                std::sort(out, out + cap);
+                rng.store(st[i]);
+            }
+        });
+    for (auto &x : th) x.join();
     return FA_OK;
 }
 

@@ -87,18 +87,21 @@ _PCG_DT = np.dtype([("s_hi", "<u8"), ("s_lo", "<u8"), ("inc_hi", "<u8"), ("inc_l
 
 def _rng_streams(ns: int, m: int, seed: int):
     """Per-subspace subsample rows and the PCG64 state after drawing them
-    (kmeans.py:50-54: default_rng(seed+i); permutation(n)[:k*256], sorted)."""
+    (kmeans.py:50-54: default_rng(seed+i); permutation(n)[:k*256], sorted).
+    The permutations run in the core library on the host cores
+    (fa_kmeans_subsample); numpy only seeds the generators."""
     cap = K * MAX_POINTS_PER_CENTROID
     states = np.zeros(m, dtype=_PCG_DT)
-    sel = np.zeros((m, cap), dtype=np.int32) if ns > cap else None
     for i in range(m):
-        rng = np.random.default_rng(seed + i)
-        if sel is not None:
-            sel[i] = np.sort(rng.permutation(ns)[:cap])
-        st = rng.bit_generator.state
+        st = np.random.default_rng(seed + i).bit_generator.state
         s, inc = st["state"]["state"], st["state"]["inc"]
         states[i] = (s >> 64, s & ((1 << 64) - 1), inc >> 64, inc & ((1 << 64) - 1),
                      st["has_uint32"], st["uinteger"])
+    if ns <= cap:
+        return None, states
+    sel = np.zeros((m, cap), dtype=np.int32)
+    check(_lib.load(require_device=False).fa_kmeans_subsample(
+        ns, cap, m, states.ctypes.data, sel.ctypes.data))
     return sel, states
 
 
