@@ -119,6 +119,46 @@ int DevBuf::upload(const void *src, size_t bytes) {
     return staged_copy(const_cast<void *>(src), p, bytes, false);
 }
 
+// A staged host-to-device copy on a helper thread (same device as the
+// caller); join() returns its status and carries its error text over.
+struct AsyncUpload {
+    int rc = FA_OK;
+    char err[sizeof(g_err)] = "";
+    std::thread th;
+    bool joined = false;
+    AsyncUpload(const void *src, void *dst, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        th = std::thread([this, src, dst, bytes, dev]() {
+            cudaError_t e = cudaSetDevice(dev);
+            rc = e == cudaSuccess ? staged_copy(const_cast<void *>(src), dst, bytes, false)
+                                  : FA_ECUDA;
+            if (rc != FA_OK) snprintf(err, sizeof(err), "%s", g_err);
+        });
+    }
+    int join() {
+        if (!joined) {
+            th.join();
+            joined = true;
+            if (rc != FA_OK) set_error("%s", err);
+        }
+        return rc;
+    }
+    ~AsyncUpload() {
+        if (!joined) th.join();
+    }
+};
+// FA_TRY that first waits for an in-flight AsyncUpload (its buffers must
+// outlive it)
+#define FA_TRY_JOIN(up, call)      \
+    do {                           \
+        int _rc = (call);          \
+        if (_rc != FA_OK) {        \
+            (up).join();           \
+            return _rc;            \
+        }                          \
+    } while (0)
+
 struct IndexGuard {
     fa_index *ix = nullptr;
     ~IndexGuard() { fa_index_destroy(ix); }
@@ -164,14 +204,16 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     }
     PhaseTimer tm;
     DevBuf dproj_b, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper;
-    FA_TRY(dproj_b.upload(proj, sizeof(float) * n * dproj));
-    tm.mark("upload proj");
-    FA_TRY(dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
-    FA_TRY(ddims.upload(dims, sizeof(int32_t) * m));
-    FA_TRY(doffs.upload(offs, sizeof(int32_t) * m));
-    FA_TRY(dsdt.upload(sdt, (size_t)m * 256));
-    FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
-    FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
+    // the projected vectors (the one large input) upload on a helper thread
+    // while the model and layer arrays go up and the index is created
+    FA_TRY(dproj_b.alloc(sizeof(float) * n * dproj));
+    AsyncUpload up(proj, dproj_b.p, sizeof(float) * n * dproj);
+    FA_TRY_JOIN(up, dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
+    FA_TRY_JOIN(up, ddims.upload(dims, sizeof(int32_t) * m));
+    FA_TRY_JOIN(up, doffs.upload(offs, sizeof(int32_t) * m));
+    FA_TRY_JOIN(up, dsdt.upload(sdt, (size_t)m * 256));
+    FA_TRY_JOIN(up, dlev.upload(levels, sizeof(int32_t) * n));
+    FA_TRY_JOIN(up, duoff.upload(uoff, sizeof(int64_t) * n));
     fa_index_desc d;
     memset(&d, 0, sizeof(d));
     d.n = n; d.m = m; d.R = R; d.dim = 0; d.dproj = dproj; d.dmax = dmax;
@@ -181,8 +223,9 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     d.uoff = duoff.as<int64_t>(); d.n_upper_rows = n_upper_rows;
     tm.mark("upload model/levels");
     IndexGuard guard;
-    FA_TRY(fa_index_create(&d, &guard.ix));
-    tm.mark("index create");
+    FA_TRY_JOIN(up, fa_index_create(&d, &guard.ix));
+    FA_TRY(up.join());
+    tm.mark("uploads + index create");
     FA_TRY(fa_index_encode(guard.ix, nullptr));
     FA_TRY(fa_index_build(guard.ix, opts, res, nullptr));
     tm.mark("encode + build");

@@ -115,36 +115,75 @@ static int pick_hash_log2(int W, int capmax, int R, int mpad, int req, size_t al
     return l;
 }
 
-// Export one row to the reference block layout (layout.py:1-45): count,
-// ids (-1 beyond count), subspace-major 16-slot code batches (0 beyond count).
-__global__ void export_kernel(Graph g, int64_t rows, bool upper, uint8_t *__restrict__ blocks,
-                              int64_t stride, int cap, int capp) {
+// Export rows to the reference block layout (layout.py:1-45): count, ids
+// (-1 beyond count), subspace-major 16-slot code batches (0 beyond count).
+// One warp per row: the live neighbours' code rows are staged in shared
+// memory (row stride mpad + 4: the 16 lanes of one output chunk read 16
+// different banks), then every 16-byte chunk (batch bt, subspace i) = the
+// i-th code byte of slots bt*16 .. bt*16+15 is packed into four words.
+constexpr int kExportWarps = 8;
+__global__ void __launch_bounds__(kExportWarps * 32) export_kernel(
+    Graph g, int64_t rows, bool upper, uint8_t *__restrict__ blocks, int64_t stride, int cap,
+    int capp) {
+    extern __shared__ __align__(16) uint8_t xs[];
     const int lane = lane_id();
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int wid = threadIdx.x >> 5;
+    const int cs = g.mpad + 4;  // staged row stride
     const int nb = (cap + 15) >> 4;
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows;
-         r += warps) {
+    uint8_t *st = xs + (size_t)wid * nb * 16 * cs;
+    const int64_t warps = (int64_t)gridDim.x * kExportWarps;
+    const int q16 = g.mpad >> 4;  // 16-byte words per code row
+    for (int64_t r = (int64_t)blockIdx.x * kExportWarps + wid; r < rows; r += warps) {
         const int32_t *ids = (upper ? g.adjU : g.adj0) + r * capp;
         const int cnt = (upper ? g.cntU : g.cnt0)[r];
         uint8_t *b = blocks + r * stride;
         if (lane == 0) *reinterpret_cast<int32_t *>(b) = cnt;
         int32_t *bid = reinterpret_cast<int32_t *>(b + 4);
         for (int j = lane; j < cap; j += 32) bid[j] = j < cnt ? ids[j] : -1;
-        uint8_t *region = b + 4 + 4 * cap;
-        const int total = nb * g.m * 16;
-        for (int t = lane; t < total; t += 32) {
-            int bt = t / (g.m * 16);
-            int rem = t % (g.m * 16);
-            int i = rem >> 4, ln = rem & 15;
-            int slot = bt * 16 + ln;
-            uint8_t c = 0;
-            if (slot < cnt) {
-                int u = ids[slot];
-                if (u >= 0) c = g.codes[(size_t)u * g.mpad + i];
+        // stage: slot j's code row (zeros past the count or for a -1 id)
+        for (int t = lane; t < nb * 16 * q16; t += 32) {
+            const int j = t / q16, w = t - j * q16;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (j < cnt) {
+                const int u = ids[j];
+                if (u >= 0)
+                    v = __ldg(reinterpret_cast<const uint4 *>(g.codes + (size_t)u * g.mpad) + w);
             }
-            region[t] = c;
+            uint32_t *d = reinterpret_cast<uint32_t *>(st + j * cs + w * 16);
+            d[0] = v.x;
+            d[1] = v.y;
+            d[2] = v.z;
+            d[3] = v.w;
         }
+        __syncwarp();
+        // the reference's rows are 4 (mod 16) bytes long: 4-byte stores
+        uint32_t *region = reinterpret_cast<uint32_t *>(b + 4 + 4 * cap);
+        for (int t = lane; t < nb * g.m; t += 32) {
+            const int bt = t / g.m, i = t - bt * g.m;
+            const uint8_t *c = st + (bt * 16) * cs + i;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t b0 = c[(4 * k + 0) * cs], b1 = c[(4 * k + 1) * cs];
+                const uint32_t b2 = c[(4 * k + 2) * cs], b3 = c[(4 * k + 3) * cs];
+                region[4 * t + k] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+            }
+        }
+        __syncwarp();
     }
+}
+
+static int launch_export(const Graph &g, int64_t rows, bool upper, uint8_t *blocks, int64_t stride,
+                         int cap, int capp, cudaStream_t st) {
+    const size_t smem = (size_t)kExportWarps * round_up(cap, 16) * (g.mpad + 4);
+    if (smem > 48 * 1024)
+        FA_CUDA(cudaFuncSetAttribute(export_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    const int grid = (int)std::min<int64_t>((rows + kExportWarps - 1) / kExportWarps,
+                                            (int64_t)num_sms() * 8);
+    export_kernel<<<std::max(grid, 1), kExportWarps * 32, smem, st>>>(g, rows, upper, blocks,
+                                                                      stride, cap, capp);
+    FA_LAUNCH_CHECK();
+    return FA_OK;
 }
 
 __global__ void import_kernel(Graph g, int64_t rows, bool upper, const uint8_t *__restrict__ blocks,
@@ -801,15 +840,12 @@ extern "C" int fa_index_export_blocks(fa_index *ix, uint8_t *base_blocks, int64_
     FA_CHECK_ARG(base_stride >= 4 + 4 * g.cap0 + nb0 * g.m * 16, "base stride too small");
     cudaStream_t st = as_stream(stream);
     if (g.n) {
-        export_kernel<<<1184, 256, 0, st>>>(g, g.n, false, base_blocks, base_stride, g.cap0, g.cap0p);
-        FA_LAUNCH_CHECK();
+        FA_TRY(launch_export(g, g.n, false, base_blocks, base_stride, g.cap0, g.cap0p, st));
     }
     if (g.nU) {
         FA_CHECK_ARG(upper_blocks && upper_stride >= 4 + 4 * g.capU + nbU * g.m * 16,
                      "upper stride too small");
-        export_kernel<<<1184, 256, 0, st>>>(g, g.nU, true, upper_blocks, upper_stride, g.capU,
-                                            g.capUp);
-        FA_LAUNCH_CHECK();
+        FA_TRY(launch_export(g, g.nU, true, upper_blocks, upper_stride, g.capU, g.capUp, st));
     }
     return FA_OK;
 }
