@@ -46,7 +46,15 @@ struct DevBuf {
 // own chunks (DMA on its own stream + host memcpy), so the DMA of one chunk
 // overlaps the host copies of the others and the host side runs on several
 // cores.  The pinned pool is allocated once per process.
-constexpr size_t kStageBytes = size_t(32) << 20;
+// chunk size (FLASHANN_B200_STAGE_MB, default 32)
+static size_t stage_bytes() {
+    static size_t b = 0;
+    if (b == 0) {
+        const char *e = getenv("FLASHANN_B200_STAGE_MB");
+        b = (size_t)(e ? std::min(256, std::max(1, atoi(e))) : 32) << 20;
+    }
+    return b;
+}
 // worker threads (FLASHANN_B200_STAGE_WORKERS, default 8, at most 32)
 static int stage_workers() {
     static int w = 0;
@@ -61,6 +69,7 @@ static std::vector<void *> g_stage;
 
 static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
     if (bytes == 0) return FA_OK;
+    const size_t kStageBytes = stage_bytes();
     const size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
     if (nchunk < 2) {
         FA_CUDA(d2h ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost)
