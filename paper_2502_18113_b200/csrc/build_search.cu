@@ -14,7 +14,7 @@ template <typename P, int J, int EM, int RC>
 __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
-    unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
+    const int32_t *__restrict__ order, unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
     int64_t *__restrict__ stats, int *__restrict__ work) {
     // sdtT: the transposed SDT in global memory (L1-resident; keeping it out of
     // shared memory leaves room for one more CTA per SM)
@@ -30,7 +30,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         if (lane == 0) p = atomicAdd(work, 1);
         p = __shfl_sync(0xffffffffu, p, 0);
         if (p >= size) break;
-        const int x = start + p;
+        // the batch's vertices in the host's processing order (upper-layer
+        // vertices, the longest searches, first: a shorter tail)
+        const int q = __ldg(order + p);
+        const int x = start + q;
         const long long t_begin = clock64();
         const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
         __syncwarp();
@@ -38,7 +41,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
             float *qv = reinterpret_cast<float *>(ws.adt);
             for (int i = lane; i < g.dim; i += 32) qv[i] = __ldg(g.vecs + (size_t)x * g.dim + i);
         } else {
-            load_adt_smem(ws.adt, adt_batch + (size_t)p * g.mpad * 16, g.mpad, lane);
+            load_adt_smem(ws.adt, adt_batch + (size_t)q * g.mpad * 16, g.mpad, lane);
         }
         __syncwarp();
         SearchCounters cnt = {};
@@ -49,7 +52,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         for (int layer = ml; layer > level; --layer)
             hill_climb<P>(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
         const int top = min(ml, level);
-        unsigned long long *myreq = req + __ldg(req_off + p);
+        unsigned long long *myreq = req + __ldg(req_off + q);
         long long sel_cycles = 0;
         for (int layer = top; layer >= 0; --layer) {
             int ts = 0;

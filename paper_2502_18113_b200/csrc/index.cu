@@ -507,6 +507,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     uint8_t *adt_batch = nullptr, *sdtT = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
+    int32_t *order_d = nullptr;
     int *err = nullptr, *nheads = nullptr, *next_seg = nullptr;
     void *cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -515,7 +516,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // cached across builds): no allocation or free synchronises the device
     auto cleanup = [&]() {
         for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
-                        (void *)req_off_d, (void *)err, cub_tmp, (void *)heads, (void *)nheads,
+                        (void *)req_off_d, (void *)order_d, (void *)err, cub_tmp, (void *)heads,
+                        (void *)nheads,
                         (void *)next_seg, (void *)sdtT})
             if (p) cudaFreeAsync(p, st);
     };
@@ -553,6 +555,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&ctr, sizeof(unsigned long long) * 8)) ||
         (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
+        (rc = dev_alloc((void **)&order_d, sizeof(int32_t) * g.n)) ||
         (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&nheads, 2 * sizeof(int))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
@@ -584,6 +587,22 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
                                   cudaMemcpyHostToDevice, st));
+    // processing order inside each batch: higher levels first (their searches
+    // are the longest: hill climb plus one beam search per layer), ties in
+    // vertex order.  Every vertex of a batch sees the graph as of the batch
+    // start and writes only its own rows and request slots, so the order
+    // changes no result, only the length of the batch's tail.
+    std::vector<int32_t> order((size_t)g.n, 0);  // lives to the end, like req_off
+    {
+        for (const Batch &b : batches) {
+            int32_t *o = order.data() + b.start;
+            for (int k = 0; k < b.size; ++k) o[k] = k;
+            const int32_t *lv = ix->levels_h.data() + b.start;
+            std::stable_sort(o, o + b.size, [lv](int32_t a, int32_t c) { return lv[a] > lv[c]; });
+        }
+        FA_BUILD_CUDA(cudaMemcpyAsync(order_d, order.data(), sizeof(int32_t) * g.n,
+                                      cudaMemcpyHostToDevice, st));
+    }
     // optional per-kernel-class timing: 5 events per batch on the build stream
     const bool prof = opts->profile != 0;
     std::vector<cudaEvent_t> ev;
@@ -611,6 +630,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
         search_fn<<<grid, kSearchWarps * 32, smem_search, st>>>(
             gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+            order_d + b.start,
             req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));

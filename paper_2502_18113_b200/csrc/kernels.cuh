@@ -61,8 +61,8 @@ __device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned
 }
 
 using BuildSearchFn = void (*)(Graph, const uint8_t *, const uint8_t *, int, int, int, int, int,
-                               int, WarpLayout, const int64_t *, unsigned long long *,
-                               unsigned long long *, int *, int64_t *, int *);
+                               int, WarpLayout, const int64_t *, const int32_t *,
+                               unsigned long long *, unsigned long long *, int *, int64_t *, int *);
 using QuerySearchFn = void (*)(Graph, const uint8_t *, int, int, int, int, int, int, const float *,
                                int, const float *, WarpLayout, int64_t *, double *,
                                unsigned long long *, int *);

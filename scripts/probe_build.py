@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--hash-log2", type=int, default=0)
     ap.add_argument("--tie", type=int, default=None)
     ap.add_argument("--expand", type=int, default=None)
+    ap.add_argument("--dump", default=None, help="save the per-point stats (.npy)")
     ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     import torch
@@ -67,6 +68,8 @@ def main():
     res = _lib.BuildResult()
     _lib.check(_lib.load().fa_index_build(g.handle, C.byref(opts), C.byref(res), None))
     st = stats.cpu().numpy()[1:]
+    if args.dump:
+        np.save(args.dump, stats.cpu().numpy())
     exp, cyc = st[:, 0], st[:, 1]
     q = [50, 90, 99, 99.9, 100]
     print(json.dumps({
