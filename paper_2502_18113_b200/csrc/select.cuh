@@ -163,45 +163,19 @@ __device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
     kept_out = kept_ids;
     int nk = 0;
     unsigned long long sym = 0;
-    // this lane's code bytes (subspaces lane + 32 k, k < 4) of the next
-    // candidate, loaded one candidate ahead: the L2 round trip of candidate
-    // j + 1's code row overlaps candidate j's domination test
-    auto code_bytes = [&](int v) {
-        const uint8_t *c = codes + (size_t)v * cs;
-        uint32_t w = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = lane + 32 * k;
-            if (i < m) w |= (uint32_t)__ldg(c + i) << (8 * k);
-        }
-        return w;
-    };
-    int v_next = 0;
-    uint32_t dv_next = 0, cb_next = 0;
-    if (ncand > 0) {
-        get(0, v_next, dv_next);
-        cb_next = code_bytes(v_next);
-    }
     for (int j = 0; j < ncand && nk < cap; ++j) {
-        const int v = v_next;
-        const uint32_t dv = dv_next, cb = cb_next;
-        if (j + 1 < ncand) {
-            get(j + 1, v_next, dv_next);
-            cb_next = code_bytes(v_next);
-        }
+        int v;
+        uint32_t dv;
+        get(j, v, dv);
         const uint8_t *cv = codes + (size_t)v * cs;
         bool bad = false;
         if (nk > 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = lane + 32 * k;
-                if (i < mpad) {
-                    uint4 row = make_uint4(0, 0, 0, 0);
-                    if (i < m)
-                        row = __ldg(reinterpret_cast<const uint4 *>(
-                            sdtT + (i << 8) + (((cb >> (8 * k)) & 0xffu) << 4)));
-                    *reinterpret_cast<uint4 *>(Tv + i * 16) = row;
-                }
+            for (int i = lane; i < mpad; i += 32) {
+                uint4 row = make_uint4(0, 0, 0, 0);
+                if (i < m)
+                    row = __ldg(reinterpret_cast<const uint4 *>(sdtT + (i << 8) +
+                                                                 ((uint32_t)__ldg(cv + i) << 4)));
+                *reinterpret_cast<uint4 *>(Tv + i * 16) = row;
             }
             __syncwarp();
             const uint32_t tv = (uint32_t)__cvta_generic_to_shared(Tv);
