@@ -183,6 +183,8 @@ extern "C" int fa_version(void) { return 1; }
 // FLASHANN_B200_TIMING=1: per-phase wall times of the host drop-ins on stderr
 struct PhaseTimer {
     bool on = getenv("FLASHANN_B200_TIMING") != nullptr;
+    // constructed first, destroyed last: the mark covers the buffer frees
+    ~PhaseTimer() { mark("teardown (frees)"); }
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
     void mark(const char *what) {
         if (!on) return;

@@ -28,6 +28,7 @@ struct fa_index {
     uint8_t *dist0 = nullptr, *distU = nullptr;  // prune-distance caches
     int32_t *upper_owner = nullptr;
     uint32_t *gvis = nullptr, *gvis_epoch = nullptr;  // global visited tier
+    int32_t *order_h = nullptr;  // pinned: the build's per-batch processing order
     int search_tie = 0;
     int64_t entry = -1;
     int max_layer = -1;
@@ -328,6 +329,7 @@ extern "C" int fa_index_destroy(fa_index *ix) {
     cudaFree(ix->upper_owner);
     cudaFree(ix->gvis);
     cudaFree(ix->gvis_epoch);
+    cudaFreeHost(ix->order_h);
     delete ix;
     return FA_OK;
 }
@@ -591,18 +593,22 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // are the longest: hill climb plus one beam search per layer), ties in
     // vertex order.  Every vertex of a batch sees the graph as of the batch
     // start and writes only its own rows and request slots, so the order
-    // changes no result, only the length of the batch's tail.
-    std::vector<int32_t> order((size_t)g.n, 0);  // lives to the end, like req_off
-    {
-        for (const Batch &b : batches) {
-            int32_t *o = order.data() + b.start;
-            for (int k = 0; k < b.size; ++k) o[k] = k;
-            const int32_t *lv = ix->levels_h.data() + b.start;
-            std::stable_sort(o, o + b.size, [lv](int32_t a, int32_t c) { return lv[a] > lv[c]; });
+    // changes no result, only the length of the batch's tail.  Filled per
+    // batch in the launch loop (pinned buffer, async copy): the host work
+    // overlaps the device's earlier batches.
+    if (!ix->order_h) {
+        cudaError_t e = cudaHostAlloc((void **)&ix->order_h, sizeof(int32_t) * g.n,
+                                      cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            ix->order_h = nullptr;
+            set_error("cudaHostAlloc(order): %s", cudaGetErrorString(e));
+            cleanup();
+            return FA_ENOMEM;
         }
-        FA_BUILD_CUDA(cudaMemcpyAsync(order_d, order.data(), sizeof(int32_t) * g.n,
-                                      cudaMemcpyHostToDevice, st));
     }
+    int maxlv = 0;
+    for (int64_t v = 0; v < g.n; ++v) maxlv = std::max(maxlv, ix->levels_h[v]);
+    std::vector<int> lvpos((size_t)maxlv + 2);
     // optional per-kernel-class timing: 5 events per batch on the build stream
     const bool prof = opts->profile != 0;
     std::vector<cudaEvent_t> ev;
@@ -625,6 +631,16 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             }
         }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
+        {  // stable counting sort of the batch by level, descending
+            int32_t *o = ix->order_h + b.start;
+            const int32_t *lv = ix->levels_h.data() + b.start;
+            std::fill(lvpos.begin(), lvpos.end(), 0);
+            for (int k = 0; k < b.size; ++k) ++lvpos[maxlv - lv[k] + 1];
+            for (int l = 1; l <= maxlv + 1; ++l) lvpos[l] += lvpos[l - 1];
+            for (int k = 0; k < b.size; ++k) o[lvpos[maxlv - lv[k]]++] = k;
+            FA_BUILD_CUDA(cudaMemcpyAsync(order_d + b.start, o, sizeof(int32_t) * b.size,
+                                          cudaMemcpyHostToDevice, st));
+        }
         // nheads[0]: reverse row heads, nheads[1]: the search's work counter
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
