@@ -10,6 +10,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -396,6 +398,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     memset(res, 0, sizeof(*res));
     res->entry_point = -1;
     res->max_layer = -1;
+    const auto t_host0 = std::chrono::steady_clock::now();
     FA_TRY(reset_graph(ix, st));
     FA_TRY(ensure_gvis(ix));
     FA_CHECK_ARG(opts->tie >= 0 && opts->tie <= 2, "tie mode must be 0, 1 or 2");
@@ -616,6 +619,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         ev.resize(batches.size() * 5);
         for (auto &e : ev) FA_BUILD_CUDA(cudaEventCreate(&e));
     }
+    if (getenv("FLASHANN_B200_TIMING"))
+        fprintf(stderr, "[fa timing] build host setup (schedule, scratch) %8.2f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                          t_host0).count());
     int64_t launches = 3;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
