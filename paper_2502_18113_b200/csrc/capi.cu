@@ -27,15 +27,8 @@ void set_error(const char *fmt, ...) {
 // RAII device buffer for the host drop-ins.
 struct DevBuf {
     void *p = nullptr;
-    ~DevBuf() { cudaFree(p); }
-    int alloc(size_t bytes) {
-        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
-        if (e != cudaSuccess) {
-            set_error("cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-            return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
-        }
-        return FA_OK;
-    }
+    ~DevBuf() { pool_free(p); }
+    int alloc(size_t bytes) { return pool_alloc(&p, bytes); }
     int upload(const void *src, size_t bytes);
     template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
 };
@@ -67,16 +60,12 @@ static int stage_workers() {
 static std::mutex g_stage_mu;
 static std::vector<void *> g_stage;
 
-static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
-    if (bytes == 0) return FA_OK;
-    const size_t kStageBytes = stage_bytes();
-    const size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
-    if (nchunk < 2) {
-        FA_CUDA(d2h ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost)
-                    : cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
-        return FA_OK;
-    }
+// Run fn(chunk, pinned buffer, stream) -> cudaError_t over chunks 0..nchunk-1
+// on the staging workers (worker w takes chunks w, w + T, ...).
+template <class F>
+static int stage_run(size_t nchunk, const char *what, F fn) {
     std::lock_guard<std::mutex> lk(g_stage_mu);  // one staged copy at a time
+    const size_t kStageBytes = stage_bytes();
     const int T = (int)std::min<size_t>(stage_workers(), nchunk);
     while ((int)g_stage.size() < T) {
         void *p = nullptr;
@@ -97,30 +86,66 @@ static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
             cudaStream_t s = nullptr;
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
             uint8_t *buf = static_cast<uint8_t *>(g_stage[w]);
-            for (size_t c = w; c < nchunk && e == cudaSuccess; c += T) {
-                const size_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
-                uint8_t *h = static_cast<uint8_t *>(host) + off;
-                uint8_t *d = static_cast<uint8_t *>(dev) + off;
-                if (d2h) {
-                    e = cudaMemcpyAsync(buf, d, len, cudaMemcpyDeviceToHost, s);
-                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                    if (e == cudaSuccess) memcpy(h, buf, len);
-                } else {
-                    memcpy(buf, h, len);
-                    e = cudaMemcpyAsync(d, buf, len, cudaMemcpyHostToDevice, s);
-                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                }
-            }
+            for (size_t c = w; c < nchunk && e == cudaSuccess; c += T) e = fn(c, buf, s);
             if (s) cudaStreamDestroy(s);
             err[w] = e;
         });
     for (auto &t : th) t.join();
     for (cudaError_t e : err)
         if (e != cudaSuccess) {
-            set_error("staged %s copy: %s", d2h ? "D2H" : "H2D", cudaGetErrorString(e));
+            set_error("staged %s: %s", what, cudaGetErrorString(e));
             return FA_ECUDA;
         }
     return FA_OK;
+}
+
+static int staged_copy(void *host, void *dev, size_t bytes, bool d2h) {
+    if (bytes == 0) return FA_OK;
+    const size_t kStageBytes = stage_bytes();
+    const size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
+    if (nchunk < 2) {
+        FA_CUDA(d2h ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost)
+                    : cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
+        return FA_OK;
+    }
+    return stage_run(nchunk, d2h ? "D2H copy" : "H2D copy",
+                     [&](size_t c, uint8_t *buf, cudaStream_t s) {
+                         const size_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
+                         uint8_t *h = static_cast<uint8_t *>(host) + off;
+                         uint8_t *d = static_cast<uint8_t *>(dev) + off;
+                         cudaError_t e;
+                         if (d2h) {
+                             e = cudaMemcpyAsync(buf, d, len, cudaMemcpyDeviceToHost, s);
+                             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                             if (e == cudaSuccess) memcpy(h, buf, len);
+                         } else {
+                             memcpy(buf, h, len);
+                             e = cudaMemcpyAsync(d, buf, len, cudaMemcpyHostToDevice, s);
+                             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                         }
+                         return e;
+                     });
+}
+
+// Upload the first row_bytes of each of `rows` strided host rows into a
+// contiguous device array (rows x row_bytes): the workers gather the rows
+// straight into their pinned buffers.  Used for the id part of reference
+// blocks, whose inline code bytes the device index never reads.
+static int staged_gather_rows(void *dev, const void *host, int64_t rows, int64_t src_stride,
+                              size_t row_bytes) {
+    if (rows == 0 || row_bytes == 0) return FA_OK;
+    const size_t per = std::max<size_t>(1, stage_bytes() / row_bytes);
+    const size_t nchunk = ((size_t)rows + per - 1) / per;
+    return stage_run(nchunk, "row gather", [&](size_t c, uint8_t *buf, cudaStream_t s) {
+        const size_t r0 = c * per, r1 = std::min<size_t>((size_t)rows, r0 + per);
+        const uint8_t *h = static_cast<const uint8_t *>(host);
+        for (size_t r = r0; r < r1; ++r)
+            memcpy(buf + (r - r0) * row_bytes, h + r * (size_t)src_stride, row_bytes);
+        cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t *>(dev) + r0 * row_bytes, buf,
+                                        (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        return e;
+    });
 }
 
 int DevBuf::upload(const void *src, size_t bytes) {
@@ -277,11 +302,13 @@ extern "C" int fa_search_batch_host(int64_t n, int dim, const float *vecs, int d
         if (counters) memset(counters, 0, 4 * sizeof(int64_t));
         return FA_OK;
     }
+    PhaseTimer tm;
     DevBuf dvecs, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper, dq, dqp, dcodes, did, dd;
     if (rerank_depth > 0) {
         FA_TRY(dvecs.upload(vecs, sizeof(float) * n * dim));
         FA_TRY(dq.upload(queries, sizeof(float) * (size_t)nq * dim));
     }
+    tm.mark("upload vecs + queries");
     FA_TRY(dqp.upload(qproj, sizeof(float) * (size_t)nq * dproj));
     FA_TRY(dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
     FA_TRY(ddims.upload(dims, sizeof(int32_t) * m));
@@ -289,9 +316,20 @@ extern "C" int fa_search_batch_host(int64_t n, int dim, const float *vecs, int d
     FA_TRY(dsdt.upload(sdt, (size_t)m * 256));
     FA_TRY(dlev.upload(levels, sizeof(int32_t) * n));
     FA_TRY(duoff.upload(uoff, sizeof(int64_t) * n));
-    FA_TRY(dbase.upload(base_blocks, (size_t)n * base_stride));
-    FA_TRY(dupper.upload(upper_blocks, (size_t)n_upper_rows * upper_stride));
+    // only the count + id prefix of each reference block: the inline code
+    // bytes repeat codes[] (write_code_slot, _core.pyx:414-422) and the device
+    // index reads codes from its own table
+    const size_t row0 = 4 + 4 * (size_t)(2 * R), rowU = 4 + 4 * (size_t)R;
+    FA_CHECK_ARG(base_stride >= (int64_t)row0 && (n_upper_rows == 0 || upper_stride >= (int64_t)rowU),
+                 "block stride too small");
+    tm.mark("upload model/levels");
+    FA_TRY(dbase.alloc((size_t)n * row0));
+    FA_TRY(staged_gather_rows(dbase.p, base_blocks, n, base_stride, row0));
+    FA_TRY(dupper.alloc((size_t)n_upper_rows * rowU));
+    FA_TRY(staged_gather_rows(dupper.p, upper_blocks, n_upper_rows, upper_stride, rowU));
+    tm.mark("gather + upload id rows");
     FA_TRY(dcodes.upload(codes, (size_t)n * m));
+    tm.mark("upload codes");
     FA_TRY(did.alloc(sizeof(int64_t) * (size_t)nq * k));
     FA_TRY(dd.alloc(sizeof(double) * (size_t)nq * k));
     fa_index_desc d;
@@ -304,11 +342,13 @@ extern "C" int fa_search_batch_host(int64_t n, int dim, const float *vecs, int d
     IndexGuard guard;
     FA_TRY(fa_index_create(&d, &guard.ix));
     FA_TRY(fa_index_set_codes(guard.ix, dcodes.as<uint8_t>(), m, nullptr));
-    FA_TRY(fa_index_import_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
-                                  upper_stride, nullptr));
+    FA_TRY(fa_index_import_blocks(guard.ix, dbase.as<uint8_t>(), (int64_t)row0,
+                                  dupper.as<uint8_t>(), (int64_t)rowU, nullptr));
+    tm.mark("index create + import");
     FA_TRY(fa_index_search(guard.ix, dq.as<float>(), dqp.as<float>(), nq, ef, k, rerank_depth,
                            entry, max_layer, did.as<int64_t>(), dd.as<double>(), counters,
                            nullptr));
+    tm.mark("search");
     FA_CUDA(cudaMemcpy(out_ids, did.p, sizeof(int64_t) * (size_t)nq * k, cudaMemcpyDeviceToHost));
     FA_CUDA(cudaMemcpy(out_d, dd.p, sizeof(double) * (size_t)nq * k, cudaMemcpyDeviceToHost));
     return FA_OK;

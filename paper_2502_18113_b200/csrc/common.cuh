@@ -45,6 +45,40 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;  // B200; grids use num_sms() (the device's own count)
 
+// ---- device memory from the stream-ordered pool -----------------------------
+// The core's device buffers (index arrays, host drop-in staging targets,
+// build scratch) come from the device's default memory pool with its release
+// threshold raised, so the repeated create/free of the host drop-ins reuses
+// mapped memory instead of paying cudaMalloc / cudaFree (which unmap and
+// synchronise) on every call.  Allocation and free are ordered on the legacy
+// default stream; pool_alloc waits for that stream so the buffer is usable on
+// any stream.
+inline void keep_pool() {
+    static unsigned long long done = 0;  // one bit per device ordinal < 64
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || ((done >> dev) & 1ull)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done |= 1ull << dev;
+}
+inline int pool_alloc(void **p, size_t bytes) {
+    keep_pool();
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        set_error("device allocation of %zu bytes: %s", bytes, cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
+    }
+    return FA_OK;
+}
+inline void pool_free(void *p) {
+    if (p) cudaFreeAsync(p, 0);
+}
+
 // SM count of the current device (cached per process; B200: 148)
 inline int num_sms() {
     static int n = 0;

@@ -38,15 +38,7 @@ struct fa_index {
 
 namespace fa {
 
-static int dev_alloc(void **p, size_t bytes) {
-    if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMalloc(p, bytes);
-    if (e != cudaSuccess) {
-        set_error("cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
-        return e == cudaErrorMemoryAllocation ? FA_ENOMEM : FA_ECUDA;
-    }
-    return FA_OK;
-}
+static int dev_alloc(void **p, size_t bytes) { return pool_alloc(p, bytes); }
 
 __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -85,7 +77,7 @@ static int ensure_gvis(fa_index *ix) {
     FA_TRY(dev_alloc((void **)&d_ns, sizeof(uint32_t)));
     nsmid_kernel<<<1, 1>>>(d_ns);
     cudaError_t e = cudaMemcpy(&nsmid, d_ns, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-    cudaFree(d_ns);
+    pool_free(d_ns);
     if (e != cudaSuccess) {
         set_error("reading %%nsmid: %s", cudaGetErrorString(e));
         return FA_ECUDA;
@@ -324,13 +316,11 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
 
 extern "C" int fa_index_destroy(fa_index *ix) {
     if (!ix) return FA_OK;
-    cudaFree(ix->codes);
-    cudaFree(ix->adj0); cudaFree(ix->cnt0); cudaFree(ix->cons0);
-    cudaFree(ix->adjU); cudaFree(ix->cntU); cudaFree(ix->consU);
-    cudaFree(ix->dist0); cudaFree(ix->distU);
-    cudaFree(ix->upper_owner);
-    cudaFree(ix->gvis);
-    cudaFree(ix->gvis_epoch);
+    for (void *p : {(void *)ix->codes, (void *)ix->adj0, (void *)ix->cnt0, (void *)ix->cons0,
+                    (void *)ix->adjU, (void *)ix->cntU, (void *)ix->consU, (void *)ix->dist0,
+                    (void *)ix->distU, (void *)ix->upper_owner, (void *)ix->gvis,
+                    (void *)ix->gvis_epoch})
+        pool_free(p);
     cudaFreeHost(ix->order_h);
     delete ix;
     return FA_OK;
@@ -534,19 +524,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
         return FA_OK;
     };
-    {
-        static bool pool_set = false;
-        if (!pool_set) {
-            int dev = 0;
-            cudaMemPool_t pool;
-            if (cudaGetDevice(&dev) == cudaSuccess &&
-                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t keep = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-            pool_set = true;
-        }
-    }
+    keep_pool();  // scratch stays mapped in the pool between builds
     int end_bit = 32;
     {
         int64_t rows = g.n + g.nU;
@@ -737,7 +715,7 @@ static int run_query_encode(fa_index *ix, const float *qproj, int nq, uint8_t **
                                ix->d.dmax, ix->d.dist_min, ix->d.delta, nullptr, ix->g.mpad, *adt_q,
                                ix->g.mpad, st);
     if (rc) {
-        cudaFree(*adt_q);
+        pool_free(*adt_q);
         *adt_q = nullptr;
     }
     return rc;
@@ -799,9 +777,9 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
             rc = FA_ECUDA;
         }
     }
-    cudaFree(adt_q);
-    cudaFree(ctr);
-    cudaFree(err);
+    pool_free(adt_q);
+    pool_free(ctr);
+    pool_free(err);
     if (rc) return rc;
     if (herr) {
         set_error("visited hash overflow in query search (ef=%d)", ef);
@@ -862,9 +840,9 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
             rc = FA_ECUDA;
         }
     }
-    cudaFree(adt_q);
-    cudaFree(ctr);
-    cudaFree(err);
+    pool_free(adt_q);
+    pool_free(ctr);
+    pool_free(err);
     if (rc) return rc;
     if (herr) {
         set_error("visited hash overflow in layer search (width=%d)", width);
