@@ -8,7 +8,8 @@ The graph is built on the GPU, exported to the reference layout, and searched
 by both cores (Flash kind, ef 64, k 10, with and without rerank 64): QPS and
 recall@10 against brute force.  The GPU leg runs on device-resident queries
 (evaluation.search_batch_dev) and through the host drop-in
-(sm100.search_batch, numpy in/out, including the block upload).
+(sm100.search_batch, numpy in/out, including the upload of the graph's id
+rows; timed on the second call of the process, like bench.py's e2e leg).
 """
 
 from __future__ import annotations
@@ -57,9 +58,12 @@ def main():
         dt = time.perf_counter() - t0
         r = {"gpu_qps": len(queries) / dt, "gpu_recall@10": evaluation.recall_at_k(
             ids.cpu().numpy(), gt)}
-        t0 = time.perf_counter()
-        sm100.search_batch(4, pv, g.levels, base, g.upper_offsets, upper, c["efC"], c["M"],
-                           g.entry_point, g.max_layer, queries, qaux, 64, 10, rr)
+        # host drop-in: one untimed call first (the per-process pinned staging
+        # pool), then the timed one, which uploads the graph again
+        for it in range(2):
+            t0 = time.perf_counter()
+            sm100.search_batch(4, pv, g.levels, base, g.upper_offsets, upper, c["efC"], c["M"],
+                               g.entry_point, g.max_layer, queries, qaux, 64, 10, rr)
         r["gpu_host_api_qps"] = len(queries) / (time.perf_counter() - t0)
         if core is not None:
             t0 = time.perf_counter()
