@@ -228,6 +228,14 @@ int fa_index_search_layer(fa_index *idx, const float *qproj, int nq, const int64
  * pointers are DEVICE pointers with the reference row strides.              */
 int fa_index_export_blocks(fa_index *idx, uint8_t *base_blocks, int64_t base_stride,
                            uint8_t *upper_blocks, int64_t upper_stride, void *stream);
+/* (count, ids) rows of every layer-0 / upper row: rows x (1 + cap) int32,
+ * ids -1 beyond the count (device pointers; upper_rows may be NULL when the
+ * graph has no upper rows).                                                  */
+int fa_index_export_rows(fa_index *idx, int32_t *base_rows, int32_t *upper_rows, void *stream);
+/* Reference blocks (layout.py:1-45) from (count, ids) rows and the n x m code
+ * table, on the host cores (host pointers; no device needed).               */
+int fa_assemble_blocks(uint8_t *blocks, int64_t rows, int64_t stride, int cap, int m,
+                       const int32_t *id_rows, const uint8_t *codes, int64_t ncodes);
 int fa_index_import_blocks(fa_index *idx, const uint8_t *base_blocks, int64_t base_stride,
                            const uint8_t *upper_blocks, int64_t upper_stride, void *stream);
 /* Device code table (n x code_stride u8) of the index, for export.           */

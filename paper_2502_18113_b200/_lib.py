@@ -67,6 +67,8 @@ _SIGS = {
     "fa_select_dev": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
     "fa_kmeans_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "fa_kmeans_subsample": (C.c_int, [i64, C.c_int, C.c_int, vp, vp]),
+    "fa_assemble_blocks": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, vp, vp, i64]),
+    "fa_index_export_rows": (C.c_int, [vp, vp, vp, vp]),
     "fa_kmeans_subspaces_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp,
                                           C.c_int, vp, C.c_int, vp, vp, vp]),
     "fa_flash_range_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp, vp,

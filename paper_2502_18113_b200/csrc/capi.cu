@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <emmintrin.h>
 #include <chrono>
 #include <mutex>
 #include <thread>
@@ -63,10 +64,10 @@ static std::vector<void *> g_stage;
 // Run fn(chunk, pinned buffer, stream) -> cudaError_t over chunks 0..nchunk-1
 // on the staging workers (worker w takes chunks w, w + T, ...).
 template <class F>
-static int stage_run(size_t nchunk, const char *what, F fn) {
+static int stage_run(size_t nchunk, const char *what, F fn, int workers = 0) {
     std::lock_guard<std::mutex> lk(g_stage_mu);  // one staged copy at a time
     const size_t kStageBytes = stage_bytes();
-    const int T = (int)std::min<size_t>(stage_workers(), nchunk);
+    const int T = (int)std::min<size_t>(workers > 0 ? workers : stage_workers(), nchunk);
     while ((int)g_stage.size() < T) {
         void *p = nullptr;
         cudaError_t e = cudaHostAlloc(&p, kStageBytes, cudaHostAllocDefault);
@@ -193,6 +194,121 @@ struct AsyncUpload {
         }                          \
     } while (0)
 
+// ---- reference blocks assembled on the host ---------------------------------
+// The inline code bytes of a reference block (layout.py:1-45) repeat codes[]
+// of its neighbours, so the host drop-in moves only (count, ids) rows over
+// PCIe and writes the code batches here, from the caller's code table.  A
+// 16-slot batch is a 16 x m byte transpose of 16 code rows: SSE2 unpacks on
+// 16 x 16 tiles (scalar for an m % 16 tail).
+static inline void transpose16(__m128i r[16]) {
+    __m128i a[16], b[16], c[16];
+    for (int k = 0; k < 8; ++k) {
+        a[2 * k] = _mm_unpacklo_epi8(r[2 * k], r[2 * k + 1]);
+        a[2 * k + 1] = _mm_unpackhi_epi8(r[2 * k], r[2 * k + 1]);
+    }
+    for (int g = 0; g < 4; ++g) {
+        b[4 * g + 0] = _mm_unpacklo_epi16(a[4 * g + 0], a[4 * g + 2]);
+        b[4 * g + 1] = _mm_unpackhi_epi16(a[4 * g + 0], a[4 * g + 2]);
+        b[4 * g + 2] = _mm_unpacklo_epi16(a[4 * g + 1], a[4 * g + 3]);
+        b[4 * g + 3] = _mm_unpackhi_epi16(a[4 * g + 1], a[4 * g + 3]);
+    }
+    for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 4; ++q) {
+            c[8 * h + 2 * q] = _mm_unpacklo_epi32(b[8 * h + q], b[8 * h + 4 + q]);
+            c[8 * h + 2 * q + 1] = _mm_unpackhi_epi32(b[8 * h + q], b[8 * h + 4 + q]);
+        }
+    for (int p = 0; p < 8; ++p) {
+        r[2 * p] = _mm_unpacklo_epi64(c[p], c[8 + p]);
+        r[2 * p + 1] = _mm_unpackhi_epi64(c[p], c[8 + p]);
+    }
+}
+
+// Copy len bytes with non-temporal 16-byte stores (no read-for-ownership of
+// the destination lines; the caller's rows are 4 mod 16 aligned, so the
+// head and tail go through ordinary stores).
+static void stream_copy(uint8_t *dst, const uint8_t *src, size_t len) {
+    size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+    if (head > len) head = len;
+    memcpy(dst, src, head);
+    size_t i = head;
+    for (; i + 16 <= len; i += 16)
+        _mm_stream_si128(reinterpret_cast<__m128i *>(dst + i),
+                         _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + i)));
+    memcpy(dst + i, src + i, len - i);
+}
+
+// rows r0 .. r1 - 1; rows0 = the (count, ids) row of r0.  Rows are built in
+// a small (L1/L2-resident) bounce buffer, eight at a time, then streamed out.
+static void assemble_range(uint8_t *blocks, int64_t r0, int64_t r1, int64_t stride, int cap,
+                           int m, const int32_t *rows0, const uint8_t *codes, int64_t ncodes) {
+    static const uint8_t zero[128 + 16] = {0};
+    constexpr int kGroup = 8;
+    const int nb = (cap + 15) / 16;
+    const int m16 = m & ~15;
+    std::vector<uint8_t> bounce((size_t)kGroup * stride);
+    for (int64_t g0 = r0; g0 < r1; g0 += kGroup) {
+        const int64_t g1 = std::min<int64_t>(r1, g0 + kGroup);
+        for (int64_t r = g0; r < g1; ++r) {
+            const int32_t *pr = rows0 + (r - r0) * (1 + (int64_t)cap);
+            uint8_t *b = bounce.data() + (r - g0) * stride;
+            memcpy(b, pr, 4 * (size_t)(1 + cap));
+            const int cnt = std::min(std::max(pr[0], 0), cap);
+            uint8_t *region = b + 4 + 4 * (size_t)cap;
+            uint8_t *region_end = b + stride;
+            for (int bt = 0; bt < nb; ++bt) {
+                const uint8_t *src[16];
+                for (int ln = 0; ln < 16; ++ln) {
+                    const int slot = bt * 16 + ln;
+                    const int u = slot < cnt ? pr[1 + slot] : -1;
+                    src[ln] = (u >= 0 && u < ncodes) ? codes + (size_t)u * m : zero;
+                }
+                uint8_t *out = region + (size_t)bt * m * 16;
+                for (int i0 = 0; i0 < m16; i0 += 16) {
+                    __m128i t[16];
+                    for (int ln = 0; ln < 16; ++ln)
+                        t[ln] = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src[ln] + i0));
+                    transpose16(t);
+                    for (int k = 0; k < 16; ++k)
+                        _mm_storeu_si128(reinterpret_cast<__m128i *>(out + (size_t)(i0 + k) * 16),
+                                         t[k]);
+                }
+                for (int i = m16; i < m; ++i)
+                    for (int ln = 0; ln < 16; ++ln) out[(size_t)i * 16 + ln] = src[ln][i];
+            }
+            // bytes past the code region (a caller's wider stride) stay zero
+            uint8_t *used = region + (size_t)nb * m * 16;
+            if (used < region_end) memset(used, 0, (size_t)(region_end - used));
+        }
+        stream_copy(blocks + g0 * stride, bounce.data(), (size_t)(g1 - g0) * stride);
+    }
+    _mm_sfence();
+}
+
+// Device (count, ids) rows -> host reference blocks: each staging worker
+// copies a chunk of rows into its pinned buffer and assembles those rows'
+// blocks straight into the caller's array (all host cores).
+static int staged_assemble(uint8_t *blocks, int64_t rows, int64_t stride, int cap, int m,
+                           const int32_t *dev_rows, const uint8_t *codes, int64_t ncodes) {
+    if (rows == 0) return FA_OK;
+    const size_t rb = 4 * (size_t)(1 + cap);
+    const size_t per = std::max<size_t>(1, std::min<size_t>(stage_bytes() / rb, 16384));
+    const size_t nchunk = ((size_t)rows + per - 1) / per;
+    const int T = std::max(stage_workers(), std::min(32, (int)std::thread::hardware_concurrency()));
+    return stage_run(
+        nchunk, "block assembly",
+        [&](size_t c, uint8_t *buf, cudaStream_t s) {
+            const size_t r0 = c * per, r1 = std::min<size_t>((size_t)rows, r0 + per);
+            cudaError_t e = cudaMemcpyAsync(buf, reinterpret_cast<const uint8_t *>(dev_rows) + r0 * rb,
+                                            (r1 - r0) * rb, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e == cudaSuccess)
+                assemble_range(blocks, (int64_t)r0, (int64_t)r1, stride, cap, m,
+                               reinterpret_cast<const int32_t *>(buf), codes, ncodes);
+            return e;
+        },
+        T);
+}
+
 struct IndexGuard {
     fa_index *ix = nullptr;
     ~IndexGuard() { fa_index_destroy(ix); }
@@ -204,6 +320,26 @@ using namespace fa;
 
 extern "C" const char *fa_last_error(void) { return g_err; }
 extern "C" int fa_version(void) { return 1; }
+
+extern "C" int fa_assemble_blocks(uint8_t *blocks, int64_t rows, int64_t stride, int cap, int m,
+                                  const int32_t *id_rows, const uint8_t *codes, int64_t ncodes) {
+    FA_CHECK_ARG(rows >= 0 && cap >= 1 && m >= 0 && m <= 128, "bad block arguments");
+    FA_CHECK_ARG(stride >= 4 + 4 * (int64_t)cap + (int64_t)((cap + 15) / 16) * m * 16,
+                 "block stride too small");
+    if (rows == 0) return FA_OK;
+    const int T = (int)std::min<int64_t>(
+        std::max(1, std::min(32, (int)std::thread::hardware_concurrency())),
+        (rows + 4095) / 4096);
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([=]() {
+            const int64_t r0 = rows * t / T, r1 = rows * (t + 1) / T;
+            assemble_range(blocks, r0, r1, stride, cap, m, id_rows + r0 * (1 + (int64_t)cap), codes,
+                           ncodes);
+        });
+    for (auto &x : th) x.join();
+    return FA_OK;
+}
 
 // FLASHANN_B200_TIMING=1: per-phase wall times of the host drop-ins on stderr
 struct PhaseTimer {
@@ -270,16 +406,19 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     const uint8_t *dcodes = fa_index_codes(guard.ix, &cs);
     FA_CUDA(cudaMemcpy2D(codes, m, dcodes, cs, m, n, cudaMemcpyDeviceToHost));
     tm.mark("codes D2H");
-    FA_TRY(dbase.alloc((size_t)n * base_stride));
-    FA_TRY(dupper.alloc((size_t)n_upper_rows * upper_stride));
-    FA_TRY(fa_index_export_blocks(guard.ix, dbase.as<uint8_t>(), base_stride, dupper.as<uint8_t>(),
-                                  upper_stride, nullptr));
+    // the graph leaves as (count, ids) rows; the blocks' inline code batches
+    // are written on the host from codes[] (just read back above)
+    const int cap0 = 2 * R;
+    FA_TRY(dbase.alloc((size_t)n * 4 * (1 + cap0)));
+    FA_TRY(dupper.alloc((size_t)n_upper_rows * 4 * (1 + R)));
+    FA_TRY(fa_index_export_rows(guard.ix, dbase.as<int32_t>(), dupper.as<int32_t>(), nullptr));
     FA_CUDA(cudaDeviceSynchronize());
-    tm.mark("export");
-    FA_TRY(staged_copy(base_blocks, dbase.p, (size_t)n * base_stride, true));
+    tm.mark("export rows");
+    FA_TRY(staged_assemble(base_blocks, n, base_stride, cap0, m, dbase.as<int32_t>(), codes, n));
     if (n_upper_rows)
-        FA_TRY(staged_copy(upper_blocks, dupper.p, (size_t)n_upper_rows * upper_stride, true));
-    tm.mark("blocks D2H");
+        FA_TRY(staged_assemble(upper_blocks, n_upper_rows, upper_stride, R, m,
+                               dupper.as<int32_t>(), codes, n));
+    tm.mark("rows D2H + block assembly");
     return FA_OK;
 }
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "kernels.cuh"
@@ -30,7 +31,6 @@ struct fa_index {
     uint8_t *dist0 = nullptr, *distU = nullptr;  // prune-distance caches
     int32_t *upper_owner = nullptr;
     uint32_t *gvis = nullptr, *gvis_epoch = nullptr;  // global visited tier
-    int32_t *order_h = nullptr;  // pinned: the build's per-batch processing order
     int search_tie = 0;
     int64_t entry = -1;
     int max_layer = -1;
@@ -39,6 +39,30 @@ struct fa_index {
 namespace fa {
 
 static int dev_alloc(void **p, size_t bytes) { return pool_alloc(p, bytes); }
+
+// The build's per-batch processing order goes up from one process-wide pinned
+// buffer (grown on demand, never freed: pinning and unpinning cost more than
+// the buffer).  Builds are serialised on it.
+static std::mutex g_order_mu;
+static int32_t *g_order_h = nullptr;
+static int64_t g_order_cap = 0;
+static int pinned_order(int64_t n, int32_t **out) {
+    if (n > g_order_cap) {
+        if (g_order_h) cudaFreeHost(g_order_h);
+        g_order_h = nullptr;
+        g_order_cap = 0;
+        cudaError_t e = cudaHostAlloc((void **)&g_order_h, sizeof(int32_t) * (size_t)n,
+                                      cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            g_order_h = nullptr;
+            set_error("cudaHostAlloc(order): %s", cudaGetErrorString(e));
+            return FA_ENOMEM;
+        }
+        g_order_cap = n;
+    }
+    *out = g_order_h;
+    return FA_OK;
+}
 
 __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -321,7 +345,6 @@ extern "C" int fa_index_destroy(fa_index *ix) {
                     (void *)ix->distU, (void *)ix->upper_owner, (void *)ix->gvis,
                     (void *)ix->gvis_epoch})
         pool_free(p);
-    cudaFreeHost(ix->order_h);
     delete ix;
     return FA_OK;
 }
@@ -577,15 +600,11 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // changes no result, only the length of the batch's tail.  Filled per
     // batch in the launch loop (pinned buffer, async copy): the host work
     // overlaps the device's earlier batches.
-    if (!ix->order_h) {
-        cudaError_t e = cudaHostAlloc((void **)&ix->order_h, sizeof(int32_t) * g.n,
-                                      cudaHostAllocDefault);
-        if (e != cudaSuccess) {
-            ix->order_h = nullptr;
-            set_error("cudaHostAlloc(order): %s", cudaGetErrorString(e));
-            cleanup();
-            return FA_ENOMEM;
-        }
+    int32_t *order_h = nullptr;
+    std::unique_lock<std::mutex> order_lock(g_order_mu);  // held to the final sync
+    if ((rc = pinned_order(g.n, &order_h))) {
+        cleanup();
+        return rc;
     }
     int maxlv = 0;
     for (int64_t v = 0; v < g.n; ++v) maxlv = std::max(maxlv, ix->levels_h[v]);
@@ -617,7 +636,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
         {  // stable counting sort of the batch by level, descending
-            int32_t *o = ix->order_h + b.start;
+            int32_t *o = order_h + b.start;
             const int32_t *lv = ix->levels_h.data() + b.start;
             std::fill(lvpos.begin(), lvpos.end(), 0);
             for (int k = 0; k < b.size; ++k) ++lvpos[maxlv - lv[k] + 1];
@@ -867,6 +886,24 @@ extern "C" int fa_index_export_blocks(fa_index *ix, uint8_t *base_blocks, int64_
         FA_CHECK_ARG(upper_blocks && upper_stride >= 4 + 4 * g.capU + nbU * g.m * 16,
                      "upper stride too small");
         FA_TRY(launch_export(g, g.nU, true, upper_blocks, upper_stride, g.capU, g.capUp, st));
+    }
+    return FA_OK;
+}
+
+extern "C" int fa_index_export_rows(fa_index *ix, int32_t *base_rows, int32_t *upper_rows,
+                                    void *stream) {
+    FA_CHECK_ARG(ix, "null index");
+    Graph g = ix->g;
+    g.m = 0;  // count + ids only
+    g.mpad = 0;
+    cudaStream_t st = as_stream(stream);
+    if (g.n)
+        FA_TRY(launch_export(g, g.n, false, reinterpret_cast<uint8_t *>(base_rows),
+                             4 + 4 * (int64_t)g.cap0, g.cap0, g.cap0p, st));
+    if (g.nU) {
+        FA_CHECK_ARG(upper_rows, "upper rows needed");
+        FA_TRY(launch_export(g, g.nU, true, reinterpret_cast<uint8_t *>(upper_rows),
+                             4 + 4 * (int64_t)g.capU, g.capU, g.capUp, st));
     }
     return FA_OK;
 }
