@@ -48,7 +48,7 @@ constexpr int kNumSMs = 148;  // B200; grids use num_sms() (the device's own cou
 // ---- device memory from the stream-ordered pool -----------------------------
 // The core's device buffers (index arrays, host drop-in staging targets,
 // build scratch) come from the device's default memory pool with its release
-// threshold raised, so the repeated create/free of the host drop-ins reuses
+// threshold raised (to a quarter of the device), so the repeated create/free of the host drop-ins reuses
 // mapped memory instead of paying cudaMalloc / cudaFree (which unmap and
 // synchronise) on every call.  Allocation and free are ordered on the legacy
 // default stream; pool_alloc waits for that stream so the buffer is usable on
@@ -58,8 +58,13 @@ inline void keep_pool() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || ((done >> dev) & 1ull)) return;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = ~0ull;
+    size_t free_b = 0, total_b = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+        cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        // keep up to a quarter of the device mapped between calls; anything
+        // above goes back at the next synchronisation (other allocators, e.g.
+        // PyTorch's, cannot use memory parked in this pool)
+        uint64_t keep = (uint64_t)total_b / 4;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     done |= 1ull << dev;
