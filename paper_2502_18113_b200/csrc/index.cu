@@ -25,6 +25,10 @@ struct fa_index {
     int cap0, capU;
     std::vector<int32_t> levels_h;
     std::vector<int64_t> uoff_h;
+    // derived once from levels_h (immutable): prefix sums of the levels and
+    // the record positions (a level above every earlier one: a new top layer)
+    std::vector<int64_t> lvl_prefix;
+    std::vector<int64_t> raisers;
     uint8_t *codes = nullptr;
     int32_t *adj0 = nullptr, *cnt0 = nullptr, *adjU = nullptr, *cntU = nullptr;
     uint8_t *cons0 = nullptr, *consU = nullptr;
@@ -40,27 +44,33 @@ namespace fa {
 
 static int dev_alloc(void **p, size_t bytes) { return pool_alloc(p, bytes); }
 
-// The build's per-batch processing order goes up from one process-wide pinned
-// buffer (grown on demand, never freed: pinning and unpinning cost more than
-// the buffer).  Builds are serialised on it.
+// The build's per-batch processing order and request offsets go up from
+// process-wide pinned buffers (grown on demand, never freed: pinning and
+// unpinning cost more than the buffers).  Builds are serialised on them.
 static std::mutex g_order_mu;
 static int32_t *g_order_h = nullptr;
+static int64_t *g_reqoff_h = nullptr;
 static int64_t g_order_cap = 0;
-static int pinned_order(int64_t n, int32_t **out) {
+static int pinned_order(int64_t n, int32_t **order, int64_t **reqoff) {
     if (n > g_order_cap) {
         if (g_order_h) cudaFreeHost(g_order_h);
+        if (g_reqoff_h) cudaFreeHost(g_reqoff_h);
         g_order_h = nullptr;
+        g_reqoff_h = nullptr;
         g_order_cap = 0;
         cudaError_t e = cudaHostAlloc((void **)&g_order_h, sizeof(int32_t) * (size_t)n,
                                       cudaHostAllocDefault);
+        if (e == cudaSuccess)
+            e = cudaHostAlloc((void **)&g_reqoff_h, sizeof(int64_t) * (size_t)n,
+                              cudaHostAllocDefault);
         if (e != cudaSuccess) {
-            g_order_h = nullptr;
-            set_error("cudaHostAlloc(order): %s", cudaGetErrorString(e));
+            set_error("cudaHostAlloc(build order): %s", cudaGetErrorString(e));
             return FA_ENOMEM;
         }
         g_order_cap = n;
     }
-    *out = g_order_h;
+    *order = g_order_h;
+    *reqoff = g_reqoff_h;
     return FA_OK;
 }
 
@@ -237,6 +247,7 @@ __global__ void import_kernel(Graph g, int64_t rows, bool upper, const uint8_t *
 struct Batch {
     int start, size, ep, ml;
     int64_t nreq;
+    bool raiser;  // a vertex that opens a new top layer, inserted alone
 };
 
 }  // namespace fa
@@ -429,41 +440,54 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int prefix = opts->seq_prefix >= 0 ? opts->seq_prefix : 256;
 
     // ---- schedule (pure function of the layer draws) ----
+    // O(batches) from the level prefix sums and the record positions; the
+    // per-vertex request offsets are written per batch in the launch loop.
+    if ((int64_t)ix->lvl_prefix.size() != g.n + 1) {
+        ix->lvl_prefix.assign(g.n + 1, 0);
+        ix->raisers.clear();
+        int run = -1;
+        for (int64_t v = 0; v < g.n; ++v) {
+            const int lv = ix->levels_h[v];
+            ix->lvl_prefix[v + 1] = ix->lvl_prefix[v] + lv;
+            if (lv > run) {
+                if (v > 0) ix->raisers.push_back(v);
+                run = lv;
+            }
+        }
+    }
     std::vector<Batch> batches;
-    std::vector<int64_t> req_off(g.n, 0);
     int ep = 0, ml = ix->levels_h[0];
     int64_t maxreq = 0;
     int maxB = 1;
     int64_t x = 1;
+    size_t ri = 0;  // next record position at or after x
     while (x < g.n) {
+        while (ri < ix->raisers.size() && ix->raisers[ri] < x) ++ri;
         Batch b;
         b.start = (int)x;
         b.ep = ep;
         b.ml = ml;
-        int B;
-        if (ix->levels_h[x] > ml) B = 1;
-        else if (x < prefix) B = 1;
-        else B = std::max(1, std::min(Bmax, (int)(frac * (double)x)));
-        int64_t off = 0;
-        int size = 0;
-        while (size < B && x < g.n) {
-            int lv = ix->levels_h[x];
-            if (size > 0 && lv > ml) break;
-            req_off[x] = off;
-            off += (int64_t)(std::min(ml, lv) + 1) * R;
-            ++size;
-            ++x;
-            if (lv > ml) break;  // a new top layer goes alone
+        const bool raiser = ri < ix->raisers.size() && ix->raisers[ri] == x;
+        int size;
+        if (raiser) {
+            size = 1;  // a new top layer goes alone
+            b.nreq = (int64_t)(ml + 1) * R;
+        } else {
+            const int B = x < prefix ? 1 : std::max(1, std::min(Bmax, (int)(frac * (double)x)));
+            int64_t end = std::min<int64_t>(g.n, x + B);
+            if (ri < ix->raisers.size()) end = std::min<int64_t>(end, ix->raisers[ri]);
+            size = (int)(end - x);
+            b.nreq = (int64_t)R * (size + (ix->lvl_prefix[end] - ix->lvl_prefix[x]));
         }
         b.size = size;
-        b.nreq = off;
+        b.raiser = raiser;
         batches.push_back(b);
-        maxreq = std::max(maxreq, off);
+        maxreq = std::max(maxreq, b.nreq);
         maxB = std::max(maxB, size);
-        int last = b.start + size - 1;
-        if (ix->levels_h[last] > ml) {
-            ep = last;
-            ml = ix->levels_h[last];
+        x += size;
+        if (raiser) {
+            ep = b.start;
+            ml = ix->levels_h[b.start];
         }
     }
 
@@ -591,8 +615,6 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         FA_BUILD_CUDA(cudaGetLastError());
     }
     FA_BUILD_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-    FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d, req_off.data(), sizeof(int64_t) * g.n,
-                                  cudaMemcpyHostToDevice, st));
     // processing order inside each batch: higher levels first (their searches
     // are the longest: hill climb plus one beam search per layer), ties in
     // vertex order.  Every vertex of a batch sees the graph as of the batch
@@ -601,8 +623,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // batch in the launch loop (pinned buffer, async copy): the host work
     // overlaps the device's earlier batches.
     int32_t *order_h = nullptr;
+    int64_t *reqoff_h = nullptr;
     std::unique_lock<std::mutex> order_lock(g_order_mu);  // held to the final sync
-    if ((rc = pinned_order(g.n, &order_h))) {
+    if ((rc = pinned_order(g.n, &order_h, &reqoff_h))) {
         cleanup();
         return rc;
     }
@@ -643,6 +666,15 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             for (int l = 1; l <= maxlv + 1; ++l) lvpos[l] += lvpos[l - 1];
             for (int k = 0; k < b.size; ++k) o[lvpos[maxlv - lv[k]]++] = k;
             FA_BUILD_CUDA(cudaMemcpyAsync(order_d + b.start, o, sizeof(int32_t) * b.size,
+                                          cudaMemcpyHostToDevice, st));
+            // request slots: (min(ml, level) + 1) R per vertex, in vertex order
+            int64_t *ro = reqoff_h + b.start;
+            int64_t off = 0;
+            for (int k = 0; k < b.size; ++k) {
+                ro[k] = off;
+                off += (int64_t)(std::min(b.ml, lv[k]) + 1) * R;
+            }
+            FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d + b.start, ro, sizeof(int64_t) * b.size,
                                           cudaMemcpyHostToDevice, st));
         }
         // nheads[0]: reverse row heads, nheads[1]: the search's work counter
