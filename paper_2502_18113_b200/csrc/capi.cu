@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <emmintrin.h>
 #include <chrono>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -183,6 +184,57 @@ struct AsyncUpload {
         if (!joined) th.join();
     }
 };
+// Two staged host-to-device copies in sequence on one helper thread: the
+// first part (rows the build needs at once), then the rest (rows it needs
+// later).  wait_first() blocks until the first part is on the device.
+struct TwoPartUpload {
+    int rc1 = FA_OK, rc2 = FA_OK;
+    char err[sizeof(g_err)] = "";
+    bool done1 = false, joined = false;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::thread th;
+    TwoPartUpload(const void *src, void *dst, size_t first, size_t total) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        th = std::thread([this, src, dst, first, total, dev]() {
+            int r = cudaSetDevice(dev) == cudaSuccess
+                        ? staged_copy(const_cast<void *>(src), dst, first, false)
+                        : FA_ECUDA;
+            if (r != FA_OK) snprintf(err, sizeof(err), "%s", g_err);
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                rc1 = r;
+                done1 = true;
+            }
+            cv.notify_all();
+            if (r == FA_OK && total > first) {
+                rc2 = staged_copy(static_cast<uint8_t *>(const_cast<void *>(src)) + first,
+                                  static_cast<uint8_t *>(dst) + first, total - first, false);
+                if (rc2 != FA_OK) snprintf(err, sizeof(err), "%s", g_err);
+            }
+        });
+    }
+    int wait_first() {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [this] { return done1; });
+        if (rc1 != FA_OK) set_error("%s", err);
+        return rc1;
+    }
+    int join() {
+        if (!joined) {
+            th.join();
+            joined = true;
+        }
+        const int rc = rc1 != FA_OK ? rc1 : rc2;
+        if (rc != FA_OK) set_error("%s", err);
+        return rc;
+    }
+    ~TwoPartUpload() {
+        if (!joined) th.join();
+    }
+};
+
 // FA_TRY that first waits for an in-flight AsyncUpload (its buffers must
 // outlive it)
 #define FA_TRY_JOIN(up, call)      \
@@ -309,6 +361,15 @@ static int staged_assemble(uint8_t *blocks, int64_t rows, int64_t stride, int ca
         T);
 }
 
+// rows of the projected vectors uploaded before the build starts (the batch
+// schedule reaches them after ~60 batches: 0.2 x inserted per batch);
+// FLASHANN_B200_EARLY_ROWS overrides (tests)
+static int64_t early_rows() {
+    const char *e = getenv("FLASHANN_B200_EARLY_ROWS");
+    const long long v = e ? atoll(e) : 0;
+    return v > 0 ? (int64_t)v : (int64_t)131072;
+}
+
 struct IndexGuard {
     fa_index *ix = nullptr;
     ~IndexGuard() { fa_index_destroy(ix); }
@@ -376,10 +437,14 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     }
     PhaseTimer tm;
     DevBuf dproj_b, dcent, ddims, doffs, dsdt, dlev, duoff, dbase, dupper;
-    // the projected vectors (the one large input) upload on a helper thread
-    // while the model and layer arrays go up and the index is created
+    // the projected vectors (the one large input) upload on a helper thread:
+    // the first rows while the model and layer arrays go up and the index is
+    // created, the rest while the build's first batches run (they read only
+    // the first rows; the build waits for the rest before the first batch
+    // that needs them)
     FA_TRY(dproj_b.alloc(sizeof(float) * n * dproj));
-    AsyncUpload up(proj, dproj_b.p, sizeof(float) * n * dproj);
+    const int64_t early = std::min<int64_t>(n, early_rows());
+    TwoPartUpload up(proj, dproj_b.p, sizeof(float) * early * dproj, sizeof(float) * n * dproj);
     FA_TRY_JOIN(up, dcent.upload(cent, sizeof(float) * (size_t)m * 16 * dmax));
     FA_TRY_JOIN(up, ddims.upload(dims, sizeof(int32_t) * m));
     FA_TRY_JOIN(up, doffs.upload(offs, sizeof(int32_t) * m));
@@ -396,10 +461,16 @@ extern "C" int fa_build_graph_host(int64_t n, int dim, const float *vecs, int dp
     tm.mark("upload model/levels");
     IndexGuard guard;
     FA_TRY_JOIN(up, fa_index_create(&d, &guard.ix));
-    FA_TRY(up.join());
+    FA_TRY_JOIN(up, up.wait_first());
     tm.mark("uploads + index create");
-    FA_TRY(fa_index_encode(guard.ix, nullptr));
-    FA_TRY(fa_index_build(guard.ix, opts, res, nullptr));
+    FA_TRY_JOIN(up, index_encode_rows(guard.ix, 0, early, nullptr));
+    if (early < n)
+        index_set_late_rows(guard.ix, early, [&up, &guard, early, n](cudaStream_t st) {
+            FA_TRY(up.join());
+            return index_encode_rows(guard.ix, early, n, st);
+        });
+    FA_TRY_JOIN(up, fa_index_build(guard.ix, opts, res, nullptr));
+    FA_TRY(up.join());
     tm.mark("encode + build");
     // codes[x] as the compiled core leaves them (prep_qctx overwrite)
     int cs = 0;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <functional>
 #include <string>
 
 #include "../../include/flashann_b200.h"
@@ -83,6 +84,10 @@ inline int pool_alloc(void **p, size_t bytes) {
 inline void pool_free(void *p) {
     if (p) cudaFreeAsync(p, 0);
 }
+
+// Internal (C++) hooks of the index for the host drop-ins (csrc/index.cu).
+int index_encode_rows(fa_index *ix, int64_t r0, int64_t r1, cudaStream_t st);
+void index_set_late_rows(fa_index *ix, int64_t from, std::function<int(cudaStream_t)> hook);
 
 // SM count of the current device (cached per process; B200: 148)
 inline int num_sms() {

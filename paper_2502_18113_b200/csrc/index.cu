@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -29,6 +30,11 @@ struct fa_index {
     // the record positions (a level above every earlier one: a new top layer)
     std::vector<int64_t> lvl_prefix;
     std::vector<int64_t> raisers;
+    // host drop-in: projected rows >= late_from arrive while the build runs;
+    // late_hook (wait for them, encode them) runs before the first batch
+    // that needs them is enqueued
+    int64_t late_from = -1;
+    std::function<int(cudaStream_t)> late_hook;
     uint8_t *codes = nullptr;
     int32_t *adj0 = nullptr, *cnt0 = nullptr, *adjU = nullptr, *cntU = nullptr;
     uint8_t *cons0 = nullptr, *consU = nullptr;
@@ -366,15 +372,27 @@ extern "C" int fa_index_set_search_tie(fa_index *ix, int mode) {
     return FA_OK;
 }
 
+namespace fa {
+// codes of rows [r0, r1) from the projected vectors (K2)
+int index_encode_rows(fa_index *ix, int64_t r0, int64_t r1, cudaStream_t st) {
+    if (ix->g.m == 0 || r1 <= r0) return FA_OK;  // exact kind: no codes
+    FA_CHECK_ARG(ix->d.proj, "index has no projected vectors to encode");
+    const size_t cs = ix->g.mpad;
+    FA_CUDA(cudaMemsetAsync(ix->codes + (size_t)r0 * cs, 0, (size_t)(r1 - r0) * cs, st));
+    return launch_encode_adt(ix->d.proj + (size_t)r0 * ix->d.dproj, r1 - r0, ix->d.dproj,
+                             ix->d.cent, ix->d.dims, ix->d.offs, ix->g.m, ix->d.dmax,
+                             ix->d.dist_min, ix->d.delta, ix->codes + (size_t)r0 * cs,
+                             ix->g.mpad, nullptr, 0, st);
+}
+void index_set_late_rows(fa_index *ix, int64_t from, std::function<int(cudaStream_t)> hook) {
+    ix->late_from = from;
+    ix->late_hook = std::move(hook);
+}
+}  // namespace fa
+
 extern "C" int fa_index_encode(fa_index *ix, void *stream) {
     FA_CHECK_ARG(ix, "null index");
-    if (ix->g.m == 0) return FA_OK;  // exact kind: no codes
-    FA_CHECK_ARG(ix->d.proj, "index has no projected vectors to encode");
-    cudaStream_t st = as_stream(stream);
-    FA_CUDA(cudaMemsetAsync(ix->codes, 0, (size_t)ix->g.n * ix->g.mpad, st));
-    return launch_encode_adt(ix->d.proj, ix->g.n, ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs,
-                             ix->g.m, ix->d.dmax, ix->d.dist_min, ix->d.delta, ix->codes,
-                             ix->g.mpad, nullptr, 0, st);
+    return index_encode_rows(ix, 0, ix->g.n, as_stream(stream));
 }
 
 extern "C" int fa_index_set_codes(fa_index *ix, const uint8_t *codes, int code_stride,
@@ -646,6 +664,15 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     int64_t launches = 3;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
+        if (ix->late_hook && ix->late_from >= 0 && (int64_t)b.start + b.size > ix->late_from) {
+            auto hook = std::move(ix->late_hook);
+            ix->late_hook = nullptr;
+            ix->late_from = -1;
+            if ((rc = hook(st))) {
+                cleanup();
+                return rc;
+            }
+        }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 0], st));
         if (!exact) {
             rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size,

@@ -125,3 +125,23 @@ def test_single_batch_whole_graph(core, model):
     sched = dict(batch_max=1 << 20, batch_frac=1e6, seq_prefix=0)
     res, levels, uoff, base, upper = _build(core, prov, 300, **sched)
     _check_oracle(prov, levels, uoff, base, upper, res, **sched)
+
+
+@pytest.mark.parametrize("early", [1, 37, 299])
+def test_late_projected_rows(core, model, early, monkeypatch):
+    """The host drop-in uploads the projected vectors in two parts and the
+    build waits for the second before the first batch that reads it
+    (FLASHANN_B200_EARLY_ROWS moves the split): blocks, codes and result are
+    byte-identical to a build whose rows all arrived first, and row-exact
+    against the oracle."""
+    data = np.random.default_rng(11).normal(size=(600, 16)).astype(np.float32)
+    _, prov = _arrays(model, data)
+    sched = dict(batch_max=64, batch_frac=0.2, seq_prefix=0)
+    ref = _build(core, dict(prov, codes=prov["codes"].copy()), 600, **sched)
+    monkeypatch.setenv("FLASHANN_B200_EARLY_ROWS", str(early))
+    p2 = dict(prov, codes=prov["codes"].copy())
+    res, levels, uoff, base, upper = _build(core, p2, 600, **sched)
+    assert res["entry_point"] == ref[0]["entry_point"] and res["max_layer"] == ref[0]["max_layer"]
+    assert res["counters"] == ref[0]["counters"]
+    assert np.array_equal(base, ref[3]) and np.array_equal(upper, ref[4])
+    _check_oracle(p2, levels, uoff, base, upper, res, **sched)
