@@ -295,6 +295,7 @@ static void assemble_range(uint8_t *blocks, int64_t r0, int64_t r1, int64_t stri
                            int m, const int32_t *rows0, const uint8_t *codes, int64_t ncodes) {
     static const uint8_t zero[128 + 16] = {0};
     constexpr int kGroup = 8;
+    constexpr int64_t kPrefetch = 4;  // rows
     const int nb = (cap + 15) / 16;
     const int m16 = m & ~15;
     std::vector<uint8_t> bounce((size_t)kGroup * stride);
@@ -302,6 +303,19 @@ static void assemble_range(uint8_t *blocks, int64_t r0, int64_t r1, int64_t stri
         const int64_t g1 = std::min<int64_t>(r1, g0 + kGroup);
         for (int64_t r = g0; r < g1; ++r) {
             const int32_t *pr = rows0 + (r - r0) * (1 + (int64_t)cap);
+            // the code rows of the row kPrefetch ahead: random 64-byte reads
+            // from the n x m table are what bounds this loop
+            if (r + kPrefetch < r1) {
+                const int32_t *pf = pr + kPrefetch * (1 + (int64_t)cap);
+                const int pc = std::min(std::max(pf[0], 0), cap);
+                for (int j = 0; j < pc; ++j) {
+                    const int u = pf[1 + j];
+                    if (u >= 0 && u < ncodes)
+                        for (int l = 0; l < m; l += 64)
+                            _mm_prefetch(reinterpret_cast<const char *>(codes + (size_t)u * m + l),
+                                         _MM_HINT_T0);
+                }
+            }
             uint8_t *b = bounce.data() + (r - g0) * stride;
             memcpy(b, pr, 4 * (size_t)(1 + cap));
             const int cnt = std::min(std::max(pr[0], 0), cap);
