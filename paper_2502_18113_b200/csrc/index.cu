@@ -545,6 +545,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaFuncSetAttribute(rev_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_rev));
 
+    // global select workspace of the reverse kernel's full prunes, per warp
+    const int rev_sel_bytes = exact ? 16 : select_tv_ws_bytes(g.mpad, capmax + 1);
     int rev_per_sm = 0;
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rev_per_sm, rev_fn,
                                                           kReverseWarps * 32, smem_rev));
@@ -564,7 +566,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                      std::min(100, std::max(0, pct))));
     }
 
-    uint8_t *adt_batch = nullptr, *sdtT = nullptr;
+    uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
     int32_t *order_d = nullptr;
@@ -578,7 +580,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
                         (void *)req_off_d, (void *)order_d, (void *)err, cub_tmp, (void *)heads,
                         (void *)nheads,
-                        (void *)next_seg, (void *)sdtT})
+                        (void *)next_seg, (void *)sdtT, (void *)rev_sel})
             if (p) cudaFreeAsync(p, st);
     };
     auto dev_alloc = [&](void **p, size_t bytes) -> int {
@@ -608,6 +610,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&nheads, 2 * sizeof(int))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
         (rc = dev_alloc((void **)&sdtT, sdt_bytes)) ||
+        (rc = dev_alloc((void **)&rev_sel, (size_t)rev_ctas * kReverseWarps * rev_sel_bytes)) ||
         (rc = dev_alloc((void **)&err, sizeof(int)))) {
         cleanup();
         return rc;
@@ -729,11 +732,11 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         else if (rc2)
             reverse_kernel<2><<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
                 gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg,
-                ix->upper_owner, RL, ctr);
+                ix->upper_owner, RL, ctr, rev_sel, rev_sel_bytes);
         else
             reverse_kernel<kRowChunks><<<rgrid, kReverseWarps * 32, smem_rev, st>>>(
                 gb, ix->d.sdt, sdtT, req_sorted, b.nreq, heads, nheads, next_seg,
-                ix->upper_owner, RL, ctr);
+                ix->upper_owner, RL, ctr, rev_sel, rev_sel_bytes);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
         launches += 4;

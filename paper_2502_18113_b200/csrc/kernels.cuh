@@ -90,7 +90,9 @@ struct ReverseLayout {
         keptd = o; o += round_up(capmax, 32);
         cand = o; o += 128 * 8;
         o = round_up(o, 256);
-        sel = o; o += select_tv_bytes(m, mpad, capmax);  // kept ids first
+        // kept ids (the rare full prune's select workspace lives in global
+        // scratch: reverse_kernel's sel_scratch)
+        sel = o; o += round_up(capmax * 4, 256);
         qv = cv = cid = cd = kd = rowd32 = keptd32 = kflag = 0;
         if (dim > 0) {
             qv = o; o += round_up(dim * 4, 16);
@@ -116,7 +118,8 @@ __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,
                                const unsigned long long *__restrict__ keys, int64_t N,
                                const int64_t *__restrict__ heads, const int *__restrict__ nheads,
                                int *__restrict__ next, const int32_t *__restrict__ upper_owner,
-                               ReverseLayout L, unsigned long long *__restrict__ ctr);
+                               ReverseLayout L, unsigned long long *__restrict__ ctr,
+                               uint8_t *__restrict__ sel_scratch, int sel_bytes);
 
 __global__ void reverse_exact_kernel(Graph g, const unsigned long long *__restrict__ keys,
                                      int64_t N, const int64_t *__restrict__ heads,

@@ -60,12 +60,19 @@ __global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys
 }
 
 // RC: row chunks of 32 slots compiled in (cap <= 32 RC)
+// 64 registers: 32 warps per SM (the kernel is latency-bound; its shared
+// workspace is ~3.7 KB per warp once the rare full prune's select workspace
+// lives in global scratch)
+#ifndef FA_REV_MAXNREG
+#define FA_REV_MAXNREG 64
+#endif
 template <int RC>
-__global__ void __maxnreg__(96) reverse_kernel(
+__global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
     Graph g, const uint8_t *__restrict__ sdt, const uint8_t *__restrict__ sdtT,
     const unsigned long long *__restrict__ keys, int64_t N, const int64_t *__restrict__ heads,
     const int *__restrict__ nheads, int *__restrict__ next, const int32_t *__restrict__ upper_owner,
-    ReverseLayout L, unsigned long long *__restrict__ ctr) {
+    ReverseLayout L, unsigned long long *__restrict__ ctr, uint8_t *__restrict__ sel_scratch,
+    int sel_bytes) {
     // sdt, sdtT: the SDT and its transpose in global memory (L1-resident)
     extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
@@ -79,8 +86,9 @@ __global__ void __maxnreg__(96) reverse_kernel(
     uint8_t *rowd_s = base + L.rowd;
     uint8_t *keptd = base + L.keptd;
     unsigned long long *cand = reinterpret_cast<unsigned long long *>(base + L.cand);
-    uint8_t *selws = base + L.sel;
-    int32_t *kept = reinterpret_cast<int32_t *>(selws);  // = warp_select_tv's kept ids
+    int32_t *kept = reinterpret_cast<int32_t *>(base + L.sel);  // fast prune's output
+    // this warp's global select workspace (full prunes: kept ids + codes)
+    uint8_t *selws = sel_scratch + (size_t)(blockIdx.x * (blockDim.x >> 5) + wid) * sel_bytes;
     const int nseg = *nheads;
     unsigned long long n_prune = 0, n_app = 0, n_sym = 0, n_full = 0;
     while (true) {
@@ -159,6 +167,7 @@ __global__ void __maxnreg__(96) reverse_kernel(
             }
             const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
             int nk = 0;
+            const int32_t *kept_src = kept;
             if (cons) {
                 // L = row_s is sorted by (d, id) and pairwise non-dominated, its
                 // distances d(y, L_j) cached in rowd_s.  p = position of x among
@@ -263,12 +272,13 @@ __global__ void __maxnreg__(96) reverse_kernel(
                         v = (int)(k & 0xffffffffu);
                         dv = (uint32_t)(k >> 32);
                     },
-                    selws, lane, &sym, kept_sel, keptd);
+                    selws, lane, &sym, kept_sel, keptd, tkeep);
+                kept_src = kept_sel;
                 n_sym += cap + 1 + sym;
             }
             __syncwarp();
             for (int j = lane; j < cap; j += 32) {
-                row_s[j] = j < nk ? kept[j] : -1;
+                row_s[j] = j < nk ? kept_src[j] : -1;
                 rowd_s[j] = j < nk ? keptd[j] : 0;
             }
             cnt = nk;
@@ -501,11 +511,11 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
 template __global__ void reverse_kernel<2>(Graph, const uint8_t *, const uint8_t *,
                                            const unsigned long long *, int64_t, const int64_t *,
                                            const int *, int *, const int32_t *, ReverseLayout,
-                                           unsigned long long *);
+                                           unsigned long long *, uint8_t *, int);
 template __global__ void reverse_kernel<kRowChunks>(Graph, const uint8_t *, const uint8_t *,
                                                     const unsigned long long *, int64_t,
                                                     const int64_t *, const int *, int *,
                                                     const int32_t *, ReverseLayout,
-                                                    unsigned long long *);
+                                                    unsigned long long *, uint8_t *, int);
 
 }  // namespace fa

@@ -107,6 +107,10 @@ __host__ __device__ inline int select_tv_bytes(int m, int mpad, int cap) {
     return round_up(cap * 4, 256) + round_up(cap * kept_enc_stride(mpad), 256) +
            round_up(mpad * 16, 256);
 }
+// ws bytes of warp_select_tv when Tv lives elsewhere (kept ids + codes)
+__host__ __device__ inline int select_tv_ws_bytes(int mpad, int cap) {
+    return round_up(cap * 4, 256) + round_up(cap * kept_enc_stride(mpad), 256);
+}
 
 // chunk-local row offsets (i % 16) * 16 of the four bytes of code word q
 __device__ __forceinline__ uint32_t kept_enc_add(int q) {
@@ -151,15 +155,20 @@ __device__ __forceinline__ uint32_t row_table_sum(uint32_t tbase, const uint8_t 
     return acc > 255u ? 255u : acc;
 }
 
+// ws: kept ids then the kept rows' pre-offset codes (any memory: shared in
+// the build, per-warp global scratch in the reverse kernel's rare full
+// prune); Tv: the candidate's table, shared memory (256-aligned, mpad x 16),
+// null = right after the kept codes in ws (ws then must be shared).
 template <class Get>
 __device__ int warp_select_tv(const uint8_t *__restrict__ sdtT, int m, int mpad,
                               const uint8_t *__restrict__ codes, int cs, int ncand, int cap,
                               Get get, uint8_t *ws, int lane, unsigned long long *sym_count,
-                              int32_t *&kept_out, uint8_t *kept_d = nullptr) {
+                              int32_t *&kept_out, uint8_t *kept_d = nullptr,
+                              uint8_t *Tv_shared = nullptr) {
     const int ks = kept_enc_stride(mpad);
     int32_t *kept_ids = reinterpret_cast<int32_t *>(ws);
     uint8_t *kenc = ws + round_up(cap * 4, 256);
-    uint8_t *Tv = kenc + round_up(cap * ks, 256);
+    uint8_t *Tv = Tv_shared ? Tv_shared : kenc + round_up(cap * ks, 256);
     kept_out = kept_ids;
     int nk = 0;
     unsigned long long sym = 0;
