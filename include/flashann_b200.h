@@ -100,6 +100,13 @@ int fa_select_dev(const uint8_t *sdt, int m, const uint8_t *codes, int code_stri
                   const int32_t *cand_ids, const double *cand_d, int ncand, int cap,
                   int32_t *out, int32_t *nout, void *stream);
 
+/* select_heur (_core.pyx:388-408) of the exact kind (kind 0; sym_one of
+ * K_EXACT, _core.pyx:179-191): candidate v is kept iff every kept u has
+ * (double) fa_l2sq_f32(u, v) >= cand_d[v]; vecs n x dim device f32.          */
+int fa_select_exact_dev(const float *vecs, int dim, const int32_t *cand_ids,
+                        const double *cand_d, int ncand, int cap, int32_t *out, int32_t *nout,
+                        void *stream);
+
 /* ---- coder training (flashann/kmeans.py, flashann/flash.py:63-107) ------- */
 
 /* State of numpy's PCG64 bit generator (Generator.bit_generator.state). */

@@ -36,6 +36,10 @@
 
 #include "oracle.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 /* ---- numerics ------------------------------------------------------------ */
 
 double or_l2sq_f32(const float *a, const float *b, int d) {
@@ -553,7 +557,6 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
     const int exact = g->kind == 0;
     /* Flash: codes are the fp32-tree codes (prep_qctx overwrite,
      * _core.pyx:493-498); exact: proj holds the vectors themselves */
-    uint8_t *adts = NULL;
     int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
     if (!exact)
         for (int64_t v = 0; v < g->n; ++v)
@@ -565,89 +568,155 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
     int maxB = 1;
     for (int b = 0; b < nb; ++b)
         if (sizes[b] > maxB) maxB = sizes[b];
-    adts = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
-    scratch s;
-    if (scratch_init(&s, g->n, C, capmax)) return -1;
-    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(C + 1));
-    int32_t *cid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
-    uint32_t *cd = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(C + capmax + 2));
-    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
-    uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 2));
+    /* per-thread workspaces: the searches of one batch read only the graph as
+     * of the batch start (no vertex of the batch is reachable before the
+     * reverse phase) and write only their own rows, so they run in parallel;
+     * the requests are sorted afterwards, so the result is thread-count
+     * independent */
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    if (nth < 1) nth = 1;
     int maxlev = 0;
     for (int64_t v = 0; v < g->n; ++v)
         if (g->levels[v] > maxlev) maxlev = g->levels[v];
     size_t reqcap = (size_t)maxB * (size_t)(maxlev + 1) * (size_t)R + 1;
     uint64_t *req = (uint64_t *)malloc(sizeof(uint64_t) * reqcap);
+    size_t *heads = (size_t *)malloc(sizeof(size_t) * reqcap);
+    int32_t *cid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+    uint32_t *cd = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(C + capmax + 2));
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+    uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 2));
+    int failed = 0;
     int ep = 0, ml = g->levels[0];
     or_counters *c = &res->counters;
     for (int b = 0; b < nb; ++b) {
         size_t nreq = 0;
-        int bep = ep, bml = ml;
-        for (int p = 0; p < sizes[b]; ++p) {
-            int x = starts[b] + p;
-            int level = g->levels[x];
-            qctx q = {adts, proj + (size_t)x * dproj};
-            if (!exact) {
-                uint8_t code_tmp[256];
-                or_encode_adt(proj + (size_t)x * dproj, cent, dims, offs, m, dmax, dmin, delta,
-                              code_tmp, adts);
-            }
-            int cur = bep;
-            uint32_t curd = qdist(g, &q, cur);
-            c->dist_comps++;
-            for (int layer = bml; layer > level; --layer)
-                hill_climb_impl(g, &q, layer, &cur, &curd, c);
-            int top = bml < level ? bml : level;
-            for (int layer = top; layer >= 0; --layer) {
-                s.salt = tie_salt(g->tie, (uint32_t)x);
-                int ts = layer_search_impl(g, &s, &q, layer, cur, curd, C, T, c);
-                for (int j = 0; j < ts; ++j) {
-                    cid[j] = (int32_t)(T[j] & 0xffffffffu);
-                    cd[j] = (uint32_t)(T[j] >> 32);
+        const int bep = ep, bml = ml;
+        const int bsize = sizes[b], bstart = starts[b];
+#pragma omp parallel num_threads(bsize > 64 ? nth : 1) reduction(|| : failed)
+        {
+            scratch s;
+            or_counters lc;
+            memset(&lc, 0, sizeof(lc));
+            uint8_t *adt = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
+            uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(C + 1));
+            int32_t *tid_ = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+            uint32_t *td = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(C + capmax + 2));
+            int32_t *tsel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+            if (scratch_init(&s, g->n, C, capmax) || !adt || !T || !tid_ || !td || !tsel) {
+                failed = 1;
+            } else {
+#pragma omp for schedule(dynamic, 16)
+                for (int p = 0; p < bsize; ++p) {
+                    int x = bstart + p;
+                    int level = g->levels[x];
+                    qctx q = {adt, proj + (size_t)x * dproj};
+                    if (!exact) {
+                        uint8_t code_tmp[256];
+                        or_encode_adt(proj + (size_t)x * dproj, cent, dims, offs, m, dmax, dmin,
+                                      delta, code_tmp, adt);
+                    }
+                    int cur = bep;
+                    uint32_t curd = qdist(g, &q, cur);
+                    lc.dist_comps++;
+                    for (int layer = bml; layer > level; --layer)
+                        hill_climb_impl(g, &q, layer, &cur, &curd, &lc);
+                    int top = bml < level ? bml : level;
+                    for (int layer = top; layer >= 0; --layer) {
+                        s.salt = tie_salt(g->tie, (uint32_t)x);
+                        int ts = layer_search_impl(g, &s, &q, layer, cur, curd, C, T, &lc);
+                        for (int j = 0; j < ts; ++j) {
+                            tid_[j] = (int32_t)(T[j] & 0xffffffffu);
+                            td[j] = (uint32_t)(T[j] >> 32);
+                        }
+                        int nsel = select_g(g, sdt, tid_, td, ts, R, tsel, &lc.sym_comps);
+                        int cap = layer == 0 ? g->cap0 : g->capU;
+                        int32_t *row = row_of(g, layer, x);
+                        for (int j = 0; j < cap; ++j) row[j] = j < nsel ? tsel[j] : -1;
+                        *cnt_of(g, layer, x) = nsel;
+                        size_t pos;
+#pragma omp atomic capture
+                        { pos = nreq; nreq += (size_t)nsel; }
+                        for (int j = 0; j < nsel; ++j) {
+                            int y = tsel[j];
+                            uint64_t rowg = layer == 0 ? (uint64_t)y
+                                                       : (uint64_t)(g->n + g->uoff[y] + layer - 1);
+                            req[pos + j] = (rowg << 32) | (uint32_t)x;
+                        }
+                        cur = (int)(T[0] & 0xffffffffu);
+                        curd = (uint32_t)(T[0] >> 32);
+                    }
                 }
-                int nsel = select_g(g, sdt, cid, cd, ts, R, sel, &c->sym_comps);
-                int cap = layer == 0 ? g->cap0 : g->capU;
-                int32_t *row = row_of(g, layer, x);
-                for (int j = 0; j < cap; ++j) row[j] = j < nsel ? sel[j] : -1;
-                *cnt_of(g, layer, x) = nsel;
-                for (int j = 0; j < nsel; ++j) {
-                    int y = sel[j];
-                    uint64_t rowg = layer == 0 ? (uint64_t)y
-                                               : (uint64_t)(g->n + g->uoff[y] + layer - 1);
-                    req[nreq++] = (rowg << 32) | (uint32_t)x;
-                }
-                cur = (int)(T[0] & 0xffffffffu);
-                curd = (uint32_t)(T[0] >> 32);
             }
+#pragma omp critical
+            {
+                c->dist_comps += lc.dist_comps;
+                c->sym_comps += lc.sym_comps;
+                c->kernel_calls += lc.kernel_calls;
+                c->visited += lc.visited;
+            }
+            scratch_free(&s);
+            free(adt); free(T); free(tid_); free(td); free(tsel);
+        }
+        if (failed) break;
+        for (int p = 0; p < bsize; ++p) {
+            int level = g->levels[bstart + p];
             if (level > ml) {
-                ep = x;
+                ep = bstart + p;
                 ml = level;
             }
         }
         /* reverse edges grouped by row, ascending x (the sequential order) */
         qsort(req, nreq, sizeof(uint64_t), cmp_u64);
-        for (size_t t = 0; t < nreq; ++t) {
-            uint64_t rowg = req[t] >> 32;
-            int x = (int)(req[t] & 0xffffffffu);
-            int layer, y;
-            if ((int64_t)rowg < g->n) {
-                layer = 0;
-                y = (int)rowg;
-            } else {
-                int64_t r = (int64_t)rowg - g->n;
-                y = g->upper_owner[r];
-                layer = (int)(r - g->uoff[y]) + 1;
+        /* rows are independent (a reverse update reads the immutable codes and
+         * writes only its own row): groups of one row run in parallel, each in
+         * ascending x */
+        size_t ng = 0;
+        for (size_t t = 0; t < nreq; ++t)
+            if (t == 0 || (req[t] >> 32) != (req[t - 1] >> 32)) heads[ng++] = t;
+        heads[ng] = nreq;
+#pragma omp parallel num_threads(ng > 256 ? nth : 1)
+        {
+            or_counters lc;
+            memset(&lc, 0, sizeof(lc));
+            uint64_t *tp = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(capmax + 2));
+            int32_t *tid_ = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+            uint32_t *td = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(C + capmax + 2));
+            int32_t *tsel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(C + capmax + 2));
+#pragma omp for schedule(dynamic, 64)
+            for (size_t gi = 0; gi < ng; ++gi) {
+                for (size_t t = heads[gi]; t < heads[gi + 1]; ++t) {
+                    uint64_t rowg = req[t] >> 32;
+                    int x = (int)(req[t] & 0xffffffffu);
+                    int layer, y;
+                    if ((int64_t)rowg < g->n) {
+                        layer = 0;
+                        y = (int)rowg;
+                    } else {
+                        int64_t r = (int64_t)rowg - g->n;
+                        y = g->upper_owner[r];
+                        layer = (int)(r - g->uoff[y]) + 1;
+                    }
+                    reverse_add(g, sdt, y, x, layer, tp, tid_, td, tsel, &lc);
+                }
             }
-            reverse_add(g, sdt, y, x, layer, pairs, cid, cd, sel, c);
+#pragma omp critical
+            {
+                c->sym_comps += lc.sym_comps;
+                c->reverse_prunes += lc.reverse_prunes;
+                c->reverse_appends += lc.reverse_appends;
+            }
+            free(tp); free(tid_); free(td); free(tsel);
         }
     }
     res->entry_point = ep;
     res->max_layer = ml;
     res->n_batches = nb;
-    free(starts); free(sizes); free(adts); free(T); free(cid); free(cd); free(sel);
-    free(pairs); free(req);
-    scratch_free(&s);
-    return 0;
+    free(starts); free(sizes); free(cid); free(cd); free(sel);
+    free(pairs); free(req); free(heads);
+    return failed ? -1 : 0;
 }
 
 int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const int32_t *dims,
@@ -656,28 +725,36 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
               int rerank_depth, int64_t *out_ids, double *out_d, or_counters *c) {
     int m = g->m;
     int capmax = g->cap0 > g->capU ? g->cap0 : g->capU;
-    scratch s;
-    if (scratch_init(&s, g->n, ef, capmax)) return -1;
-    uint8_t *adt = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
-    uint8_t code[256];
-    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(ef + 1));
     typedef struct {
         double d;
         int32_t id;
     } pair;
+    int failed = 0;
+    /* queries are independent: one workspace per thread */
+#pragma omp parallel reduction(|| : failed)
+    {
+    scratch s;
+    or_counters lc;
+    memset(&lc, 0, sizeof(lc));
+    uint8_t *adt = (uint8_t *)malloc((size_t)(m > 0 ? m : 1) * 16);
+    uint8_t code[256];
+    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(ef + 1));
     pair *pr = (pair *)malloc(sizeof(pair) * (size_t)(ef + 1));
+    if (scratch_init(&s, g->n, ef, capmax) || !adt || !T || !pr) failed = 1;
+#pragma omp for schedule(dynamic, 8)
     for (int q = 0; q < nq; ++q) {
+        if (failed) continue;
         qctx qc = {adt, queries + (size_t)q * dim};
         if (g->kind != 0)
             or_encode_adt(qproj + (size_t)q * dproj, cent, dims, offs, m, dmax, dmin, delta, code,
                           adt);
         int cur = entry;
         uint32_t curd = qdist(g, &qc, cur);
-        if (c) c->dist_comps++;
+        lc.dist_comps++;
         for (int layer = max_layer; layer > 0; --layer)
-            hill_climb_impl(g, &qc, layer, &cur, &curd, c);
+            hill_climb_impl(g, &qc, layer, &cur, &curd, &lc);
         s.salt = tie_salt(g->tie, (uint32_t)q);
-        int ts = layer_search_impl(g, &s, &qc, 0, cur, curd, ef, T, c);
+        int ts = layer_search_impl(g, &s, &qc, 0, cur, curd, ef, T, &lc);
         int64_t *oi = out_ids + (size_t)q * k;
         double *od = out_d + (size_t)q * k;
         if (rerank_depth > 0) {
@@ -708,7 +785,17 @@ int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const 
             }
         }
     }
+    if (c) {
+#pragma omp critical
+        {
+            c->dist_comps += lc.dist_comps;
+            c->sym_comps += lc.sym_comps;
+            c->kernel_calls += lc.kernel_calls;
+            c->visited += lc.visited;
+        }
+    }
     free(adt); free(T); free(pr);
     scratch_free(&s);
-    return 0;
+    }
+    return failed ? -1 : 0;
 }

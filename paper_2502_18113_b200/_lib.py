@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from .errors import ConfigError, DeviceError
+from .errors import DeviceError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libflashann_b200.so"
 
@@ -65,6 +65,7 @@ _SIGS = {
                                     C.c_int, vp, C.c_int, vp]),
     "fa_sdt_sum_dev": (C.c_int, [vp, C.c_int, vp, i64, vp, i64, i64, vp, vp]),
     "fa_select_dev": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
+    "fa_select_exact_dev": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
     "fa_kmeans_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "fa_kmeans_subsample": (C.c_int, [i64, C.c_int, C.c_int, vp, vp]),
     "fa_assemble_blocks": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, vp, vp, i64]),
@@ -155,8 +156,6 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == FA_EOVERFLOW:
         raise DeviceError(f"capacity overflow: {msg}")
-    if rc == FA_EINVAL:
-        raise ConfigError(msg)
     raise DeviceError(f"CUDA error: {msg}")
 
 

@@ -169,7 +169,7 @@ BuildSearchFn build_search_exact_variant(int W, int cap0) {
     } else {
         FA_BUILD_J(ExactDist, 1, kRowChunks)
     }
-    return nullptr;  // W > kRegSetMax: not served for the exact kind
+    return build_search_kernel<ExactDist, 0, 1, kRowChunks>;  // W > kRegSetMax
 }
 #undef FA_BUILD_J
 

@@ -40,7 +40,7 @@ struct fa_index {
     uint8_t *cons0 = nullptr, *consU = nullptr;
     uint8_t *dist0 = nullptr, *distU = nullptr;  // prune-distance caches
     int32_t *upper_owner = nullptr;
-    uint32_t *gvis = nullptr, *gvis_epoch = nullptr;  // global visited tier
+    uint32_t *gvis = nullptr, *gvis_epoch = nullptr, *gvis_owner = nullptr;  // global visited tier
     int search_tie = 0;
     int64_t entry = -1;
     int max_layer = -1;
@@ -100,35 +100,42 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
     return FA_OK;
 }
 
-// Global visited tier (VisitedSet): one 2^kGlobalHashLog2-entry table per
-// hardware warp slot, allocated on first use; absent for n >= 2^24 (the tier
-// packs ids into 24 bits), where the shared tier alone must suffice.
-__global__ void nsmid_kernel(uint32_t *out) {
-    uint32_t v;
-    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
-    *out = v;
-}
-
-static int ensure_gvis(fa_index *ix) {
-    if (ix->gvis || ix->g.n >= (1ll << 24) - 1) return FA_OK;
-    // warp slots are indexed by %smid, which is not dense on parts with fused-off
-    // SMs: size by %nsmid (an upper bound of %smid), not by the SM count
-    uint32_t *d_ns = nullptr, nsmid = 0;
-    FA_TRY(dev_alloc((void **)&d_ns, sizeof(uint32_t)));
-    nsmid_kernel<<<1, 1>>>(d_ns);
-    cudaError_t e = cudaMemcpy(&nsmid, d_ns, sizeof(uint32_t), cudaMemcpyDeviceToHost);
-    pool_free(d_ns);
-    if (e != cudaSuccess) {
-        set_error("reading %%nsmid: %s", cudaGetErrorString(e));
-        return FA_ECUDA;
-    }
-    const size_t slots = (size_t)nsmid * kMaxWarpsPerSM;
-    FA_TRY(dev_alloc((void **)&ix->gvis, (slots << kGlobalHashLog2) * sizeof(uint32_t)));
-    FA_TRY(dev_alloc((void **)&ix->gvis_epoch, slots * sizeof(uint32_t)));
-    FA_CUDA(cudaMemset(ix->gvis, 0, (slots << kGlobalHashLog2) * sizeof(uint32_t)));
-    FA_CUDA(cudaMemset(ix->gvis_epoch, 0, slots * sizeof(uint32_t)));
+// Global visited tier (VisitedSet): a pool of tables claimed per search.  The
+// pool holds one slot per warp the launch can keep resident (occupancy x SMs)
+// and each table 2^gvis_log2_for(W) entries; it grows on demand (reallocated
+// only when a launch needs more slots or a wider table).  Absent for n >= 2^24
+// (the tier packs ids into 24 bits), where the shared tier alone must suffice.
+static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t smem, int W) {
+    if (ix->g.n >= (1ll << 24) - 1) return FA_OK;
+    int dev = 0, nsm = 0, per_sm = 0;
+    FA_CUDA(cudaGetDevice(&dev));
+    FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    const int slots = std::max(1, nsm * std::max(per_sm, 1) * (threads / 32));
+    const int capmax = std::max(ix->g.cap0, ix->g.capU);
+    const int l2 = gvis_log2_for(W, capmax, ix->g.n);
+    if (ix->gvis && slots <= ix->g.gvis_nslots && l2 <= ix->g.gvis_log2) return FA_OK;
+    // grow to cover both this launch and earlier ones
+    const int ns = std::max(slots, ix->gvis ? ix->g.gvis_nslots : 0);
+    const int lg = std::max(l2, ix->gvis ? ix->g.gvis_log2 : 0);
+    FA_CUDA(cudaDeviceSynchronize());  // no search may still hold the old pool
+    pool_free(ix->gvis);
+    pool_free(ix->gvis_epoch);
+    pool_free(ix->gvis_owner);
+    ix->gvis = ix->gvis_epoch = ix->gvis_owner = nullptr;
+    ix->g.gvis = ix->g.gvis_epoch = ix->g.gvis_owner = nullptr;
+    const size_t tab = ((size_t)ns << lg) * sizeof(uint32_t);
+    FA_TRY(dev_alloc((void **)&ix->gvis, tab));
+    FA_TRY(dev_alloc((void **)&ix->gvis_epoch, (size_t)ns * sizeof(uint32_t)));
+    FA_TRY(dev_alloc((void **)&ix->gvis_owner, (size_t)ns * sizeof(uint32_t)));
+    FA_CUDA(cudaMemset(ix->gvis, 0, tab));
+    FA_CUDA(cudaMemset(ix->gvis_epoch, 0, (size_t)ns * sizeof(uint32_t)));
+    FA_CUDA(cudaMemset(ix->gvis_owner, 0, (size_t)ns * sizeof(uint32_t)));
     ix->g.gvis = ix->gvis;
     ix->g.gvis_epoch = ix->gvis_epoch;
+    ix->g.gvis_owner = ix->gvis_owner;
+    ix->g.gvis_nslots = ns;
+    ix->g.gvis_log2 = lg;
     return FA_OK;
 }
 
@@ -311,6 +318,9 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.expand = 1;
     g.gvis = nullptr;
     g.gvis_epoch = nullptr;
+    g.gvis_owner = nullptr;
+    g.gvis_log2 = 14;
+    g.gvis_nslots = 0;
     // host copies of the layer draws drive the batch schedule
     ix->levels_h.resize(g.n);
     ix->uoff_h.resize(g.n);
@@ -360,7 +370,7 @@ extern "C" int fa_index_destroy(fa_index *ix) {
     for (void *p : {(void *)ix->codes, (void *)ix->adj0, (void *)ix->cnt0, (void *)ix->cons0,
                     (void *)ix->adjU, (void *)ix->cntU, (void *)ix->consU, (void *)ix->dist0,
                     (void *)ix->distU, (void *)ix->upper_owner, (void *)ix->gvis,
-                    (void *)ix->gvis_epoch})
+                    (void *)ix->gvis_epoch, (void *)ix->gvis_owner})
         pool_free(p);
     delete ix;
     return FA_OK;
@@ -435,14 +445,12 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CHECK_ARG(C >= 1 && C <= 2048, "C=%d outside [1,2048]", C);
     const bool exact = g.m == 0;  // kind 0: fp32 L2 everywhere
     FA_CHECK_ARG(exact || ix->d.sdt, "index has no SDT");
-    FA_CHECK_ARG(!exact || C <= kRegSetMax, "the exact kind serves C <= %d", kRegSetMax);
     cudaStream_t st = as_stream(stream);
     memset(res, 0, sizeof(*res));
     res->entry_point = -1;
     res->max_layer = -1;
     const auto t_host0 = std::chrono::steady_clock::now();
     FA_TRY(reset_graph(ix, st));
-    FA_TRY(ensure_gvis(ix));
     FA_CHECK_ARG(opts->tie >= 0 && opts->tie <= 2, "tie mode must be 0, 1 or 2");
     Graph gb = g;  // the build's view: its own tie order
     gb.tie = opts->tie;
@@ -565,6 +573,12 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                      cudaFuncAttributePreferredSharedMemoryCarveout,
                                      std::min(100, std::max(0, pct))));
     }
+    FA_TRY(ensure_gvis(ix, (const void *)search_fn, kSearchWarps * 32, smem_search, C));
+    gb.gvis = g.gvis;
+    gb.gvis_epoch = g.gvis_epoch;
+    gb.gvis_owner = g.gvis_owner;
+    gb.gvis_log2 = g.gvis_log2;
+    gb.gvis_nslots = g.gvis_nslots;
 
     uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
@@ -771,7 +785,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
 #undef FA_BUILD_CUDA
     cleanup();
     if (herr) {
-        set_error("visited hash overflow (2^%d entries per warp): raise hash_log2", L.hash_log2);
+        set_error("visited-set overflow: an insertion search (C=%d) visited more vertices than "
+                  "its 2^%d-entry global table holds", C, g.gvis_log2);
         return FA_EOVERFLOW;
     }
     ix->entry = ep;
@@ -815,11 +830,9 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     FA_CHECK_ARG(rerank_depth == 0 || (ix->d.vecs && queries), "rerank needs vectors and queries");
     const bool exact = ix->g.m == 0;
     FA_CHECK_ARG(!exact || queries, "the exact kind searches with the query vectors");
-    FA_CHECK_ARG(!exact || ef <= kRegSetMax, "the exact kind serves ef <= %d", kRegSetMax);
     cudaStream_t st = as_stream(stream);
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
-    FA_TRY(ensure_gvis(ix));
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
     L.init(ix->g.mpad, ef, capmax,
@@ -831,6 +844,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     const QuerySearchFn qfn = query_search_variant(ef, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
+    FA_TRY(ensure_gvis(ix, (const void *)qfn, kSearchWarps * 32, smem, ef));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
@@ -863,7 +877,8 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     pool_free(err);
     if (rc) return rc;
     if (herr) {
-        set_error("visited hash overflow in query search (ef=%d)", ef);
+        set_error("visited-set overflow in query search (ef=%d, table 2^%d)", ef,
+                  ix->g.gvis_log2);
         return FA_EOVERFLOW;
     }
     if (counters)
@@ -881,10 +896,8 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     cudaStream_t st = as_stream(stream);
     if (counters) memset(counters, 0, 4 * sizeof(int64_t));
     if (nq == 0) return FA_OK;
-    FA_TRY(ensure_gvis(ix));
     // exact kind: qproj holds the query vectors (dim floats per row)
     const bool exact = ix->g.m == 0;
-    FA_CHECK_ARG(!exact || width <= kRegSetMax, "the exact kind serves width <= %d", kRegSetMax);
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
     L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1, false,
@@ -894,6 +907,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     const LayerSearchFn lfn = layer_search_variant(width, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
+    FA_TRY(ensure_gvis(ix, (const void *)lfn, kSearchWarps * 32, smem, width));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
@@ -926,7 +940,8 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     pool_free(err);
     if (rc) return rc;
     if (herr) {
-        set_error("visited hash overflow in layer search (width=%d)", width);
+        set_error("visited-set overflow in layer search (width=%d, table 2^%d)", width,
+                  ix->g.gvis_log2);
         return FA_EOVERFLOW;
     }
     if (counters)

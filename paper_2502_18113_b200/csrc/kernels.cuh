@@ -72,8 +72,8 @@ using LayerSearchFn = void (*)(Graph, const uint8_t *, int, const int64_t *, int
 // Kernel instantiations per result-set variant (set_variant(W)) and, for the
 // build, per expansion width (1 or kMaxExpand).
 BuildSearchFn build_search_variant(int W, int expand, int cap0);
-BuildSearchFn build_search_exact_variant(int W, int cap0);  // null when W > kRegSetMax
-// exact = true: the exact-kind instantiations (null when W > kRegSetMax)
+BuildSearchFn build_search_exact_variant(int W, int cap0);
+// exact = true: the exact-kind instantiations
 QuerySearchFn query_search_variant(int W, bool exact);
 LayerSearchFn layer_search_variant(int W, bool exact);
 

@@ -390,13 +390,15 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
                                                    lane < 8 ? vy : nullptr, g.dim, lane)),
                     0);
                 const unsigned long long kx = ((unsigned long long)dx << 32) | (uint32_t)x;
+                // warp-uniform chunk loop, full-mask ballots (lanes past cap vote false)
                 int p = 0;
-                for (int j = lane; j < cap; j += 32) {
-                    const unsigned long long kj =
-                        ((unsigned long long)rowd[j] << 32) | (uint32_t)row_s[j];
-                    p += __popc(__ballot_sync(__activemask(), kj < kx));
+                for (int c0 = 0; c0 < cap; c0 += 32) {
+                    const int j = c0 + lane;
+                    bool lt = false;
+                    if (j < cap)
+                        lt = (((unsigned long long)rowd[j] << 32) | (uint32_t)row_s[j]) < kx;
+                    p += __popc(__ballot_sync(0xffffffffu, lt));
                 }
-                p = __reduce_max_sync(0xffffffffu, p);  // lanes beyond cap saw no chunk
                 n_sym += cap + 1 + p;
                 // domination of x by a closer member, four at a time
                 bool xkept = true;

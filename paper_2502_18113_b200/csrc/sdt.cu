@@ -46,9 +46,61 @@ __global__ void select_hook_kernel(const uint8_t *__restrict__ sdt, int m, int m
     if (lane == 0) *nout = nk;
 }
 
+// select_heur of the exact kind for the select_neighbors hook: candidate v
+// (distance dv, f64 as given) is kept iff no kept u has (double) fp32 L2(u, v)
+// < dv (_core.pyx:388-408 with sym_one of K_EXACT, _core.pyx:179-191).  One
+// warp; lanes test the kept set in parallel, each with the fa_l2sq_f32 tree.
+__global__ void select_exact_hook_kernel(const float *__restrict__ vecs, int dim,
+                                         const int32_t *__restrict__ cand_ids,
+                                         const double *__restrict__ cand_d, int ncand, int cap,
+                                         int32_t *__restrict__ out, int32_t *__restrict__ nout) {
+    extern __shared__ __align__(16) int32_t kept[];
+    const int lane = threadIdx.x;
+    int nk = 0;
+    for (int j = 0; j < ncand && nk < cap; ++j) {
+        const int v = __ldg(cand_ids + j);
+        const double dv = __ldg(cand_d + j);
+        const float *b = vecs + (size_t)v * dim;
+        bool bad = false;
+        for (int t = lane; t < nk; t += 32) {
+            const float *a = vecs + (size_t)kept[t] * dim;
+            const float s = l2_tree(dim, [&](int i) { return __fsub_rn(__ldg(a + i), __ldg(b + i)); });
+            bad |= (double)s < dv;
+        }
+        if (!__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) kept[nk] = v;
+            ++nk;
+        }
+        __syncwarp();
+    }
+    for (int t = lane; t < nk; t += 32) out[t] = kept[t];
+    if (lane == 0) *nout = nk;
+}
+
 }  // namespace fa
 
 using namespace fa;
+
+extern "C" int fa_select_exact_dev(const float *vecs, int dim, const int32_t *cand_ids,
+                                   const double *cand_d, int ncand, int cap, int32_t *out,
+                                   int32_t *nout, void *stream) {
+    FA_CHECK_ARG(dim >= 1, "dim must be >= 1");
+    FA_CHECK_ARG(ncand >= 0 && cap >= 0, "negative sizes");
+    cudaStream_t st = as_stream(stream);
+    if (ncand == 0 || cap == 0) {
+        FA_CUDA(cudaMemsetAsync(nout, 0, sizeof(int32_t), st));
+        return FA_OK;
+    }
+    const size_t smem = (size_t)round_up(cap, 4) * 4;
+    FA_CHECK_ARG(smem <= 220 * 1024, "cap too large for one select call");
+    if (smem > 48 * 1024)
+        FA_CUDA(cudaFuncSetAttribute(select_exact_hook_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    select_exact_hook_kernel<<<1, 32, smem, st>>>(vecs, dim, cand_ids, cand_d, ncand, cap, out,
+                                                  nout);
+    FA_LAUNCH_CHECK();
+    return FA_OK;
+}
 
 extern "C" int fa_sdt_sum_dev(const uint8_t *sdt, int m, const uint8_t *a, int64_t a_stride,
                               const uint8_t *b, int64_t b_stride, int64_t npairs, int32_t *out,

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
 QuerySearchFn query_search_variant(int W, bool exact) {
     if (exact) {
         FA_VARIANTS(query_search_kernel, ExactDist)
-        return nullptr;
+        return query_search_kernel<ExactDist, 0>;
     }
     FA_VARIANTS(query_search_kernel, FlashDist)
     return query_search_kernel<FlashDist, 0>;
@@ -163,7 +163,7 @@ QuerySearchFn query_search_variant(int W, bool exact) {
 LayerSearchFn layer_search_variant(int W, bool exact) {
     if (exact) {
         FA_VARIANTS(layer_search_kernel, ExactDist)
-        return nullptr;
+        return layer_search_kernel<ExactDist, 0>;
     }
     FA_VARIANTS(layer_search_kernel, FlashDist)
     return layer_search_kernel<FlashDist, 0>;

@@ -37,8 +37,10 @@ struct Graph {
     int64_t nU;
     int tie;     // tie order of the searches (TieOrder modes)
     int expand;  // frontier entries expanded per step (1 = semantic core)
-    uint32_t *gvis;        // global visited tables, one per SM warp slot (or null)
+    uint32_t *gvis;        // global visited tables, gvis_nslots of 2^gvis_log2 (or null)
     uint32_t *gvis_epoch;  // their epoch counters
+    uint32_t *gvis_owner;  // 1 while a search holds the slot (claimed atomically)
+    int gvis_log2, gvis_nslots;
     const float *vecs;     // n x dim vectors (exact kind: every distance; rerank)
     int dim;
 };
@@ -107,7 +109,7 @@ struct WarpLayout {
         } else {
             // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
             T = o;
-            o += Wp * (W > kRegSetMax ? 8 + 4 + 1 : 8);
+            o += Wp * (W > kRegSetMax ? 8 + key_bytes + 1 : 8);
             o = round_up(o, 16);
         }
         S = o; o += 2 * nc * key_bytes;  // candidate keys (two buffers)
@@ -204,13 +206,31 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
 // bijection h = id * odd (mod 2^24) to bucket h >> (24 - kb) and remainder
 // (h & low bits) + 1 (0 = empty), so a slot needs 16 bits and one 16-byte load
 // tests a whole bucket.  Slots fill in order and are never removed; an id whose
-// bucket is full lives in the global tier: a per-warp-slot open-addressing
-// table in global memory (L2-resident) holding (epoch << 24 | id).  Entries of
-// older epochs count as empty, so a slot's table is cleared only once every
-// 255 searches.  Either way every id lives in exactly one tier.
-constexpr int kGlobalHashLog2 = 14;
+// bucket is full lives in the global tier: an open-addressing table in global
+// memory (L2-resident) holding (epoch << 24 | id), one per claimed slot.
+// Entries of older epochs count as empty, so a slot's table is cleared only
+// once every 255 searches.  Either way every id lives in exactly one tier.
+//
+// Global-tier slots are claimed per search with an atomic on an owner word
+// (the probe starts at %smid / %warpid, which is free in the common case) and
+// released when the search ends, so a preempted or migrated warp can never
+// share a table with another live search.  The host sizes the pool to the
+// launch's resident warps and each table (2^gvis_log2 entries) to the search
+// width (gvis_log2_for).
 constexpr int kMaxWarpsPerSM = 64;
 constexpr uint32_t kVisMul = 0x9E3779B1u;
+
+// log2 entries of a global-tier table for searches of width W over n vertices:
+// room for every id such a search can plausibly visit (the shared tier holds
+// the first few thousand), at a 3/4 load limit.
+__host__ __device__ inline int gvis_log2_for(int W, int capmax, int64_t n) {
+    int64_t want = 16 * (int64_t)W + 2 * (int64_t)capmax;
+    if (want > n) want = n;
+    want = want * 4 / 3 + 1;
+    int l = 14;
+    while (l < 20 && ((int64_t)1 << l) < want) ++l;
+    return l;
+}
 
 __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
     uint4 v;
@@ -223,14 +243,15 @@ __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
 
 // The global tier's probe (ids whose shared bucket is full: the cold path,
 // kept out of line so the hot loop stays compact).  0 = already visited,
-// 2 = inserted.
-static __device__ __noinline__ int global_visit(uint32_t *G, uint32_t epoch, int id) {
+// 2 = inserted.  Reads bypass L1 (the table may have been written on another SM
+// by the slot's previous owner).
+static __device__ __noinline__ int global_visit(uint32_t *G, int glog2, uint32_t epoch, int id) {
     const uint32_t key = (uint32_t)id + 1u;
     const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
-    const uint32_t gmask = (1u << kGlobalHashLog2) - 1u;
-    uint32_t p = (key * 2654435761u) >> (32 - kGlobalHashLog2);
+    const uint32_t gmask = (1u << glog2) - 1u;
+    uint32_t p = (key * 2654435761u) >> (32 - glog2);
     while (true) {
-        const uint32_t v = G[p];
+        const uint32_t v = __ldcg(G + p);
         if (v == gk) return 0;
         if ((v >> 24) != epoch) {
             const uint32_t old = atomicCAS(G + p, v, gk);
@@ -249,44 +270,63 @@ struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
     int nslots;        // usable slots per bucket
-    uint32_t *G;       // global tier of this warp slot
-    uint32_t *gepoch;  // epoch counter of this warp slot
+    uint32_t *G;       // global tier of the claimed slot
+    uint32_t *gown;    // its owner word
+    int glog2;
     uint32_t epoch;
     int gcount, glimit;
 
-    __device__ static uint32_t slot_id() {
+    __device__ static uint32_t slot_hint() {
         uint32_t sm, w;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
         asm volatile("mov.u32 %0, %%warpid;" : "=r"(w));
         return sm * kMaxWarpsPerSM + w;
     }
 
-    __device__ void begin(void *H, int hlog2, uint32_t *gtables, uint32_t *gepochs, int lane) {
+    __device__ void begin(void *H, int hlog2, const Graph &g, int lane) {
         B = reinterpret_cast<uint4 *>(H);
         kb = KB ? KB : vis_buckets_log2(hlog2);
         nslots = vis_bucket_slots(hlog2);
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
         gcount = 0;
-        glimit = (1 << kGlobalHashLog2) * 3 / 4;
+        glog2 = g.gvis_log2;
+        glimit = g.gvis ? (1 << glog2) * 3 / 4 : (1 << 30);  // no tier: visit() reports 3
         G = nullptr;
-        if (gtables) {
-            const uint32_t slot = slot_id();
-            G = gtables + ((size_t)slot << kGlobalHashLog2);
-            gepoch = gepochs + slot;
-            uint32_t e = 0;
-            if (lane == 0) e = *gepoch + 1u;
+        gown = nullptr;
+        if (g.gvis) {
+            uint32_t slot = 0, e = 0;
+            if (lane == 0) {
+                const uint32_t ns = (uint32_t)g.gvis_nslots;
+                slot = slot_hint() % ns;
+                while (atomicCAS(g.gvis_owner + slot, 0u, 1u) != 0u) slot = (slot + 1u) % ns;
+                e = atomicAdd(g.gvis_epoch + slot, 1u) + 1u;
+            }
+            slot = __shfl_sync(0xffffffffu, slot, 0);
             e = __shfl_sync(0xffffffffu, e, 0);
+            G = g.gvis + ((size_t)slot << glog2);
+            gown = g.gvis_owner + slot;
             if (e > 255u) {  // wrap: clear this slot's table once
-                for (int i = lane; i < (1 << kGlobalHashLog2) / 4; i += 32)
-                    reinterpret_cast<uint4 *>(G)[i] = z;
+                for (int i = lane; i < (1 << glog2) / 4; i += 32)
+                    __stcg(reinterpret_cast<uint4 *>(G) + i, z);
                 e = 1u;
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(g.gvis_epoch + slot, 1u);
+                }
             }
             epoch = e;
-            __syncwarp();
-            if (lane == 0) *gepoch = e;
         }
         __syncwarp();
+    }
+    // release the global-tier slot (every exit of a search)
+    __device__ void end(int lane) {
+        __syncwarp();
+        if (gown && lane == 0) {
+            __threadfence();
+            atomicExch(gown, 0u);
+        }
     }
 
     // bucket of id and its remainder r (1 .. 2^(24 - kb))
@@ -327,7 +367,7 @@ struct VisitedSet {
             // another lane took the slot: re-read the bucket
             v = lds128_volatile(bk);
         }
-        return G == nullptr ? 3 : global_visit(G, epoch, id);
+        return G == nullptr ? 3 : global_visit(G, glog2, epoch, id);
     }
 };
 
@@ -437,40 +477,6 @@ __device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane, 
 // On return T[0..ts) holds the result as 64-bit keys (make_key of the tie id)
 // ascending by (d, tie id).  false = visited-set overflow.
 __device__ __forceinline__ uint32_t k32(uint32_t d, uint32_t tie) { return (d << 24) | tie; }
-
-// min key over entries with flag == 0 (mask_expanded) or over all entries
-// whose distance equals dsel (dsel < 256); returns (key, index), key = ~0u if none
-__device__ __forceinline__ uint32_t warp_argmin32(const uint32_t *K, const uint8_t *F, int n,
-                                                  int dsel, int lane, int &idx) {
-    uint32_t best = 0xffffffffu;
-    int bi = -1;
-#pragma unroll 4
-    for (int c = 0; c < n; c += 32) {
-        const int i = c + lane;
-        if (i < n) {
-            const uint32_t k = K[i];
-            const bool ok = dsel < 0 ? (F[i] == 0) : ((int)(k >> 24) == dsel);
-            if (ok && k < best) {
-                best = k;
-                bi = i;
-            }
-        }
-    }
-    const uint32_t m = __reduce_min_sync(0xffffffffu, best);
-    const unsigned own = __ballot_sync(0xffffffffu, best == m && bi >= 0);
-    idx = own ? __shfl_sync(0xffffffffu, bi, __ffs(own) - 1) : -1;
-    return m;
-}
-
-__device__ __forceinline__ uint32_t warp_maxd(const uint32_t *K, int n, int lane) {
-    uint32_t mx = 0;
-#pragma unroll 4
-    for (int c = 0; c < n; c += 32) {
-        const int i = c + lane;
-        if (i < n) mx = max(mx, K[i] >> 24);
-    }
-    return __reduce_max_sync(0xffffffffu, mx);
-}
 
 // ---- distance policies -------------------------------------------------------
 // fp32 L2 (fa_l2sq_f32 tree, common.cuh l2_tree) of four (query, vector) pairs
@@ -826,7 +832,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     K *Sb = Sa + cand_capacity(g);
     const unsigned lt = (1u << lane) - 1u;
     VisitedSet<KB> vs;
-    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
+    vs.begin(H, hlog2, g, lane);
     if (lane == 0) vs.visit(entry);
     RegSet<J, K> rs;
 #pragma unroll
@@ -919,7 +925,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) return false;
+        if (vs.gcount + npop * cap > vs.glimit) { vs.end(lane); return false; }
         // visited filter over the rows (pop order, slot order), compacted
         bool over = false;
         int nf = 0;
@@ -944,7 +950,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
-        if (__any_sync(FULL, over)) return false;
+        if (__any_sync(FULL, over)) { vs.end(lane); return false; }
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
@@ -955,28 +961,74 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     }
     sort_out<J>(rs, ts, T, lane);
     ts_out = ts;
+    vs.end(lane);
     return true;
 }
 
-// Shared-memory variant for W > kRegSetMax (same rules, same results).
+// Generic-key warp helpers of the shared-memory result set.  Keys are distinct.
+// min key over the entries not yet expanded (F[i] == 0), or, with dsel_on,
+// over the entries whose distance (key >> 24) equals dsel; idx = its slot.
+template <typename Kt>
+__device__ __forceinline__ Kt warp_argmin_key(const Kt *K, const uint8_t *F, int n, bool dsel_on,
+                                              uint32_t dsel, int lane, int &idx) {
+    Kt best = ~Kt(0);
+    int bi = -1;
+#pragma unroll 4
+    for (int c = 0; c < n; c += 32) {
+        const int i = c + lane;
+        if (i < n) {
+            const Kt k = K[i];
+            const bool ok = dsel_on ? ((uint32_t)(k >> 24) == dsel) : (F[i] == 0);
+            if (ok && k < best) {
+                best = k;
+                bi = i;
+            }
+        }
+    }
+    Kt m = ~Kt(0);
+    int owner = -1;
+    if (!warp_pick(bi >= 0, best, m, owner)) {
+        idx = -1;
+        return ~Kt(0);
+    }
+    idx = __shfl_sync(0xffffffffu, bi, owner);
+    return m;
+}
+
+template <typename Kt>
+__device__ __forceinline__ uint32_t warp_maxd_key(const Kt *K, int n, int lane) {
+    uint32_t mx = 0;
+#pragma unroll 4
+    for (int c = 0; c < n; c += 32) {
+        const int i = c + lane;
+        if (i < n) mx = max(mx, (uint32_t)(K[i] >> 24));
+    }
+    return __reduce_max_sync(0xffffffffu, mx);
+}
+
+// Shared-memory variant for W > kRegSetMax (same rules, same results), for
+// either distance policy (32-bit Flash keys, 64-bit exact keys).
+template <typename P>
 __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, uint32_t entry_d, int W,
-                                    const uint8_t *adt_s, unsigned long long *T, int &ts,
+                                    const uint8_t *qc, unsigned long long *T, int &ts,
                                     unsigned long long *S, int32_t *TQ, int32_t *fresh,
                                     uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
                                     const TieOrder &to, int lane) {
+    using Kt = typename P::Key;
+    constexpr Kt NONE = ~Kt(0);
     const int cap = layer_cap(g, layer);
-    // workspace (WarpLayout::T): 64-bit result slots, then the 32-bit keys, then
+    // workspace (WarpLayout::T): 64-bit result slots, then the keys, then
     // the expanded flags, Wp = round_up(W, 32) of each
     const int Wp = round_up(W, 32);
-    uint32_t *K = reinterpret_cast<uint32_t *>(T + Wp);
+    Kt *K = reinterpret_cast<Kt *>(T + Wp);
     uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
-    uint32_t *Sa = reinterpret_cast<uint32_t *>(S);
-    uint32_t *Sb = Sa + cand_capacity(g);
+    Kt *Sa = reinterpret_cast<Kt *>(S);
+    Kt *Sb = Sa + cand_capacity(g);
     VisitedSet<> vs;
-    vs.begin(H, hlog2, g.gvis, g.gvis_epoch, lane);
+    vs.begin(H, hlog2, g, lane);
     if (lane == 0) {
         vs.visit(entry);
-        K[0] = k32(entry_d, to.fwd((uint32_t)entry));
+        K[0] = P::key(entry_d, to.fwd((uint32_t)entry));
         F[0] = 0;
     }
     ts = 1;
@@ -998,11 +1050,11 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         for (int r = 0; r < kMaxExpand; ++r) {
             if (r >= E) break;
             int ia;
-            const uint32_t kT = warp_argmin32(K, F, ts, -1, lane, ia);
-            const uint32_t kQ = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
-            if (kT == 0xffffffffu && kQ == 0xffffffffu) break;
+            const Kt kT = warp_argmin_key(K, F, ts, false, 0u, lane, ia);
+            const Kt kQ = tq_h < tq_t ? P::key(wd, (uint32_t)TQ[tq_h]) : NONE;
+            if (kT == NONE && kQ == NONE) break;
             const bool fromT = kT < kQ;
-            pv[r] = to.back((fromT ? kT : kQ) & 0xffffffu);
+            pv[r] = to.back((uint32_t)((fromT ? kT : kQ) & 0xffffffu));
             ++npop;
             __syncwarp();
             if (fromT) {
@@ -1028,15 +1080,15 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         if (E == 1) {  // predict the next pop assuming nothing new enters
             int ib;
-            const uint32_t k1 = warp_argmin32(K, F, ts, -1, lane, ib);
-            const uint32_t k2 = tq_h < tq_t ? k32(wd, (uint32_t)TQ[tq_h]) : 0xffffffffu;
-            const uint32_t kn = k1 < k2 ? k1 : k2;
-            pre_v = kn != 0xffffffffu ? to.back(kn & 0xffffffu) : -1;
+            const Kt k1 = warp_argmin_key(K, F, ts, false, 0u, lane, ib);
+            const Kt k2 = tq_h < tq_t ? P::key(wd, (uint32_t)TQ[tq_h]) : NONE;
+            const Kt kn = k1 < k2 ? k1 : k2;
+            pre_v = kn != NONE ? to.back((uint32_t)(kn & 0xffffffu)) : -1;
             if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) return false;
+        if (vs.gcount + npop * cap > vs.glimit) { vs.end(lane); return false; }
         bool over = false;
         // visited filter over the rows (pop order, slot order), compacted
         int nf = 0;
@@ -1061,12 +1113,12 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
-        if (__any_sync(0xffffffffu, over)) return false;
+        if (__any_sync(0xffffffffu, over)) { vs.end(lane); return false; }
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
         if (nf == 0) continue;
-        dists_for(adt_s, g.codes, g.mpad, fresh, nf, fdist, lane);
+        P::dists(g, qc, fresh, nf, fdist, lane);
         phase_mark(cnt, 2, tph);
         // candidates that can possibly enter: all while the set is not full,
         // else d < worst
@@ -1077,7 +1129,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
             const unsigned b = __ballot_sync(0xffffffffu, ok);
             if (ok)
                 Sa[ns + __popc(b & ((1u << lane) - 1u))] =
-                    k32(fdist[f], to.fwd((uint32_t)fresh[f]));
+                    P::key(fdist[f], to.fwd((uint32_t)fresh[f]));
             ns += __popc(b);
         }
         __syncwarp();
@@ -1091,12 +1143,12 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
             }
             ts += ns;
             __syncwarp();
-            if (ts == W) wd = warp_maxd(K, ts, lane);
+            if (ts == W) wd = warp_maxd_key(K, ts, lane);
             continue;
         }
         // offers are processed in ascending order: rank-sort them
         for (int j = lane; j < ns; j += 32) {
-            const uint32_t k = Sa[j];
+            const Kt k = Sa[j];
             int r = 0;
             for (int t = 0; t < ns; ++t) r += Sa[t] < k;
             Sb[r] = k;
@@ -1108,12 +1160,12 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         ts += nfill;
         __syncwarp();
-        wd = warp_maxd(K, ts, lane);
+        wd = warp_maxd_key(K, ts, lane);
         for (int j = nfill; j < ns; ++j) {
-            const uint32_t s = Sb[j];
-            if ((s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+            const Kt s = Sb[j];
+            if ((uint32_t)(s >> 24) >= wd) break;  // sorted: every later offer is rejected too
             int e;
-            const uint32_t ev = warp_argmin32(K, F, ts, (int)wd, lane, e);
+            const Kt ev = warp_argmin_key(K, F, ts, true, wd, lane, e);
             if (!F[e]) {
                 if (lane == 0) TQ[tq_t] = (int32_t)(ev & 0xffffffu);
                 ++tq_t;
@@ -1124,7 +1176,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
                 F[e] = 0;
             }
             __syncwarp();
-            const uint32_t nwd = warp_maxd(K, ts, lane);
+            const uint32_t nwd = warp_maxd_key(K, ts, lane);
             if (nwd < wd) {
                 wd = nwd;
                 tq_h = tq_t = 0;  // the evicted ties are beyond the new worst
@@ -1133,19 +1185,20 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
     }
     // sort the keys once: rank by counting (keys are distinct) into the 64-bit slots
     for (int i = lane; i < ts; i += 32) {
-        const uint32_t k = K[i];
+        const Kt k = K[i];
         int r = 0;
         for (int t = 0; t < ts; ++t) r += K[t] < k;
-        T[r] = make_key(k >> 24, (int)(k & 0xffffffu));
+        T[r] = make_key((uint32_t)(k >> 24), (int)(k & 0xffffffu));
     }
     __syncwarp();
+    vs.end(lane);
     return true;
 }
 
 
 // Best-first layer search with the result-set variant J chosen by the host
 // (set_variant): J slots per lane in registers, J = 0 the shared-memory set
-// (Flash only).  P: the distance policy (FlashDist / ExactDist).
+// (either kind).  P: the distance policy (FlashDist / ExactDist).
 template <typename P, int J, int EM, int RC = kRowChunks, int KB = 0>
 __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entry, uint32_t entry_d,
                                              int W, const uint8_t *qc, unsigned long long *T,
@@ -1154,8 +1207,7 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
                                              int hlog2, SearchCounters &cnt, const TieOrder &to,
                                              int lane) {
     if constexpr (J == 0) {
-        static_assert(!P::kExact, "the shared-memory result set serves the Flash kind only");
-        return layer_search_smem(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
+        return layer_search_smem<P>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
                                  hlog2, cnt, to, lane);
     } else {
         return layer_search_reg<P, J, EM, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ,

@@ -103,49 +103,64 @@ CONFIGS = {
 def baseline_config(cfg: int, n: int | None = None, nq: int | None = None, seed: int = 0):
     """(base (n, dim) f32, queries (nq, dim) f32) for BASELINE config `cfg`.
 
+    Prefix-stable: the mixture parameters come from one generator and every
+    per-row quantity from its own sequential generator, base rows and queries
+    on separate streams, so base row i (and query j) is the same for every n
+    (nq): a smaller n is exactly the first n rows of the full workload.
     Queries are fresh draws from the same distribution (same mixture
-    centres).  `n` may select a prefix-sized sample of the same law."""
+    parameters).  Rows are generated in chunks to bound host memory."""
     c = CONFIGS[cfg]
     n = c["n"] if n is None else n
     nq = c["nq"] if nq is None else nq
-    rng = np.random.default_rng(seed)
-    tot = n + nq
+    if cfg not in CONFIGS:
+        raise ConfigError(f"unknown config {cfg}")
+    d = c["dim"]
+    prm = np.random.default_rng([seed, cfg, 0])
     if cfg == 1:
         # 64-component isotropic mixture, centres ~ N(0,1), sigma 0.3
-        centres = rng.normal(0.0, 1.0, (64, c["dim"]))
-        a = rng.integers(0, 64, tot)
-        x = centres[a] + rng.normal(0.0, 0.3, (tot, c["dim"]))
+        params = dict(centres=prm.normal(0.0, 1.0, (64, d)))
     elif cfg == 2:
         # 256-component mixture, centres ~ U(0,255), sigma 20, rounded, clipped
-        centres = rng.uniform(0.0, 255.0, (256, c["dim"]))
-        a = rng.integers(0, 256, tot)
-        x = np.clip(np.rint(centres[a] + rng.normal(0.0, 20.0, (tot, c["dim"]))), 0, 255)
+        params = dict(centres=prm.uniform(0.0, 255.0, (256, d)))
     elif cfg == 3:
-        centres = rng.normal(0.0, 1.0, (1024, c["dim"]))
-        a = rng.integers(0, 1024, tot)
-        x = centres[a] + rng.normal(0.0, 0.3, (tot, c["dim"]))
-        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        # 1024 components, centres ~ N(0,1), sigma 0.3, then unit L2 norm
+        params = dict(centres=prm.normal(0.0, 1.0, (1024, d)))
     elif cfg == 4:
         # 512 components, covariance spectrum i^-1.2 in one random rotation
-        d = c["dim"]
-        q, _ = np.linalg.qr(rng.normal(size=(d, d)))
-        scale = np.arange(1, d + 1, dtype=np.float64) ** -0.6
-        centres = rng.normal(0.0, 1.0, (512, d))
-        a = rng.integers(0, 512, tot)
-        x = centres[a] + (rng.normal(size=(tot, d)) * scale) @ q.T
-    elif cfg == 5:
-        # rank-64 signal + isotropic noise at SNR 3 (power ratio), unit norm, bf16
-        d = c["dim"]
-        basis = rng.normal(size=(64, d)) / np.sqrt(d)
-        sig = rng.normal(size=(tot, 64)) @ basis
-        noise = rng.normal(size=(tot, d)) * np.sqrt((sig ** 2).mean() / 3.0)
-        x = sig + noise
-        x /= np.linalg.norm(x, axis=1, keepdims=True)
-        x = _round_bf16(x.astype(np.float32))
+        q, _ = np.linalg.qr(prm.normal(size=(d, d)))
+        params = dict(rot=q, scale=np.arange(1, d + 1, dtype=np.float64) ** -0.6,
+                      centres=prm.normal(0.0, 1.0, (512, d)))
     else:
-        raise ConfigError(f"unknown config {cfg}")
-    x = x.astype(np.float32)
-    return x[:n], x[n:]
+        # rank-64 signal + isotropic noise at SNR 3 (power ratio), unit norm,
+        # bf16; the noise power is the signal's expected power / 3
+        basis = prm.normal(size=(64, d)) / np.sqrt(d)
+        params = dict(basis=basis, noise_sd=np.sqrt((basis ** 2).sum() / d / 3.0))
+    return (_rows(cfg, params, n, seed, 1), _rows(cfg, params, nq, seed, 2))
+
+
+def _rows(cfg: int, p: dict, count: int, seed: int, stream: int, chunk: int = 1 << 18):
+    d = CONFIGS[cfg]["dim"]
+    ra = np.random.default_rng([seed, cfg, stream, 0])  # component / signal draws
+    rn = np.random.default_rng([seed, cfg, stream, 1])  # noise draws
+    out = np.empty((count, d), np.float32)
+    for lo in range(0, count, chunk):
+        s = min(chunk, count - lo)
+        if cfg == 1:
+            x = p["centres"][ra.integers(0, 64, s)] + rn.normal(0.0, 0.3, (s, d))
+        elif cfg == 2:
+            x = p["centres"][ra.integers(0, 256, s)] + rn.normal(0.0, 20.0, (s, d))
+            x = np.clip(np.rint(x), 0, 255)
+        elif cfg == 3:
+            x = p["centres"][ra.integers(0, 1024, s)] + rn.normal(0.0, 0.3, (s, d))
+            x /= np.linalg.norm(x, axis=1, keepdims=True)
+        elif cfg == 4:
+            x = p["centres"][ra.integers(0, 512, s)] + (rn.normal(size=(s, d)) * p["scale"]) @ p["rot"].T
+        else:
+            x = ra.normal(size=(s, 64)) @ p["basis"] + rn.normal(size=(s, d)) * p["noise_sd"]
+            x /= np.linalg.norm(x, axis=1, keepdims=True)
+            x = _round_bf16(x.astype(np.float32))
+        out[lo: lo + s] = x
+    return out
 
 
 def _round_bf16(x: np.ndarray) -> np.ndarray:

@@ -14,8 +14,9 @@ exposes the same names and signatures as the compiled core
 
 Every call runs on the GPU through the C-ABI (include/flashann_b200.h); array
 arguments are host numpy buffers exactly as in the reference, blocks and
-codes are mutated in place.  Only the Flash strategy (kind 4) is served —
-the other strategies are outside this core's scope and raise ValueError.
+codes are mutated in place.  The Flash strategy (kind 4) and the exact
+strategy (kind 0) are served — the PQ / SQ / PCA strategies are outside this
+core's scope and raise ValueError.
 
 Batched insertion replaces OpenMP threads: ``threads`` is accepted and
 ignored; the batch schedule is set by BUILD_OPTIONS.
@@ -34,8 +35,15 @@ from ._lib import check, ptr
 CORE_NAME = "sm100"
 KIND_FLASH = 4
 
-# kernel names; index = kernel id (reference evaluate() indexes this tuple)
-KERNEL_NAMES = ("sm100",)
+# Lookup-kernel names; index = kernel id.  The reference resolves a kernel
+# name through its own registry (core.py:28 KERNEL_IDS, :40-57 resolve_kernel)
+# and evaluate() indexes this tuple by id (evaluation.py:142-143), so the core
+# answers with the registry's names.  Every id selects the same sm_100a code
+# path: the reference requires its kernels to be bit-identical to each other
+# (tests/test_flash.py:207-217), which a single implementation is by
+# construction.  Serving all four ids makes the core a drop-in without a patch
+# to the reference's registry.
+KERNEL_NAMES = ("scalar", "vector128", "vector256", "vector512")
 
 BUILD_OPTIONS = {
     "batch_max": int(os.environ.get("FLASHANN_B200_BATCH_MAX", "65536")),
@@ -212,42 +220,58 @@ def search_batch(kind, prov, levels, base_blocks, upper_offsets, upper_blocks, C
 
 
 class DeviceIndex:
-    """A device graph built from reference-layout host arrays (test hooks)."""
+    """A device graph built from reference-layout host arrays (test hooks).
 
-    def __init__(self, prov, levels, base_blocks, upper_offsets, upper_blocks, R, vecs=None):
+    kind 4 (Flash): codes, tables and the SDT from ``prov``; kind 0 (exact):
+    the vectors only (a device index with m = 0)."""
+
+    def __init__(self, prov, levels, base_blocks, upper_offsets, upper_blocks, R, vecs=None,
+                 kind=KIND_FLASH):
         torch = _torch()
         self.lib = _lib_()
         self.keep = []
-        cent, dims, offs, sdt, proj = _prov_arrays(prov)
         lv = _c(levels, np.int32)
         uo = _c(upper_offsets, np.int64)
         self.n = lv.shape[0]
+        self.kind = kind
         d = _lib.IndexDesc()
         d.n = self.n
-        d.m = cent.shape[0]
         d.R = int(R)
-        d.dproj = proj.shape[1]
-        d.dmax = cent.shape[2]
-        d.dist_min = float(prov["dist_min"])
-        d.delta = float(prov["delta"])
-        for name, arr in (("cent", cent), ("dims", dims), ("offs", offs), ("sdt", sdt),
-                          ("levels", lv), ("uoff", uo), ("proj", proj)):
-            t = _dev(arr)
-            self.keep.append(t)
-            setattr(d, name, t.data_ptr())
+        if kind == KIND_EXACT:
+            vecs = prov["vecs"]
+            d.m = 0
+            for name, arr in (("levels", lv), ("uoff", uo)):
+                t = _dev(arr)
+                self.keep.append(t)
+                setattr(d, name, t.data_ptr())
+        else:
+            cent, dims, offs, sdt, proj = _prov_arrays(prov)
+            d.m = cent.shape[0]
+            d.dproj = proj.shape[1]
+            d.dmax = cent.shape[2]
+            d.dist_min = float(prov["dist_min"])
+            d.delta = float(prov["delta"])
+            for name, arr in (("cent", cent), ("dims", dims), ("offs", offs), ("sdt", sdt),
+                              ("levels", lv), ("uoff", uo), ("proj", proj)):
+                t = _dev(arr)
+                self.keep.append(t)
+                setattr(d, name, t.data_ptr())
         if vecs is not None:
             t = _dev(_c(vecs, np.float32))
             self.keep.append(t)
             d.vecs = t.data_ptr()
             d.dim = t.shape[1]
+            if kind == KIND_EXACT:
+                d.dproj = d.dim
         ub = np.ascontiguousarray(upper_blocks)
         d.n_upper_rows = ub.shape[0]
         self.desc = d
         h = _lib.vp()
         check(self.lib.fa_index_create(C.byref(d), C.byref(h)))
         self.h = h
-        codes = _dev(_c(prov["codes"], np.uint8))
-        check(self.lib.fa_index_set_codes(h, codes.data_ptr(), codes.shape[1], None))
+        if kind != KIND_EXACT:
+            codes = _dev(_c(prov["codes"], np.uint8))
+            check(self.lib.fa_index_set_codes(h, codes.data_ptr(), codes.shape[1], None))
         bb = _dev(np.ascontiguousarray(base_blocks))
         ubd = _dev(ub) if ub.size else torch.zeros(1, dtype=torch.uint8, device="cuda")
         check(self.lib.fa_index_import_blocks(h, bb.data_ptr(), bb.shape[1], ubd.data_ptr(),
@@ -286,12 +310,15 @@ def greedy_search_layer(kind, prov, levels, base_blocks, upper_offsets, upper_bl
     """Single-layer candidate search: ([(id, dist)], counters)
     (reference hook _core.pyx:891-939; (d, id) ordering)."""
     _require_flash(kind)
-    if qaux is None:
+    if kind == KIND_FLASH and qaux is None:
         raise ValueError("this strategy requires a prepared query payload (qaux)")
     torch = _torch()
-    ix = DeviceIndex(prov, levels, base_blocks, upper_offsets, upper_blocks, R)
+    ix = DeviceIndex(prov, levels, base_blocks, upper_offsets, upper_blocks, R, kind=kind)
     try:
-        qp = _dev(_c(np.atleast_2d(qaux), np.float32))
+        # Flash: the reduced query (its table is built on the device); exact:
+        # the query vector itself
+        qsrc = query if kind == KIND_EXACT else qaux
+        qp = _dev(_c(np.atleast_2d(qsrc), np.float32))
         ent = _dev(np.array([entry], dtype=np.int64))
         oid = torch.empty((1, width), dtype=torch.int32, device="cuda")
         od = torch.empty((1, width), dtype=torch.float64, device="cuda")
@@ -332,6 +359,16 @@ def select_neighbors(kind, prov, cand_ids, cand_dists, cap):
     n = ci.shape[0]
     if n == 0 or cap <= 0:
         return []
+    if kind == KIND_EXACT:
+        vecs = _dev(_c(prov["vecs"], np.float32))
+        dci, dcd = _dev(ci), _dev(cd)
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        nout = torch.zeros(1, dtype=torch.int32, device="cuda")
+        check(lib.fa_select_exact_dev(vecs.data_ptr(), vecs.shape[1], dci.data_ptr(),
+                                      dcd.data_ptr(), n, int(cap), out.data_ptr(),
+                                      nout.data_ptr(), None))
+        nk = int(nout.cpu()[0])
+        return [int(x) for x in out.cpu().numpy()[:nk]]
     sdt = _dev(_c(prov["sdt"], np.uint8))
     codes = _dev(_padded_codes(prov["codes"]))
     m = int(prov["sdt"].shape[0])

@@ -56,7 +56,10 @@ def test_core_module_contract():
                  "flash_batch_distance_many", "flash_batch_blocks", "flash_sdt_distance",
                  "flash_encode_adt", "quantize_distance", "l2sq_f32"):
         assert hasattr(sm100, name), name
-    assert sm100.available_kernels() == ("sm100",)
+    # the reference's kernel registry names (core.py:28), in id order, so
+    # core.resolve_kernel needs no patch
+    assert sm100.available_kernels() == ("scalar", "vector128", "vector256", "vector512")
+    assert sm100.CORE_NAME == "sm100"
 
 
 def test_no_cpu_fallback_without_device():

@@ -19,14 +19,19 @@ from oracle import native
 pytestmark = pytest.mark.gpu
 
 N = 3000
+SCHED = dict(batch_max=512, batch_frac=0.2, seq_prefix=32)
+# a schedule whose third batch is a full 65,536-vertex batch (1, 100, 10,100,
+# 65,536, ...): the batch size of the production build
+BIG = dict(batch_max=65536, batch_frac=100.0, seq_prefix=0)
 SHAPES = {
     "c1": dict(cfg=1, C=None),
+    "c2": dict(cfg=2, C=None),  # the bench's shape: m = 64 (4 ADT chunks), C = 200
     "c3": dict(cfg=3, C=None),
     "c4": dict(cfg=4, C=None),
     "c5": dict(cfg=5, C=None),
     "c1_wide": dict(cfg=1, C=600),  # W > 512: shared-memory result set
+    "c2_batch64k": dict(cfg=2, C=None, n=80_000, sched=BIG),
 }
-SCHED = dict(batch_max=512, batch_frac=0.2, seq_prefix=32)
 
 
 @pytest.fixture(scope="module")
@@ -41,13 +46,14 @@ def _setup(name):
 
     spec = SHAPES[name]
     c = dataset.CONFIGS[spec["cfg"]]
-    data, queries = dataset.baseline_config(spec["cfg"], n=N, nq=50)
-    model = flash.flash_train(data, c["d_f"], c["m_f"], seed=0, kmeans_iters=4)
+    n = spec.get("n", N)
+    data, queries = dataset.baseline_config(spec["cfg"], n=n, nq=50)
+    model = flash.flash_train(data[:20_000], c["d_f"], c["m_f"], seed=0, kmeans_iters=4)
     prov = flash.FlashProvider(model)
     prov.attach(data)
     arrays = prov.core_arrays()
     qaux = prov.query_aux(queries)
-    levels = graph.assign_layers(N, 0, c["M"])
+    levels = graph.assign_layers(n, 0, c["M"])
     uoff = graph.upper_offsets_of(levels)
     C = spec["C"] or c["efC"]
     return c, data, queries, arrays, qaux, levels, uoff, C
@@ -58,12 +64,14 @@ def test_config_shape_build_and_search(core, name):
     from paper_2502_18113_b200 import layout
 
     c, data, queries, prov, qaux, levels, uoff, C = _setup(name)
+    sched = SHAPES[name].get("sched", SCHED)
+    n = levels.shape[0]
     R, m = c["M"], prov["cent"].shape[0]
     prov = dict(prov, codes=np.zeros_like(prov["codes"]))
-    base = layout.empty_rows(N, 2 * R, m)
+    base = layout.empty_rows(n, 2 * R, m)
     upper = layout.empty_rows(int(levels.sum()), R, m)
     saved = dict(core.BUILD_OPTIONS)
-    core.BUILD_OPTIONS.update(SCHED, tie=2, expand=1, hash_log2=0)
+    core.BUILD_OPTIONS.update(sched, tie=2, expand=1, hash_log2=0)
     try:
         res = core.build_graph(4, prov, levels, base, uoff, upper, C, R)
     finally:
@@ -71,10 +79,12 @@ def test_config_shape_build_and_search(core, name):
         core.BUILD_OPTIONS.update(saved)
     hg = native.HostGraph(levels, uoff, R, m, tie=2, expand=1)
     ores = hg.build(prov["proj"], prov["cent"], prov["dims"], prov["offs"], prov["dist_min"],
-                    prov["delta"], prov["sdt"], C, **SCHED)
+                    prov["delta"], prov["sdt"], C, **sched)
     assert (res["entry_point"], res["max_layer"]) == (ores["entry_point"], ores["max_layer"])
     assert np.array_equal(prov["codes"], hg.codes)
-    for v in range(N):
+    if sched is BIG:
+        assert ores["n_batches"] >= 4
+    for v in range(n):
         assert np.array_equal(layout.row_ids(base, v, 2 * R), hg.neighbors(v, 0)), v
         for lay in range(1, levels[v] + 1):
             r = uoff[v] + lay - 1
