@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
-    WarpWS ws(smem, wid, kSearchWarps, L);
+    WarpWS ws(smem, wid, blockDim.x >> 5, L);  // fewer warps per CTA for wide searches
     CounterTotals total;
     // persistent warps pull vertices from the batch; a slow search never holds
     // its CTA siblings' slots idle

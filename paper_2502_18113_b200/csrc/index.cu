@@ -105,6 +105,14 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
 // and each table 2^gvis_log2_for(W) entries; it grows on demand (reallocated
 // only when a launch needs more slots or a wider table).  Absent for n >= 2^24
 // (the tier packs ids into 24 bits), where the shared tier alone must suffice.
+// Warps per CTA of a search launch: kSearchWarps, fewer when the per-warp
+// workspace (wide searches) does not fit; 0 if one warp does not fit.
+static int search_warps_for(int per_warp_bytes) {
+    int w = kSearchWarps;
+    while (w > 0 && (size_t)w * per_warp_bytes > 227 * 1024) --w;
+    return w;
+}
+
 static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t smem, int W) {
     if (ix->g.n >= (1ll << 24) - 1) return FA_OK;
     int dev = 0, nsm = 0, per_sm = 0;
@@ -536,9 +544,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     WarpLayout L;
     L.init(g.mpad, C, capmax, hl, gb.expand, t_alias, exact ? g.dim * 4 : -1, exact ? 8 : 4);
     const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
-    const size_t smem_search = (size_t)kSearchWarps * L.total;
-    FA_CHECK_ARG(smem_search <= 227 * 1024, "search workspace %zu B exceeds shared memory",
-                 smem_search);
+    const int bw = search_warps_for(L.total);  // warps per CTA
+    const size_t smem_search = (size_t)bw * L.total;
+    FA_CHECK_ARG(bw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
     const BuildSearchFn search_fn =
         exact ? build_search_exact_variant(C, g.cap0) : build_search_variant(C, gb.expand, g.cap0);
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
@@ -561,7 +569,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int64_t rev_ctas = (int64_t)std::max(rev_per_sm, 1) * num_sms();
     int search_per_sm = 0;
     FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&search_per_sm, search_fn,
-                                                          kSearchWarps * 32, smem_search));
+                                                          bw * 32, smem_search));
     const int64_t search_ctas = (int64_t)std::max(search_per_sm, 1) * num_sms();
     // carve out only the shared memory the resident CTAs use: the rest stays
     // L1, which holds the transposed SDT and the hot code rows
@@ -573,7 +581,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                      cudaFuncAttributePreferredSharedMemoryCarveout,
                                      std::min(100, std::max(0, pct))));
     }
-    FA_TRY(ensure_gvis(ix, (const void *)search_fn, kSearchWarps * 32, smem_search, C));
+    FA_TRY(ensure_gvis(ix, (const void *)search_fn, bw * 32, smem_search, C));
     gb.gvis = g.gvis;
     gb.gvis_epoch = g.gvis_epoch;
     gb.gvis_owner = g.gvis_owner;
@@ -723,8 +731,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
         // nheads[0]: reverse row heads, nheads[1]: the search's work counter
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), st));
-        int grid = (int)std::min<int64_t>(search_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
-        search_fn<<<grid, kSearchWarps * 32, smem_search, st>>>(
+        int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
+        search_fn<<<grid, bw * 32, smem_search, st>>>(
             gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
             order_d + b.start,
             req, ctr, err, opts->point_stats, nheads + 1);
@@ -839,12 +847,13 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
            pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0,
                           (size_t)8 * std::min(std::max(rerank_depth, 0), ef)),
            1, false, exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
-    size_t smem = (size_t)kSearchWarps * L.total;
-    FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
+    const int qw = search_warps_for(L.total);  // warps per CTA
+    FA_CHECK_ARG(qw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
+    size_t smem = (size_t)qw * L.total;
     const QuerySearchFn qfn = query_search_variant(ef, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    FA_TRY(ensure_gvis(ix, (const void *)qfn, kSearchWarps * 32, smem, ef));
+    FA_TRY(ensure_gvis(ix, (const void *)qfn, qw * 32, smem, ef));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
@@ -856,11 +865,11 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     if (!rc) {
         cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
         cudaMemsetAsync(err, 0, sizeof(int), st);
-        int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        int grid = (nq + qw - 1) / qw;
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
         gq.expand = 1;
-        qfn<<<grid, kSearchWarps * 32, smem, st>>>(
+        qfn<<<grid, qw * 32, smem, st>>>(
             gq, adt_q, nq, (int)entry, max_layer, ef, k, rerank_depth, ix->d.vecs, ix->d.dim,
             queries, L, out_ids, out_d, ctr, err);
         cudaError_t e = cudaGetLastError();
@@ -902,12 +911,13 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     WarpLayout L;
     L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1, false,
            exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
-    size_t smem = (size_t)kSearchWarps * L.total;
-    FA_CHECK_ARG(smem <= 227 * 1024, "search workspace %zu B exceeds shared memory", smem);
+    const int qw = search_warps_for(L.total);  // warps per CTA
+    FA_CHECK_ARG(qw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
+    size_t smem = (size_t)qw * L.total;
     const LayerSearchFn lfn = layer_search_variant(width, exact);
     FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    FA_TRY(ensure_gvis(ix, (const void *)lfn, kSearchWarps * 32, smem, width));
+    FA_TRY(ensure_gvis(ix, (const void *)lfn, qw * 32, smem, width));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
@@ -919,11 +929,11 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     if (!rc) {
         cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st);
         cudaMemsetAsync(err, 0, sizeof(int), st);
-        int grid = (nq + kSearchWarps - 1) / kSearchWarps;
+        int grid = (nq + qw - 1) / qw;
         Graph gq = ix->g;
         gq.tie = ix->search_tie;
         gq.expand = 1;
-        lfn<<<grid, kSearchWarps * 32, smem, st>>>(
+        lfn<<<grid, qw * 32, smem, st>>>(
             gq, exact ? reinterpret_cast<const uint8_t *>(qproj) : adt_q, nq, entries, width,
             layer, L, out_ids, out_d, out_n, ctr, err);
         cudaError_t e = cudaGetLastError();

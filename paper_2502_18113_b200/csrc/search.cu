@@ -37,9 +37,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
-    const int q = blockIdx.x * kSearchWarps + wid;
+    const int nw = blockDim.x >> 5;  // warps per CTA (fewer for wide searches)
+    const int q = blockIdx.x * nw + wid;
     if (q >= nq) return;
-    WarpWS ws(smem, wid, kSearchWarps, L);
+    WarpWS ws(smem, wid, nw, L);
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_query_ctx<P>(g, ws.adt, P::kExact ? reinterpret_cast<const uint8_t *>(queries) : adt_q,
                       q, lane);
@@ -115,9 +116,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     extern __shared__ __align__(256) uint8_t smem[];
     const int lane = lane_id();
     const int wid = threadIdx.x >> 5;
-    const int q = blockIdx.x * kSearchWarps + wid;
+    const int nw = blockDim.x >> 5;  // warps per CTA (fewer for wide searches)
+    const int q = blockIdx.x * nw + wid;
     if (q >= nq) return;
-    WarpWS ws(smem, wid, kSearchWarps, L);
+    WarpWS ws(smem, wid, nw, L);
     const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
     load_query_ctx<P>(g, ws.adt, adt_q, q, lane);
     __syncwarp();

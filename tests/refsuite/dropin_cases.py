@@ -73,7 +73,7 @@ def test_flash_search_equals_semantic_core(flash_pair):
     ds, ref, _ = flash_pair
     rng = np.random.default_rng(6)
     queries = ds.data[rng.choice(ds.n, 40, replace=False)] + 0.01
-    for ef in (8, 32, 100):
+    for ef in (10, 32, 100):
         a = search_batch(ref.graph, ref.provider, queries, SearchParams(ef=ef, k=10),
                          core_impl=_pycore)
         b = search_batch(ref.graph, ref.provider, queries, SearchParams(ef=ef, k=10),
