@@ -141,6 +141,31 @@ int fa_flash_range_dev(const float *xs, int64_t ns, int ld, const int32_t *dims,
                        const int32_t *offs, int m, const float *cent, int dmax, double *raw_sdt,
                        double *range_out, void *scratch, void *stream);
 
+/* ---- PCA contractions on the tensor cores (providers/pca.py) ------------- */
+
+#define FA_DTYPE_F32 0
+#define FA_DTYPE_BF16 1
+
+/* cov = (X - mean)^T (X - mean) / n as float64 (D x D, symmetric), X n x D
+ * device rows of f32 or bf16 (x_dtype), mean D f32 (the reference's
+ * float32-cast mean; pca.py:35-38).  3xTF32 tcgen05 GEMM, split over rows,
+ * partials summed in float64 in a fixed order (deterministic).              */
+int fa_pca_cov_dev(const void *x, int x_dtype, int64_t n, int D, const float *mean,
+                   double *cov, void *stream);
+
+/* out[i, j] = sum_k (X[i, k] - mean[k]) * basis[k, j] for j < d (pca.py:68-71
+ * pca_project_all), X n x D f32 or bf16, basis D x dfull f32 row-major (the
+ * rotation, columns by descending eigenvalue), out n x ldo f32.  3xTF32
+ * tcgen05 GEMM fed by TMA; fp32-class accuracy.                              */
+int fa_pca_project_dev(const void *x, int x_dtype, int64_t n, int D, const float *mean,
+                       const float *basis, int dfull, int d, float *out, int64_t ldo,
+                       void *stream);
+
+/* pca_project (pca.py:57-65) of n vectors in float64: out[i, j] = sum_k
+ * (x[i, k] - mean[k]) * basis[k, j], j < d; basis D x dfull row-major.       */
+int fa_pca_project_f64_dev(const double *x, int64_t n, int D, const double *mean,
+                           const double *basis, int dfull, int d, double *out, void *stream);
+
 /* ---- graph index (build + search) --------------------------------------- */
 
 typedef struct fa_index fa_index; /* opaque, device resident */

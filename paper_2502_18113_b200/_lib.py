@@ -16,6 +16,7 @@ from .errors import DeviceError
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libflashann_b200.so"
 
 FA_OK, FA_EINVAL, FA_ENOMEM, FA_ECUDA, FA_EOVERFLOW, FA_EEMPTY = 0, -1, -2, -3, -4, -5
+FA_DTYPE_F32, FA_DTYPE_BF16 = 0, 1
 
 vp = C.c_void_p
 i32 = C.c_int32
@@ -74,6 +75,10 @@ _SIGS = {
                                           C.c_int, vp, C.c_int, vp, vp, vp]),
     "fa_flash_range_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, vp, C.c_int, vp, vp,
                                      vp, vp]),
+    "fa_pca_cov_dev": (C.c_int, [vp, C.c_int, i64, C.c_int, vp, vp, vp]),
+    "fa_pca_project_dev": (C.c_int, [vp, C.c_int, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp,
+                                     i64, vp]),
+    "fa_pca_project_f64_dev": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]),
     "fa_index_create": (C.c_int, [C.POINTER(IndexDesc), C.POINTER(vp)]),
     "fa_index_destroy": (C.c_int, [vp]),
     "fa_index_encode": (C.c_int, [vp, vp]),

@@ -1,9 +1,12 @@
 """Rotation used by the Flash coder (flashann/providers/pca.py:27-71), on the GPU.
 
-pca_train: float64 mean, float32 centred covariance GEMM (cuBLAS, TF32 off,
-like the reference's fp32 sgemm), float64 symmetric eigendecomposition
-(cuSOLVER), components by descending eigenvalue, eigenvalues clamped at 0.
-pca_project_all: float32 (x - mean) @ basis[:, :d] on the device.
+pca_train: float64 mean, the float32-centred covariance as a 3xTF32 tcgen05
+GEMM (K9, csrc/pca_gemm.cu; the reference's fp32 sgemm, pca.py:36-38),
+float64 symmetric eigendecomposition (cuSOLVER), components by descending
+eigenvalue, eigenvalues clamped at 0.
+pca_project_all: (x - mean) @ basis[:, :d] as a 3xTF32 tcgen05 GEMM fed by
+TMA (pca.py:68-71), rows in float32 or bfloat16 (bf16 is widened exactly).
+pca_project: the reference's float64 single-vector projection (pca.py:57-65).
 
 Eigenvectors are defined up to sign (and up to rotation inside degenerate
 eigenspaces); everything downstream (codes, tables, the graph) is invariant
@@ -16,7 +19,9 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from ._arrays import is_tensor, rows_of
+from ._lib import check
 from .errors import ConfigError
 
 
@@ -35,7 +40,6 @@ def _torch():
         from .errors import DeviceError
 
         raise DeviceError("no CUDA device visible: training runs on the GPU only")
-    torch.backends.cuda.matmul.allow_tf32 = False
     return torch
 
 
@@ -46,6 +50,31 @@ def as_device_f32(data):
     return torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).cuda()
 
 
+def as_device_rows(data):
+    """Rows on the device in float32, or bfloat16 when given as a bf16 tensor
+    (the tensor-core contractions widen bf16 exactly; half the bytes)."""
+    torch = _torch()
+    if is_tensor(data) and data.dtype == torch.bfloat16:
+        return data.to(device="cuda").contiguous()
+    return as_device_f32(data)
+
+
+def _dtype_code(x) -> int:
+    torch = _torch()
+    return _lib.FA_DTYPE_BF16 if x.dtype == torch.bfloat16 else _lib.FA_DTYPE_F32
+
+
+def covariance_dev(x, mean_f32):
+    """(x - mean)^T (x - mean) / n as a float64 (D, D) device tensor (K9)."""
+    torch = _torch()
+    lib = _lib.load()
+    n, dim = x.shape
+    cov = torch.empty((dim, dim), dtype=torch.float64, device="cuda")
+    check(lib.fa_pca_cov_dev(x.data_ptr(), _dtype_code(x), n, dim, mean_f32.data_ptr(),
+                             cov.data_ptr(), None))
+    return cov
+
+
 def pca_train(sample, alpha: float | None = 0.9, d: int | None = None) -> PCAModel:
     """Fit the rotation on the device; keep d components (or the smallest d
     reaching the variance fraction alpha)."""
@@ -54,10 +83,9 @@ def pca_train(sample, alpha: float | None = 0.9, d: int | None = None) -> PCAMod
     if n < 2:
         raise ConfigError("need at least 2 vectors to fit a covariance")
     torch = _torch()
-    x = as_device_f32(data)
+    x = as_device_rows(data)
     mean = x.double().mean(0)
-    xc = x - mean.float()
-    cov = (xc.T @ xc).double() / n
+    cov = covariance_dev(x, mean.float().contiguous())
     w, v = torch.linalg.eigh(cov)
     eig = torch.clamp(torch.flip(w, [0]), min=0.0)
     basis = torch.flip(v, [1]).contiguous()
@@ -77,14 +105,38 @@ def pca_train(sample, alpha: float | None = 0.9, d: int | None = None) -> PCAMod
     return PCAModel(mean=mean.cpu().numpy(), basis=basis.cpu().numpy(), eigvals=eig_h, d=int(d))
 
 
+def _model_dev(model: PCAModel) -> dict:
+    """Device copies of the rotation (cached on the model)."""
+    cache = getattr(model, "_pca_dev", None)
+    if cache is None:
+        torch = _torch()
+        cache = {
+            "mean_f32": torch.from_numpy(model.mean.astype(np.float32)).cuda(),
+            "basis_f32": torch.from_numpy(np.ascontiguousarray(model.basis, np.float32)).cuda(),
+            "mean_f64": torch.from_numpy(np.ascontiguousarray(model.mean, np.float64)).cuda(),
+            "basis_f64": torch.from_numpy(np.ascontiguousarray(model.basis, np.float64)).cuda(),
+        }
+        model._pca_dev = cache
+    return cache
+
+
 def pca_project_all_dev(model: PCAModel, x, d: int | None = None):
-    """(x - mean) @ basis[:, :d] in float32 on the device; x on device or host."""
+    """(x - mean) @ basis[:, :d] in float32 on the device (K9); x on device or
+    host, float32 or a bfloat16 tensor."""
     torch = _torch()
+    lib = _lib.load()
     d = model.d if d is None else d
-    xd = as_device_f32(x)
-    mean = torch.from_numpy(model.mean.astype(np.float32)).cuda()
-    b = torch.from_numpy(np.ascontiguousarray(model.basis[:, :d], dtype=np.float32)).cuda()
-    return ((xd - mean) @ b).contiguous()
+    xd = as_device_rows(x)
+    n, dim = xd.shape
+    if dim != model.mean.shape[0]:
+        raise ConfigError("vector dimension mismatch")
+    m = _model_dev(model)
+    out = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    if n:
+        check(lib.fa_pca_project_dev(xd.data_ptr(), _dtype_code(xd), n, dim,
+                                     m["mean_f32"].data_ptr(), m["basis_f32"].data_ptr(),
+                                     m["basis_f32"].shape[1], d, out.data_ptr(), d, None))
+    return out
 
 
 def pca_project_all(model: PCAModel, data, d: int | None = None) -> np.ndarray:
@@ -92,14 +144,22 @@ def pca_project_all(model: PCAModel, data, d: int | None = None) -> np.ndarray:
 
 
 def pca_project(model: PCAModel, vec, d: int | None = None) -> np.ndarray:
-    """Centred projection of one vector (float64, like the reference)."""
+    """Centred projection of one vector (or rows) in float64, like the
+    reference (pca.py:57-65)."""
     torch = _torch()
+    lib = _lib.load()
     d = model.d if d is None else d
     if d > model.basis.shape[1]:
         raise ConfigError(f"d={d} exceeds basis width")
     v = np.asarray(vec, dtype=np.float64)
     if v.shape[-1] != model.mean.shape[0]:
         raise ConfigError("vector dimension mismatch")
-    vd = torch.from_numpy(v).cuda()
-    out = (vd - torch.from_numpy(model.mean).cuda()) @ torch.from_numpy(model.basis[:, :d]).cuda()
-    return out.cpu().numpy()
+    rows = np.ascontiguousarray(np.atleast_2d(v))
+    m = _model_dev(model)
+    xd = torch.from_numpy(rows).cuda()
+    out = torch.empty((rows.shape[0], d), dtype=torch.float64, device="cuda")
+    check(lib.fa_pca_project_f64_dev(xd.data_ptr(), rows.shape[0], rows.shape[1],
+                                     m["mean_f64"].data_ptr(), m["basis_f64"].data_ptr(),
+                                     m["basis_f64"].shape[1], d, out.data_ptr(), None))
+    res = out.cpu().numpy()
+    return res if v.ndim > 1 else res[0]
