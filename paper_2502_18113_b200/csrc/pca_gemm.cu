@@ -5,26 +5,36 @@
 //
 // The reference computes both in fp32 (numpy sgemm over the float32-centred
 // rows).  Here they run as 3xTF32 on tcgen05: every fp32 operand x is split
-// into hi = rna_tf32(x) and lo = x - hi (exact in fp32), and the tile product
-// accumulates lo*hi + hi*lo + hi*hi in fp32 in TMEM — fp32-class accuracy
-// (the dropped lo*lo term is 2^-22 relative) at tensor-core rate.
+// into hi = rna_tf32(x) and lo = x - hi (exact in fp32), and each stage's
+// product is hi*hi + (lo*hi + hi*lo) — fp32-class accuracy (the dropped lo*lo
+// term is 2^-22 relative) at tensor-core rate.
 //
-// One persistent CTA per SM, warp-specialised (384 threads):
+// Accumulation: the tensor core's fp32 accumulator does not round to nearest
+// (it truncates after aligning to the largest term), so a long chain of MMAs
+// into one TMEM tile drifts (4.6e-6 relative over 375 MMAs, measured, against
+// 3e-7 for the reference's sgemm).  Each stage (K = 32) therefore goes into a
+// fresh pair of TMEM accumulators — hi*hi (4 MMAs) and the two small cross
+// terms (8 MMAs, whose truncation is relative to their own 2^-11-smaller
+// magnitude) — and the epilogue warps add every stage's pair into fp32
+// running sums in registers with round-to-nearest FADDs.  Two such pairs
+// alternate, so the epilogue drains one while the tensor core fills the other.
+//
+// One persistent CTA per SM, warp-specialised (448 threads):
 //   warp 0      TMA producer: raw X tiles (and, for the projection, the
 //               pre-split basis tiles hi/lo, already in the UMMA K-major
 //               128-byte-swizzled layout) into a 2-stage shared-memory ring;
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.kind::tf32
-//               (M = 128, N = BN, K = 8) x 4 k-steps x 3 passes per stage;
-//   warp 2      TMEM allocator (2 accumulators of BN fp32 columns);
-//   warps 4-7   converters: raw tile -> centred (x - mean, the reference's
+//   warp 1      TMEM allocator and MMA issuer: one thread issues
+//               tcgen05.mma.kind::tf32 (M = 128, N = 128, K = 8), 12 per stage;
+//   warps 2-5   converters: raw tile -> centred (x - mean, the reference's
 //               fp32 subtraction; bf16 inputs are widened exactly) -> hi/lo
 //               written in the K-major SW128 layout (transposed for the
 //               covariance, whose contraction runs over the rows of X);
-//   warps 8-11  epilogue: tcgen05.ld of the accumulator (lane quarter =
-//               warp % 4) -> global fp32.
+//   warps 6-13  epilogue: tcgen05.ld of the accumulators (lane quarter =
+//               warp % 4, column half = (warp - 6) / 4) -> register sums ->
+//               global fp32 at the end of the tile.
 // Barriers: full (TMA -> converters, transaction bytes), conv (converters ->
-// MMA), empty (MMA commit -> TMA), tfull / tempty (MMA <-> epilogue, double-
-// buffered accumulators so the epilogue of one tile overlaps the next).
+// MMA), empty (MMA commit -> TMA), tfull / tempty (MMA <-> epilogue, per
+// stage, double-buffered accumulator pairs).
 //
 // The covariance is symmetric: only tiles with n-block >= m-block are
 // computed, split over K (rows of X) into per-split fp32 partials that a
@@ -43,9 +53,9 @@ namespace pg {
 
 constexpr int BM = 128;   // tile rows (MMA M, TMEM lanes)
 constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row = one stage's K
-constexpr int kThreads = 384;
+constexpr int kThreads = 448;
 constexpr int kStages = 2;
-constexpr int kConvWarp0 = 4, kEpiWarp0 = 8;
+constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -114,6 +124,16 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
            ((uint32_t)(BM >> 4) << 24);
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane (32x32b.x16)
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
+        "%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(ta));
 }
 __device__ __forceinline__ float rna_tf32(float x) {
     uint32_t r;
@@ -211,7 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    constexpr uint32_t kTmemCols = 2 * BN;
+    // two accumulator pairs (hi*hi, cross terms) of BN columns each
+    constexpr uint32_t kTmemCols = 4 * BN;
+    static_assert(4 * BN <= 512, "TMEM holds 512 fp32 columns");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -221,11 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 2) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(kTmemCols)
@@ -282,13 +304,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
+        // ===== MMA issuer: every stage into a fresh accumulator pair =====
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(BN);
             int s = 0;
             uint32_t ph = 0;
-            int it = 0;
-            for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x, ++it) {
+            uint32_t fl = 0;  // stages flushed so far (accumulator pair = fl & 1)
+            for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
                 int k0, k1;
                 bool diag = false;
                 if constexpr (COV) {
@@ -300,14 +322,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     k0 = 0;
                     k1 = p.nk;
                 }
-                const int acc = it & 1;
-                mbar_wait(tempty + acc, ((it >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t dt = tmem_base + (uint32_t)(acc * BN);
-                for (int kb = k0; kb < k1; ++kb) {
+                for (int kb = k0; kb < k1; ++kb, ++fl) {
+                    const uint32_t acc = fl & 1u;
+                    mbar_wait(tempty + acc, ((fl >> 1) & 1u) ^ 1u);
                     mbar_wait(full + s, ph);
                     mbar_wait(conv + s, ph);
                     tc_fence_after();
+                    const uint32_t d_big = tmem_base + acc * (2 * BN);
+                    const uint32_t d_small = d_big + BN;
                     uint8_t *st = smem + s * L::stage;
                     const uint32_t ahi = smem_u32(st + L::off_ahi), alo = smem_u32(st + L::off_alo);
                     const uint32_t bhi = COV && diag ? ahi : smem_u32(st + L::off_bhi);
@@ -315,18 +337,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 8; ++k) {
                         const uint32_t o = (uint32_t)k * 32u;  // 8 tf32 = 32 bytes along K
-                        const uint32_t first = (kb == k0 && k == 0) ? 0u : 1u;
-                        mma_tf32(dt, sdesc(alo + o), sdesc(bhi + o), idesc, first);
-                        mma_tf32(dt, sdesc(ahi + o), sdesc(blo + o), idesc, 1u);
-                        mma_tf32(dt, sdesc(ahi + o), sdesc(bhi + o), idesc, 1u);
+                        const uint32_t more = k > 0 ? 1u : 0u;
+                        mma_tf32(d_big, sdesc(ahi + o), sdesc(bhi + o), idesc, more);
+                        mma_tf32(d_small, sdesc(alo + o), sdesc(bhi + o), idesc, more);
+                        mma_tf32(d_small, sdesc(ahi + o), sdesc(blo + o), idesc, 1u);
                     }
-                    tc_commit(empty + s);  // frees the stage once these MMAs retire
+                    tc_commit(empty + s);       // the stage's smem is free once these retire
+                    tc_commit(tfull + acc);     // and the pair is ready for the epilogue
                     if (++s == kStages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                tc_commit(tfull + acc);
             }
         }
     } else if (warp >= kConvWarp0 && warp < kEpiWarp0) {
@@ -416,18 +438,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ===== epilogue: TMEM -> registers -> global =====
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // ===== epilogue: per stage TMEM -> register sums; per tile -> global =====
+        constexpr int HC = BN / 2;  // columns per epilogue warp (its half)
+        const int q = warp & 3;     // TMEM lane quarter this warp may access
+        const int h = (warp - kEpiWarp0) >> 2;
         const int r = 32 * q + lane;
-        int it = 0;
-        for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x, ++it) {
-            int m0, n0;
+        uint32_t fl = 0;
+        for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
+            int m0, n0, k0, k1;
             float *dst;
             int64_t ld;
             int ncol;
             if constexpr (COV) {
                 int mb, nb, sp;
                 cov_item(p, w, mb, nb, sp);
+                cov_krange(p, sp, k0, k1);
                 m0 = mb * BM;
                 n0 = nb * BM;
                 dst = p.out + (size_t)sp * p.D * p.D;
@@ -436,53 +461,54 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 m0 = (int)(w / p.nn) * BM;
                 n0 = (int)(w % p.nn) * BN;
+                k0 = 0;
+                k1 = p.nk;
                 dst = p.out;
                 ld = p.ldo;
                 ncol = p.d;
             }
             const int64_t nrow = COV ? (int64_t)p.D : p.n;
-            const int acc = it & 1;
-            mbar_wait(tfull + acc, (it >> 1) & 1);
-            tc_fence_after();
+            float sum[HC];
+#pragma unroll
+            for (int j = 0; j < HC; ++j) sum[j] = 0.f;
+            for (int kb = k0; kb < k1; ++kb, ++fl) {
+                const uint32_t acc = fl & 1u;
+                mbar_wait(tfull + acc, (fl >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * (2 * BN) +
+                                    (uint32_t)(h * HC);
+#pragma unroll
+                for (int c = 0; c < HC / 16; ++c) {
+                    uint32_t vb[16], vs[16];
+                    tmem_ld16(tb + 16 * c, vb);
+                    tmem_ld16(tb + BN + 16 * c, vs);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        sum[16 * c + j] += __uint_as_float(vb[j]) + __uint_as_float(vs[j]);
+                }
+                tc_fence_before();
+                mbar_arrive(tempty + acc);
+            }
             const int64_t row = (int64_t)m0 + r;
-            float *orow = dst + row * ld;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + 32 * c);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
-                    "%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,"
-                    "%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-                      "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]),
-                      "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(ta));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int col0 = n0 + 32 * c;
-                if (row < nrow) {
-                    if (col0 + 32 <= ncol && (ld & 3) == 0) {
+            const int col0 = n0 + h * HC;
+            if (row < nrow) {
+                float *orow = dst + row * ld;
+                if (col0 + HC <= ncol && (ld & 3) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4 *>(orow + col0 + j) =
-                                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                    } else {
+                    for (int j = 0; j < HC; j += 4)
+                        *reinterpret_cast<float4 *>(orow + col0 + j) =
+                            make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+                } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < ncol) orow[col0 + j] = __uint_as_float(v[j]);
-                    }
+                    for (int j = 0; j < HC; ++j)
+                        if (col0 + j < ncol) orow[col0 + j] = sum[j];
                 }
             }
-            tc_fence_before();
-            mbar_arrive(tempty + acc);
         }
     }
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(kTmemCols)
@@ -683,7 +709,7 @@ extern "C" int fa_pca_project_dev(const void *x, int x_dtype, int64_t n, int D,
     const bool bf = x_dtype == FA_DTYPE_BF16;
     Padded P;
     FA_TRY(pad_input(x, bf, n, D, mean, BK, st, P));
-    const int BN = d > 128 ? 256 : 128;
+    constexpr int BN = 128;
     const int ldb = (P.ldx + 3) / 4 * 4;
     float *bsplit = nullptr;
     FA_TRY(pool_alloc((void **)&bsplit, sizeof(float) * 2 * (size_t)d * ldb));
@@ -712,12 +738,8 @@ extern "C" int fa_pca_project_dev(const void *x, int x_dtype, int64_t n, int D,
     if (!rc) rc = make_map(&mbh, bhi, false, (uint64_t)ldb, (uint64_t)d, (uint64_t)ldb * 4, BK, BN, true);
     if (!rc) rc = make_map(&mbl, blo, false, (uint64_t)ldb, (uint64_t)d, (uint64_t)ldb * 4, BK, BN, true);
     if (!rc) {
-        if (BN == 256)
-            rc = bf ? launch<false, 256, __nv_bfloat16>(mx, mbh, mbl, p, st)
-                    : launch<false, 256, float>(mx, mbh, mbl, p, st);
-        else
-            rc = bf ? launch<false, 128, __nv_bfloat16>(mx, mbh, mbl, p, st)
-                    : launch<false, 128, float>(mx, mbh, mbl, p, st);
+        rc = bf ? launch<false, BN, __nv_bfloat16>(mx, mbh, mbl, p, st)
+                : launch<false, BN, float>(mx, mbh, mbl, p, st);
     }
     cudaFreeAsync(bsplit, st);
     return rc;
