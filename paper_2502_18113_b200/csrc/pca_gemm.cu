@@ -532,14 +532,14 @@ __global__ void split_basis_kernel(const float *__restrict__ basis, int D, int d
     }
 }
 
-// cov[i][j] = sum_s part[s][min-block order] / n in float64, mirrored
+// cov[i][j] = sum_s part[s][min(i,j)][max(i,j)] / n in float64 (exactly symmetric)
 __global__ void cov_reduce_kernel(const float *__restrict__ part, int nsplit, int D, double inv_n,
                                   double *__restrict__ cov) {
     const int64_t total = (int64_t)D * D;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         int i = (int)(e / D), j = (int)(e % D);
-        if (i / BM > j / BM) {  // lower-triangle block: read the mirrored tile
+        if (i > j) {  // lower triangle: the mirrored (computed) element -> exact symmetry
             const int t = i;
             i = j;
             j = t;
