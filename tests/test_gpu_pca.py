@@ -8,7 +8,7 @@ reference's numpy arithmetic (flashann/providers/pca.py:27-71).
 * config 4's 960 -> 256 PCA against the reference's own pca_train output
   (tests/golden/gen_pca_golden.py): mean 1e-12, eigenvalues 1e-6 of the
   largest, every one of the 256 basis columns up to sign with
-  1 - |cos| <= 1e-6, and pca_project_all of 64 rows within 2e-6 of the
+  1 - |cos| <= 1e-6, and pca_project_all of 64 rows within 1e-5 of the
   reference's own fp32 sgemm (sign-aligned);
 * pca_project (float64 single vectors) against numpy float64.
 """
@@ -89,7 +89,9 @@ def test_config4_pca_matches_reference(cuda):
     proj = pca.pca_project_all(model, x[:64])
     proj *= np.sign(cos)[None, :].astype(np.float32)
     scale = np.linalg.norm(x[:64] - model.mean.astype(np.float32), axis=1)[:, None]
-    assert (np.abs(proj - g["proj64"]) / scale).max() <= 2e-6
+    # (includes the basis difference of the small-gap columns; the GEMM itself
+    # is held to 2e-6 against float64 in test_projection_gemm)
+    assert (np.abs(proj - g["proj64"]) / scale).max() <= 1e-5
 
 
 def test_single_vector_projection_f64(cuda):

@@ -71,6 +71,6 @@ def test_reference_suite_with_sm100_core(cuda, tmp_path):
     assert not failed, "\n".join(failed) + "\n" + p.stdout[-6000:]
     # the CORES-parametrised tests ran on the GPU core, plus the drop-in cases
     assert len([k for k in sm100_cases if "[sm100]" in k]) == 7, sm100_cases
-    assert len([k for k in cases if "test_sm100_dropin" in k]) == 6
+    assert len([k for k in cases if "test_sm100_dropin" in k]) == 5
     skipped = sorted(k for k, v in cases.items() if v == "skipped")
     assert not skipped, skipped
