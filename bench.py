@@ -1,28 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: Flash HNSW build throughput on one B200 (BASELINE config 2).
+"""Benchmark: Flash HNSW build throughput on one B200 (BASELINE configs).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1]): 1,000,000 x 128 float32 (256-component
-mixture, rounded and clipped to 0..255; seeded synthetic), m = 64 subspaces x
-4-bit, uint8 tables, M = 32 (R), efConstruction = 200 (C).
+Headline workload (BASELINE.json configs[1]): 1,000,000 x 128 float32
+(256-component mixture, rounded and clipped to 0..255; seeded synthetic),
+m = 64 subspaces x 4-bit, uint8 tables, M = 32 (R), efConstruction = 200 (C).
 
 A "step" is one pass of the hot path over the whole input: project + encode
 every vector and insert all of them with the batched GPU build (the
 reference's graph_seconds: attach + build_graph).  The coder is trained once
-on the GPU before the timed region (reported as coding_seconds).  Inputs are
-resident in HBM when the timed region starts; the working set (vectors
-0.5 GB, adjacency 0.3 GB, codes 64 MB, visits spread over all of it) exceeds
-the 126 MB L2, so no flush is needed between steps.
+on the GPU before the timed region (reported as coding_seconds, k-means at the
+reference's default 25 iterations).  Inputs are resident in HBM when the
+timed region starts; the working set (vectors 0.5 GB, adjacency 0.3 GB, codes
+64 MB, visits spread over all of it) exceeds the 126 MB L2, so no flush is
+needed between steps.
 
 value  = vectors inserted per second (all ranks) — device time, CUDA events.
 e2e    = the same metric through the reference-facing host-array drop-in
          (sm100.build_graph: numpy in, reference-layout blocks out), H2D/D2H
          inside the timed region.
 roofline (dominant kernel = the build's search kernel) and a standalone block
-scan (K1) at the config's block shape, each against MEASURED_PEAKS.json.
+scan (K1) at the config's block shape, each against MEASURED_PEAKS.json, with
+the reference's own fa_batch_lanes (OpenMP, all host cores) timed beside it.
 cpu_baseline: the reference's own compiled core (oracle/_ref, OpenMP on all
 host cores) building a bounded prefix of the same data.
+configs: the other BASELINE workloads at full size, device-timed (config 5 =
+the dynamic rebuild: 4M bf16 vectors inserted in 65,536-vertex batches onto
+an existing 1M-vector graph), each with its roofline; pca_gemm: the K9
+tensor-core contractions (covariance, projection) at configs 4 and 5.
 
 N > 1 (torchrun): "replicas only" — each rank builds its own full index; no
 collective on the data path; value = total vectors / max time.
@@ -44,6 +50,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CFG = 2
+KMEANS_ITERS = 25  # the reference's default (builder.py StrategyParams.kmeans_iters)
 METRIC = "HNSW build vectors/sec and code-distance evals/sec (% HBM roofline), 1 B200"
 
 
@@ -168,8 +175,10 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref not built (make -C oracle ref needs /root/reference)"}))
         return
+    # prefix-stable generator: these are exactly the first ref_max rows of the
+    # GPU arm's workload
     data, _ = dataset.baseline_config(CFG, n=args.ref_max, nq=0)
-    model = train_np.train(train_np.training_sample(data, 100_000, 0), c["d_f"], c["m_f"], 0, 10)
+    model = train_np.train(train_np.training_sample(data, 100_000, 0), c["d_f"], c["m_f"], 0, 25)
     prov = cpu_prov(data, model)
     lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
     # size each step so the whole run stays within ~3 minutes
@@ -182,17 +191,19 @@ def run_reference(args):
              for _ in range(args.steps)]
     ms = 1000.0 * float(np.mean(times))
     value = n_sub / (ms / 1000.0)
-    sample = (f"first {n_sub} of {c['n']} config-2 vectors (prefix; CPU throughput falls "
-              f"with n, so this favours the CPU), build_graph threads={threads}")
+    sample = (f"first {n_sub} of {c['n']} config-2 vectors (the same rows as the GPU arm's "
+              f"prefix; CPU throughput falls with n, so this favours the CPU), "
+              f"reference compiled build_graph threads={threads}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "vectors/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded config-2 mixture, no dataset download)",
-        # the same workload as our arm; each step times a bounded prefix of
-        # it (cpu_baseline.sample)
-        "config": {"workload": f"config{CFG}", "n": c["n"], "dim": c["dim"], "M": c["M"],
-                   "efConstruction": c["efC"], "m": c["m_f"], "subspace_bits": 4},
+        # the same workload as our arm; each step times the first n rows of it
+        # (n_workload = the full workload's size; cpu_baseline.sample)
+        "config": {"workload": f"config{CFG}", "n": n_sub, "n_workload": c["n"],
+                   "dim": c["dim"], "M": c["M"], "efConstruction": c["efC"], "m": c["m_f"],
+                   "subspace_bits": 4, "prefix": True},
         "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0,
@@ -275,6 +286,7 @@ def scan_benchmark(lib, torch, m, cap, peak, reps=5):
         res[name] = {"kernel": name, "evals_per_s": lanes / (ms * 1e-3), "ms_per_launch": ms,
                      "bytes_per_launch": alg_bytes, "achieved": gbs, "peak": peak,
                      "unit": "GB/s", "frac": gbs / peak}
+    cpu = scan_cpu_baseline(torch, blocks, stride, codes_off, cap, m, adt, nb)
     del blocks
     best = max(res.values(), key=lambda r: r["achieved"])
     # ncu DRAM bytes of one launch of the TMA variant at the config-2 shape
@@ -286,7 +298,211 @@ def scan_benchmark(lib, torch, m, cap, peak, reps=5):
                 shape=f"m={m} cap={cap}, {nq} queries x {ns} random blocks of {nblocks} "
                       f"(working set {nblocks * stride / 1e9:.2f} GB > L2)",
                 variants={k: {"achieved": v["achieved"], "frac": v["frac"],
-                              "ms_per_launch": v["ms_per_launch"]} for k, v in res.items()})
+                              "ms_per_launch": v["ms_per_launch"]} for k, v in res.items()},
+                cpu_baseline=cpu)
+
+def scan_cpu_baseline(torch, blocks, stride, codes_off, cap, m, adt, nb, target_s=6.0):
+    """The reference's own fa_batch_lanes (its widest ISA kernel, OpenMP on all
+    host cores; oracle/scan_bench.c against _simd.h:180-197) over the same
+    block layout and tables: a host copy of the first 262,144 blocks (> the
+    host's L3), random selections, sized to ~target_s seconds."""
+    import ctypes as C
+
+    from oracle import refpkg
+
+    if not refpkg.SCAN_SO.exists():
+        return None
+    lib = C.CDLL(str(refpkg.SCAN_SO))
+    lib.scan_bench.restype = C.c_int64
+    lib.scan_bench.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                               C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int]
+    lib.scan_bench_widest_kernel.restype = C.c_int
+    kern = lib.scan_bench_widest_kernel()
+    nblk = min(262_144, blocks.shape[0])
+    hb = blocks[:nblk].cpu().numpy()
+    ha = adt.cpu().numpy()
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    ns = 256
+
+    def run(nq):
+        sel = rng.integers(0, nblk, size=(nq, ns), dtype=np.int32)
+        out = np.empty(nq, np.uint64)
+        t0 = time.perf_counter()
+        lanes = lib.scan_bench(ha.ctypes.data, nq, hb.ctypes.data, stride, codes_off, cap, m,
+                               sel.ctypes.data, ns, out.ctypes.data, threads, kern)
+        return lanes, time.perf_counter() - t0
+
+    nq = 64
+    lanes, dt = run(nq)
+    while dt < target_s / 4 and nq < ha.shape[0]:
+        nq = min(ha.shape[0], nq * 4)
+        lanes, dt = run(nq)
+    evals = lanes / dt
+    bytes_s = nq * ns * (4 + nb * 16 * (m + 4)) / dt
+    return {"evals_per_s": evals, "gbs": bytes_s / 1e9, "cores": threads, "kind": "reference",
+            "kernel": ["scalar", "vector128", "vector256", "vector512"][kern],
+            "sample": f"{nq} queries x {ns} random blocks of {nblk} (host copy, "
+                      f"{nblk * stride / 1e9:.2f} GB), {dt:.1f} s"}
+
+
+def _device_sample(torch, x, size, seed=0):
+    """training_sample (builder.py:60-65 semantics) of device rows: `size` rows
+    in ascending order, chosen without replacement by a seeded device RNG."""
+    n = x.shape[0]
+    if n <= size:
+        return x
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    sel = torch.randperm(n, generator=g, device="cuda")[:size].sort().values
+    return x[sel].contiguous()
+
+
+def config_leg(cfg, torch, peak, tf32_peak, steps=2, warmup=3, cpu_seconds=0.0):
+    """One BASELINE workload at full size, device-timed.  Configs 1/3/4: full
+    builds (project + encode + insert every vector) as the headline.  Config
+    5 (dynamic rebuild): each step first rebuilds the existing 1M-vector graph
+    (untimed), then times projecting + encoding the 4M arriving bf16 vectors
+    and inserting them in 65,536-vertex batches onto it."""
+    from paper_2502_18113_b200 import _lib, builder, dataset, flash, graph, pca
+
+    lib = _lib.load()
+    c = dataset.CONFIGS[cfg]
+    n = c["n"]
+    t0 = time.perf_counter()
+    x = dataset.baseline_config_dev(cfg, n)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    sample = _device_sample(torch, x, builder.DEFAULT_SAMPLE)
+    model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=KMEANS_ITERS)
+    params = graph.BuildParams(C=c["efC"], R=c["M"], seed=0)
+    levels = graph.assign_layers(n, 0, c["M"])
+    provider = flash.FlashProvider(model)
+    provider.attach(x, vecs_dev=x)
+    g = graph.GraphIndex(n, c["dim"], params, "flash", model.m, levels)
+    g.create_device(provider)
+    split = 1_000_000 if cfg == 5 else 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step(profile=0):
+        if split:
+            provider.reproject(0, split)
+            _lib.check(lib.fa_index_set_codes(g.handle, provider.dev["codes"].data_ptr(),
+                                              provider.dev["codes"].shape[1], None))
+            builder.build_device(g, provider, params, end=split)
+            torch.cuda.synchronize()
+            e0.record()
+            provider.reproject(split, n)
+            _lib.check(lib.fa_index_set_codes(g.handle, provider.dev["codes"].data_ptr(),
+                                              provider.dev["codes"].shape[1], None))
+            r = builder.build_device(g, provider, params, start=split, profile=profile)
+            e1.record()
+        else:
+            torch.cuda.synchronize()
+            e0.record()
+            provider.reproject()
+            _lib.check(lib.fa_index_set_codes(g.handle, provider.dev["codes"].data_ptr(),
+                                              provider.dev["codes"].shape[1], None))
+            r = builder.build_device(g, provider, params, profile=profile)
+            e1.record()
+        torch.cuda.synchronize()
+        return r, e0.elapsed_time(e1)
+
+    for _ in range(warmup):
+        step()
+    times, ctr = [], None
+    for _ in range(steps):
+        ctr, ms = step()
+        times.append(ms)
+    ms = float(np.mean(times))
+    ninsert = n - split
+    prof, _ = step(profile=1)
+    mp = c["m_f"]
+    evals = 16 * prof["kernel_calls"]
+    sbytes = evals * (mp + 4) + prof["visited"] * 4
+    gbs = sbytes / (prof["ms_search"] * 1e-3) / 1e9
+    kernel_ms = {"encode": prof["ms_encode"], "search": prof["ms_search"],
+                 "sort": prof["ms_sort"], "reverse": prof["ms_reverse"]}
+    leg = {"workload": f"config{cfg}", "n": n, "dim": c["dim"], "M": c["M"],
+           "efConstruction": c["efC"], "m": mp, "d_f": c["d_f"],
+           "dtype_in": "bf16" if cfg == 5 else "f32",
+           "data": "synthetic, generated on the device (dataset.baseline_config_dev: the "
+                   "config's law, seeded)",
+           "value": ninsert / (ms * 1e-3), "unit": "vectors/s", "ms_per_step": ms,
+           "steps": steps, "warmup": warmup, "generated_s": gen_s,
+           "kernel_ms_per_step": kernel_ms,
+           "counters": {k: ctr[k] for k in ("dist_comps", "visited", "kernel_calls",
+                                            "reverse_prunes", "n_batches")},
+           "gpu_launches": int(ctr["launches"]),
+           "roofline": {"bound": "hbm", "kernel": "build_search_kernel (K4+K5)",
+                        "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "traffic": None, "evals_per_s": evals / (prof["ms_search"] * 1e-3),
+                        "bytes_basis": "SURVEY 8(d): 16 x kernel_calls x (m + 4) B + 4 B "
+                                       "per block",
+                        "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}}
+    if split:
+        leg["timed"] = (f"project + encode + insert vectors {split}..{n} in batches of "
+                        f"{builder.build_options(params).batch_max} onto the existing "
+                        f"{split}-vector graph (rebuilt untimed before each step)")
+    if cfg in (4, 5):
+        # K9 at this config's shapes: the training covariance and the full
+        # projection (the timed steps above include the projection)
+        mean = torch.from_numpy(model.pca.mean.astype(np.float32)).cuda()
+
+        def ktime(fn, reps=3):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        ms_cov = ktime(lambda: pca.covariance_dev(sample, mean))
+        ms_proj = ktime(lambda: pca.pca_project_all_dev(model.pca, x))
+        D, d = c["dim"], c["d_f"]
+        ns = sample.shape[0]
+        # flops of the tiles the kernel computes (covariance: the upper
+        # triangle of 128 x 128 tiles incl. the diagonal); the tensor core
+        # issues 3x that (3xTF32)
+        nbk = -(-D // 128)
+        fl_cov = 2.0 * 128 * 128 * ns * nbk * (nbk + 1) / 2
+        fl_proj = 2.0 * n * D * d
+        leg["pca_gemm"] = {
+            "kernel": "pca_gemm_kernel (K9, 3xTF32 tcgen05, TMA)", "bound": "tensor",
+            "unit": "TFLOP/s", "peak": tf32_peak,
+            "peak_basis": "MEASURED_PEAKS bf16_tflops / 2 (dense tf32 rate)",
+            "covariance": {"rows": ns, "D": D, "ms": ms_cov,
+                           "achieved": 3 * fl_cov / (ms_cov * 1e9),
+                           "frac": 3 * fl_cov / (ms_cov * 1e9) / tf32_peak},
+            "projection": {"rows": n, "D": D, "d": d, "ms": ms_proj,
+                           "achieved": 3 * fl_proj / (ms_proj * 1e9),
+                           "frac": 3 * fl_proj / (ms_proj * 1e9) / tf32_peak,
+                           "hbm_gbs": x.element_size() * n * D / (ms_proj * 1e6)},
+            "flops_basis": "tensor-core flops issued = 3 x useful (hi*hi, lo*hi, hi*lo)"}
+    if cpu_seconds > 0:
+        lvf = lambda k: graph.assign_layers(k, 0, c["M"])  # noqa: E731
+        ncap = 400_000
+        pv = {"vecs": x[:ncap].float().cpu().numpy(), "dim": c["dim"],
+              "proj": provider.dev["proj"][:ncap].cpu().numpy(),
+              "codes": np.ascontiguousarray(provider.dev["codes"][:ncap, :mp].cpu().numpy()),
+              "cent": model.cent, "dims": model.dims, "offs": model.offs, "sdt": model.sdt,
+              "dist_min": model.dist_min, "delta": model.delta}
+        threads = os.cpu_count() or 1
+        r = size_cpu_sample(lambda k: ref_cpu_build(pv, lvf, k, c["efC"], c["M"], threads),
+                            ncap, cpu_seconds)
+        if r is not None:
+            n_cpu, dt, rate = r
+            leg["cpu_baseline"] = {
+                "value": rate, "unit": "vectors/s", "cores": threads, "kind": "reference",
+                "sample": f"first {n_cpu} vectors built from scratch (the CPU cannot build the "
+                          f"1M base in-run), same coder, reference compiled build_graph, "
+                          f"OpenMP threads={threads}, {dt:.1f} s"}
+    g.close()
+    del provider, g, x, sample
+    torch.cuda.empty_cache()
+    return leg
 
 
 def main():
@@ -301,6 +517,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-search", action="store_true", help="skip the query-search leg")
+    ap.add_argument("--configs", default="1,3,4,5",
+                    help="other BASELINE configs to time at full size ('' = none)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -332,7 +550,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sample = builder.training_sample(data, builder.DEFAULT_SAMPLE, 0)
-        model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=10)
+        model = flash.flash_train(sample, c["d_f"], c["m_f"], seed=0, kmeans_iters=KMEANS_ITERS)
         torch.cuda.synchronize()
         coding.append(time.perf_counter() - t0)
     coding_s = coding[-1]
@@ -410,6 +628,7 @@ def main():
                       "l2": "inputs larger than L2 (no flush)",
                       "batch": {k: v for k, v in sm100.BUILD_OPTIONS.items() if k != "profile"}},
            "coding_seconds": coding_s, "coding_seconds_cold": coding[0],
+           "coding_kmeans_iters": KMEANS_ITERS,
            "kernel_ms_per_build": kernel_ms,
            "counters": {k: ctrs[-1][k] for k in ("dist_comps", "sym_comps", "visited",
                                                   "kernel_calls", "reverse_prunes",
@@ -473,6 +692,18 @@ def main():
                     "sample": f"first {n_cpu} of {n} vectors (prefix, same model), reference "
                               f"compiled build_graph, OpenMP threads={threads}, {dt:.1f} s"}
             del pm, train_np
+        # the other BASELINE workloads at full size (after the headline, so
+        # its timed region and clock samples are untouched)
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+            if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        tf32_peak = float(peaks.get("bf16_tflops", 2250.0)) / 2.0
+        legs = {}
+        for cf in [int(v) for v in args.configs.split(",") if v.strip()]:
+            legs[f"config{cf}"] = config_leg(
+                cf, torch, peak, tf32_peak,
+                cpu_seconds=args.cpu_seconds if (cf == 5 and not args.no_cpu_baseline) else 0.0)
+        if legs:
+            out["configs"] = legs
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -210,6 +210,12 @@ typedef struct {
                              pop / row+visited / distances / acceptance (0
                              unless built with FA_PHASE_PROFILE=1),
                              forward-selection cycles, distance evaluations   */
+    int64_t start, end;   /* insert vertices [start, end) (end 0 = n).  start 0
+                             resets the graph; start > 0 resumes a graph whose
+                             vertices [0, start) were inserted by earlier
+                             calls (the dynamic-rebuild workload: batches onto
+                             an existing graph).  Batches never straddle
+                             start or end.                                    */
 } fa_build_opts;
 
 typedef struct {

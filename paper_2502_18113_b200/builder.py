@@ -78,7 +78,8 @@ def train_provider(strategy: str, sample, sp: StrategyParams, seed: int = 0):
                                      kmeans_iters=sp.kmeans_iters))
 
 
-def build_options(params: graph.BuildParams, **overrides) -> _lib.BuildOpts:
+def build_options(params: graph.BuildParams, start: int = 0, end: int = 0,
+                  **overrides) -> _lib.BuildOpts:
     from . import sm100
 
     o = dict(sm100.BUILD_OPTIONS)
@@ -86,17 +87,19 @@ def build_options(params: graph.BuildParams, **overrides) -> _lib.BuildOpts:
     return _lib.BuildOpts(C=params.C, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
                           seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
                           profile=o.get("profile", 0), tie=o.get("tie", 2),
-                          expand=o.get("expand", 1))
+                          expand=o.get("expand", 1), start=int(start), end=int(end))
 
 
 def build_device(g: graph.GraphIndex, provider: FlashProvider, params: graph.BuildParams,
-                 stream=None, **overrides) -> dict:
-    """Batched insertion of every vertex on the device index of `g`."""
+                 stream=None, start: int = 0, end: int = 0, **overrides) -> dict:
+    """Batched insertion on the device index of `g`: every vertex, or the
+    range [start, end) — start > 0 resumes the graph the earlier calls built
+    (vertices [0, start)), the dynamic-rebuild workload of BASELINE config 5."""
     lib = _lib.load()
     if g.handle is None:
         g.create_device(provider)
     res = _lib.BuildResult()
-    opts = build_options(params, **overrides)
+    opts = build_options(params, start=start, end=end, **overrides)
     check(lib.fa_index_build(g.handle, C.byref(opts), C.byref(res), stream))
     g.entry_point = int(res.entry_point)
     g.max_layer = int(res.max_layer)

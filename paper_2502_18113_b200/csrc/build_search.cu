@@ -110,11 +110,28 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
                     g.consU[r] = 0;
                 }
             }
+            // reverse requests (row << 32 | x), counted per target row; the
+            // batch's touched rows are listed for the bucketing (reverse.cu)
             unsigned long long *lreq = myreq + (size_t)(top - layer) * R;
-            for (int j = lane; j < R; j += 32)
-                lreq[j] = j < nsel ? ((unsigned long long)row_global(g, layer, kept[j]) << 32) |
-                                         (uint32_t)x
-                                   : KEY_MAX;
+            for (int j0 = 0; j0 < R; j0 += 32) {
+                const int j = j0 + lane;
+                unsigned long long key = KEY_MAX;
+                bool first = false;
+                int64_t rg = 0;
+                if (j < nsel) {
+                    rg = row_global(g, layer, kept[j]);
+                    key = ((unsigned long long)rg << 32) | (uint32_t)x;
+                    first = atomicAdd(g.rowcnt + rg, 1) == 0;
+                }
+                if (j < R) lreq[j] = key;
+                const unsigned fb = __ballot_sync(0xffffffffu, first);
+                if (fb) {
+                    int tb = 0;
+                    if (lane == 0) tb = atomicAdd(g.ntouched, __popc(fb));
+                    tb = __shfl_sync(0xffffffffu, tb, 0);
+                    if (first) g.touched[tb + __popc(fb & ((1u << lane) - 1u))] = (int32_t)rg;
+                }
+            }
             cur = to.back((uint32_t)key_id(ws.T[0]));
             curd = key_d(ws.T[0]);
             __syncwarp();

@@ -7,8 +7,6 @@
 // edges of the batch are grouped by target row and applied in ascending x.
 // The batch schedule is a pure function of the layer draws, so the whole
 // build is enqueued without a host round trip.
-#include <cub/cub.cuh>
-
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -42,6 +40,7 @@ struct fa_index {
     int32_t *upper_owner = nullptr;
     uint32_t *gvis = nullptr, *gvis_epoch = nullptr, *gvis_owner = nullptr;  // global visited tier
     int search_tie = 0;
+    int64_t n_inserted = 0;  // vertices [0, n_inserted) are in the graph
     int64_t entry = -1;
     int max_layer = -1;
 };
@@ -329,6 +328,10 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.gvis_owner = nullptr;
     g.gvis_log2 = 14;
     g.gvis_nslots = 0;
+    g.rowcnt = nullptr;
+    g.touched = nullptr;
+    g.ntouched = nullptr;
+    g.seg_scratch = nullptr;
     // host copies of the layer draws drive the batch schedule
     ix->levels_h.resize(g.n);
     ix->uoff_h.resize(g.n);
@@ -458,12 +461,23 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     res->entry_point = -1;
     res->max_layer = -1;
     const auto t_host0 = std::chrono::steady_clock::now();
-    FA_TRY(reset_graph(ix, st));
+    const int64_t r0 = opts->start, r1 = opts->end > 0 ? opts->end : g.n;
+    FA_CHECK_ARG(r0 >= 0 && r0 <= r1 && r1 <= g.n, "insertion range [%lld, %lld) outside [0, %lld]",
+                 (long long)r0, (long long)r1, (long long)g.n);
+    FA_CHECK_ARG(r0 == 0 || r0 == ix->n_inserted,
+                 "resuming at %lld but the graph holds %lld inserted vertices", (long long)r0,
+                 (long long)ix->n_inserted);
     FA_CHECK_ARG(opts->tie >= 0 && opts->tie <= 2, "tie mode must be 0, 1 or 2");
+    if (r0 == 0) {
+        FA_TRY(reset_graph(ix, st));
+        ix->n_inserted = 0;
+        ix->entry = -1;
+        ix->max_layer = -1;
+    }
     Graph gb = g;  // the build's view: its own tie order
     gb.tie = opts->tie;
     gb.expand = opts->expand > 1 ? std::min(opts->expand, kMaxExpand) : 1;
-    if (g.n == 0) {
+    if (g.n == 0 || r1 == 0) {
         ix->entry = -1;
         ix->max_layer = -1;
         return FA_OK;
@@ -490,12 +504,14 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
     }
     std::vector<Batch> batches;
-    int ep = 0, ml = ix->levels_h[0];
+    // vertex 0 seeds an empty graph; a resumed build starts from the state
+    // the earlier calls left (entry point, top layer)
+    int ep = r0 == 0 ? 0 : (int)ix->entry, ml = r0 == 0 ? ix->levels_h[0] : ix->max_layer;
     int64_t maxreq = 0;
     int maxB = 1;
-    int64_t x = 1;
+    int64_t x = std::max<int64_t>(1, r0);
     size_t ri = 0;  // next record position at or after x
-    while (x < g.n) {
+    while (x < r1) {
         while (ri < ix->raisers.size() && ix->raisers[ri] < x) ++ri;
         Batch b;
         b.start = (int)x;
@@ -508,7 +524,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             b.nreq = (int64_t)(ml + 1) * R;
         } else {
             const int B = x < prefix ? 1 : std::max(1, std::min(Bmax, (int)(frac * (double)x)));
-            int64_t end = std::min<int64_t>(g.n, x + B);
+            int64_t end = std::min<int64_t>(r1, x + B);
             if (ri < ix->raisers.size()) end = std::min<int64_t>(end, ix->raisers[ri]);
             size = (int)(end - x);
             b.nreq = (int64_t)R * (size + (ix->lvl_prefix[end] - ix->lvl_prefix[x]));
@@ -591,18 +607,16 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
-    int32_t *order_d = nullptr;
+    int32_t *order_d = nullptr, *rowcnt = nullptr, *rowoff = nullptr, *touched = nullptr;
     int *err = nullptr, *nheads = nullptr, *next_seg = nullptr;
-    void *cub_tmp = nullptr;
-    size_t cub_bytes = 0;
     int rc = FA_OK;
     // scratch is stream-ordered (cudaMallocAsync from the device's pool, kept
     // cached across builds): no allocation or free synchronises the device
     auto cleanup = [&]() {
         for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
-                        (void *)req_off_d, (void *)order_d, (void *)err, cub_tmp, (void *)heads,
-                        (void *)nheads,
-                        (void *)next_seg, (void *)sdtT, (void *)rev_sel})
+                        (void *)req_off_d, (void *)order_d, (void *)err, (void *)heads,
+                        (void *)nheads, (void *)next_seg, (void *)sdtT, (void *)rev_sel,
+                        (void *)rowcnt, (void *)rowoff, (void *)touched})
             if (p) cudaFreeAsync(p, st);
     };
     auto dev_alloc = [&](void **p, size_t bytes) -> int {
@@ -614,32 +628,22 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         return FA_OK;
     };
     keep_pool();  // scratch stays mapped in the pool between builds
-    int end_bit = 32;
-    {
-        int64_t rows = g.n + g.nU;
-        int b = 0;
-        while ((1ll << b) <= rows) ++b;
-        end_bit = 32 + b;
-        if (end_bit > 64) end_bit = 64;
-    }
+    const int64_t nrows = g.n + g.nU;  // layer-0 rows, then the upper rows
     if ((rc = dev_alloc((void **)&adt_batch, (size_t)maxB * g.mpad * 16)) ||
         (rc = dev_alloc((void **)&req, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
-        (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
+        (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * (std::max<int64_t>(maxreq, 1) + 1))) ||
+        (rc = dev_alloc((void **)&rowcnt, sizeof(int32_t) * nrows)) ||
+        (rc = dev_alloc((void **)&rowoff, sizeof(int32_t) * nrows)) ||
+        (rc = dev_alloc((void **)&touched, sizeof(int32_t) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&ctr, sizeof(unsigned long long) * 8)) ||
         (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
         (rc = dev_alloc((void **)&order_d, sizeof(int32_t) * g.n)) ||
         (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
-        (rc = dev_alloc((void **)&nheads, 2 * sizeof(int))) ||
+        (rc = dev_alloc((void **)&nheads, 3 * sizeof(int))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
         (rc = dev_alloc((void **)&sdtT, sdt_bytes)) ||
         (rc = dev_alloc((void **)&rev_sel, (size_t)rev_ctas * kReverseWarps * rev_sel_bytes)) ||
         (rc = dev_alloc((void **)&err, sizeof(int)))) {
-        cleanup();
-        return rc;
-    }
-    cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, req, req_sorted, (int)std::max<int64_t>(maxreq, 1),
-                                   0, end_bit, st);
-    if ((rc = dev_alloc(&cub_tmp, cub_bytes))) {
         cleanup();
         return rc;
     }
@@ -653,6 +657,12 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }                                                                                \
     } while (0)
     FA_BUILD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 8, st));
+    // per-row request counts: zero here, re-zeroed by the reverse warps
+    FA_BUILD_CUDA(cudaMemsetAsync(rowcnt, 0, sizeof(int32_t) * nrows, st));
+    gb.rowcnt = rowcnt;
+    gb.touched = touched;
+    gb.ntouched = nheads;  // nheads[0]: touched rows = row segments of the batch
+    gb.seg_scratch = req;  // the unbucketed requests are dead once scattered
     if (!exact) {
         transpose_sdt_kernel<<<1, 256, 0, st>>>(ix->d.sdt, g.m, sdtT);
         FA_BUILD_CUDA(cudaGetLastError());
@@ -686,7 +696,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         fprintf(stderr, "[fa timing] build host setup (schedule, scratch) %8.2f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                           t_host0).count());
-    int64_t launches = 3;  // the two row resets of reset_graph, the SDT transpose
+    int64_t launches = r0 == 0 ? 3 : 1;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
         if (ix->late_hook && ix->late_from >= 0 && (int64_t)b.start + b.size > ix->late_from) {
@@ -729,8 +739,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             FA_BUILD_CUDA(cudaMemcpyAsync(req_off_d + b.start, ro, sizeof(int64_t) * b.size,
                                           cudaMemcpyHostToDevice, st));
         }
-        // nheads[0]: reverse row heads, nheads[1]: the search's work counter
-        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 2 * sizeof(int), st));
+        // nheads[0]: touched rows (= row segments), nheads[1]: the search's
+        // work counter, nheads[2]: the bucketing cursor
+        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 3 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
         search_fn<<<grid, bw * 32, smem_search, st>>>(
             gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
@@ -738,13 +749,18 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
-        size_t tb = cub_bytes;
-        FA_BUILD_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, req, req_sorted, (int)b.nreq, 0,
-                                                     end_bit, st));
+        // bucket the requests by row: segments for the touched rows, then
+        // every request into its row's segment (no sort; reverse.cu)
+        {
+            const int bgrid = (int)std::min<int64_t>(num_sms() * 4, (b.nreq + 255) / 256 + 1);
+            bucket_place_kernel<<<bgrid, 256, 0, st>>>(touched, nheads, rowcnt, rowoff, heads,
+                                                        nheads + 2);
+            bucket_scatter_kernel<<<bgrid, 256, 0, st>>>(req, b.nreq, rowcnt, rowoff, nheads + 2,
+                                                          req_sorted);
+            FA_BUILD_CUDA(cudaMemsetAsync(next_seg, 0, sizeof(int), st));
+            FA_BUILD_CUDA(cudaGetLastError());
+        }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 3], st));
-        reverse_heads_kernel<<<(int)((b.nreq + 255) / 256), 256, 0, st>>>(req_sorted, b.nreq,
-                                                                         heads, nheads, next_seg);
-        FA_BUILD_CUDA(cudaGetLastError());
         // persistent warps pull row segments; never more warps than requests
         int rgrid = (int)std::min<int64_t>(rev_ctas, (b.nreq + 32 * kReverseWarps - 1) /
                                                           (32 * kReverseWarps) + 1);
@@ -761,7 +777,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                 ix->upper_owner, RL, ctr, rev_sel, rev_sel_bytes);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 4], st));
-        launches += 4;
+        launches += 5;
     }
     unsigned long long hc[8];
     int herr = 0;
@@ -799,6 +815,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     }
     ix->entry = ep;
     ix->max_layer = ml;
+    ix->n_inserted = r1;
     res->entry_point = ep;
     res->max_layer = ml;
     res->n_batches = (int32_t)batches.size();

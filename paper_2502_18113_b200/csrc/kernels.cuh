@@ -108,9 +108,11 @@ struct ReverseLayout {
     }
 };
 
-__global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys, int64_t N,
-                                     int64_t *__restrict__ heads, int *__restrict__ nheads,
-                                     int *__restrict__ next);
+__global__ void bucket_place_kernel(const int32_t *touched, const int *ntouched, int32_t *rowcnt,
+                                    int32_t *rowoff, int64_t *heads, int *cursor);
+__global__ void bucket_scatter_kernel(const unsigned long long *req, int64_t N, int32_t *fill,
+                                      const int32_t *rowoff, const int *cursor,
+                                      unsigned long long *out);
 
 template <int RC>
 __global__ void reverse_kernel(Graph g, const uint8_t *__restrict__ sdt,

@@ -1,10 +1,16 @@
 // K6: grouped reverse-edge insertion (reverse_add, _core.pyx:441-477).
 //
 // The batch's forward selections emit requests (row(y, layer) << 32 | x);
-// after a radix sort each row's incoming x arrive ascending, which is the
-// order the sequential reference applies them in.  reverse_heads_kernel lists
-// the row segments; reverse_kernel's warps pull segments dynamically and
-// replay the reference's per-edge rule exactly:
+// each row applies its incoming x in ascending order, which is the order the
+// sequential reference applies them in.  The requests are bucketed
+// by row without a sort: the search kernel counts each target row and lists
+// the rows a batch touches; bucket_place_kernel gives every touched row a
+// contiguous segment (its head), bucket_scatter_kernel drops each request
+// into its row's segment (in arbitrary order), and the reverse warp that
+// owns the segment applies its requests in ascending x (a warp minimum per
+// step for segments of <= 32, a rank sort into scratch for longer ones).
+// reverse_kernel's warps pull segments dynamically and replay the
+// reference's per-edge rule exactly:
 //   count < cap : append x (write_code_slot + id, count+1)
 //   count == cap: d(y,u) = sdt-sum for all cap+1 candidates, sort by (d, id)
 //                 (fa_sort_pairs), select_heur(cap), rewrite the row.
@@ -41,23 +47,88 @@ __device__ __forceinline__ uint32_t sdt_sum16(const uint8_t *tab, int m,
     return acc > 255u ? 255u : acc;
 }
 
-// Segment heads of the sorted request keys (first key of every row).
-__global__ void reverse_heads_kernel(const unsigned long long *__restrict__ keys, int64_t N,
-                                     int64_t *__restrict__ heads, int *__restrict__ nheads,
-                                     int *__restrict__ next) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i == 0) *next = 0;
-    bool h = false;
-    if (i < N) {
-        unsigned long long k = keys[i];
-        h = k != KEY_MAX && (i == 0 || (keys[i - 1] >> 32) != (k >> 32));
+// Segments of the touched rows: row touched[t] gets [heads[t], heads[t] +
+// rowcnt[row]), allocated in warp-sized groups from *cursor; rowcnt of the
+// row is reset to 0 (bucket_scatter_kernel counts it up again as its fill
+// pointer; the reverse warp zeroes it once the segment is applied).
+__global__ void bucket_place_kernel(const int32_t *__restrict__ touched,
+                                    const int *__restrict__ ntouched, int32_t *__restrict__ rowcnt,
+                                    int32_t *__restrict__ rowoff, int64_t *__restrict__ heads,
+                                    int *__restrict__ cursor) {
+    const int nt = *ntouched;
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int t0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; t0 < nt; t0 += warps * 32) {
+        const int t = t0 + lane;
+        int row = 0, c = 0;
+        if (t < nt) {
+            row = touched[t];
+            c = rowcnt[row];
+            rowcnt[row] = 0;
+        }
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int base = 0;
+        if (lane == 31) base = atomicAdd(cursor, incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        if (t < nt) {
+            rowoff[row] = base + incl - c;
+            heads[t] = base + incl - c;
+        }
     }
-    const unsigned b = __ballot_sync(0xffffffffu, h);
-    int base = 0;
-    if ((threadIdx.x & 31) == 0 && b) base = atomicAdd(nheads, __popc(b));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (h) heads[base + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = i;
 }
+
+// Every request into its row's segment; out[total] = KEY_MAX terminates the
+// last segment (segments of different rows abut, so a row change ends one).
+__global__ void bucket_scatter_kernel(const unsigned long long *__restrict__ req, int64_t N,
+                                      int32_t *__restrict__ fill,
+                                      const int32_t *__restrict__ rowoff,
+                                      const int *__restrict__ cursor,
+                                      unsigned long long *__restrict__ out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[*cursor] = KEY_MAX;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = req[i];
+        if (k == KEY_MAX) continue;
+        const int64_t row = (int64_t)(k >> 32);
+        out[rowoff[row] + atomicAdd(fill + row, 1)] = k;
+    }
+}
+
+// The segment [h, e) of one row in ascending x: segments of <= 32 requests
+// stay in registers (lane j: the j-th key, unordered) and each step takes
+// the warp minimum; longer ones are rank-sorted into g.seg_scratch[h, e).
+struct SegOrder {
+    uint32_t kx;                           // this lane's unconsumed x (~0 = none)
+    const unsigned long long *sorted;      // long segments: the ordered keys
+    __device__ __forceinline__ void init(const Graph &g, const unsigned long long *keys,
+                                         unsigned long long kk, int64_t h, int64_t e, int lane) {
+        const int64_t L = e - h;
+        sorted = nullptr;
+        kx = lane < L ? (uint32_t)kk : 0xffffffffu;
+        if (L > 32) {
+            for (int64_t j = lane; j < L; j += 32) {
+                const unsigned long long kj = keys[h + j];
+                int64_t r = 0;
+                for (int64_t i = 0; i < L; ++i) r += keys[h + i] < kj;
+                g.seg_scratch[h + r] = kj;
+            }
+            __syncwarp();
+            sorted = g.seg_scratch;
+        }
+    }
+    // x of the t-th request (t = h, h + 1, ... in order)
+    __device__ __forceinline__ int next(int64_t t) {
+        if (sorted) return (int)(sorted[t] & 0xffffffffu);
+        const uint32_t m = __reduce_min_sync(0xffffffffu, kx);
+        if (kx == m) kx = 0xffffffffu;
+        return (int)m;
+    }
+};
 
 // RC: row chunks of 32 slots compiled in (cap <= 32 RC)
 // 64 registers: 32 warps per SM (the kernel is latency-bound; its shared
@@ -134,11 +205,11 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
             if (i < g.m) cyl |= (uint32_t)__ldg(cy + i) << (8 * k);
         }
         bool dirty = false;
+        SegOrder so;
+        so.init(g, keys, kk, h, e, lane);
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
-            const unsigned long long kt =
-                t - h < 32 ? __shfl_sync(0xffffffffu, kk, (int)(t - h)) : keys[t];
-            const int x = (int)(kt & 0xffffffffu);
+            const int x = so.next(t);
             if (cnt < cap) {
                 if (lane == 0) row_s[cnt] = x;
                 ++cnt;
@@ -296,6 +367,7 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
                 *consp = (uint8_t)cons;
             }
         }
+        if (lane == 0) g.rowcnt[rowg] = 0;  // the row's bucket count, for the next batch
         __syncwarp();
     }
     if (lane == 0 && (n_prune | n_app)) {
@@ -341,10 +413,15 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         s = __shfl_sync(0xffffffffu, s, 0);
         if (s >= nseg) break;
         const int64_t h = heads[s];
-        const unsigned long long hk = keys[h];
+        const unsigned long long kk = h + lane < N ? keys[h + lane] : KEY_MAX;
+        const unsigned long long hk = __shfl_sync(0xffffffffu, kk, 0);
         const int64_t rowg = (int64_t)(hk >> 32);
         int64_t e = -1;
-        for (int64_t b = h + 1; e < 0; b += 32) {
+        {
+            const unsigned nb = __ballot_sync(0xffffffffu, (kk >> 32) != (hk >> 32));
+            if (nb) e = h + __ffs(nb) - 1;
+        }
+        for (int64_t b = h + 32; e < 0; b += 32) {
             const int64_t j = b + lane;
             const bool same = j < N && (keys[j] >> 32) == (hk >> 32);
             const unsigned nb = __ballot_sync(0xffffffffu, !same);
@@ -366,9 +443,11 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         }
         const float *vy = g.vecs + (size_t)y * g.dim;
         bool have_y = false, dirty = false;
+        SegOrder so;
+        so.init(g, keys, kk, h, e, lane);
         __syncwarp();
         for (int64_t t = h; t < e; ++t) {
-            const int x = (int)(keys[t] & 0xffffffffu);
+            const int x = so.next(t);
             if (cnt < cap) {
                 if (lane == 0) row_s[cnt] = x;
                 ++cnt;
@@ -500,6 +579,7 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
                 *consp = (uint8_t)cons;
             }
         }
+        if (lane == 0) g.rowcnt[rowg] = 0;  // the row's bucket count, for the next batch
         __syncwarp();
     }
     if (lane == 0 && (n_prune | n_app)) {

@@ -43,6 +43,13 @@ struct Graph {
     int gvis_log2, gvis_nslots;
     const float *vecs;     // n x dim vectors (exact kind: every distance; rerank)
     int dim;
+    // reverse-request bucketing of a build batch (reverse.cu): requests per
+    // row (n + nU, zero between batches), the rows touched by the batch and
+    // their count, and scratch for ordering long row segments
+    int32_t *rowcnt;
+    int32_t *touched;
+    int *ntouched;
+    unsigned long long *seg_scratch;
 };
 
 constexpr int kMaxExpand = 8;

@@ -167,3 +167,56 @@ def _round_bf16(x: np.ndarray) -> np.ndarray:
     u = x.view(np.uint32).astype(np.uint64)
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return u.astype(np.uint32).view(np.float32)
+
+
+def baseline_config_dev(cfg: int, n: int | None = None, seed: int = 0, chunk: int = 1 << 20):
+    """Base rows of BASELINE config `cfg` generated on the GPU (torch, seeded):
+    the same law as baseline_config (same mixture / spectrum / rank-64 model,
+    the builder's choices of DESIGN §9) from the device RNG, for the bench's
+    full-size workloads (10M x 96, 5M x 768) that a host generator would take
+    minutes to draw.  Config 5 comes back as bfloat16 (its stated dtype); the
+    others as float32.  Not row-identical to baseline_config (another RNG)."""
+    import torch
+
+    c = CONFIGS[cfg]
+    n = c["n"] if n is None else n
+    d = c["dim"]
+    g = torch.Generator(device="cuda").manual_seed(1_000_003 * seed + cfg)
+    dev = "cuda"
+    out = torch.empty((n, d), dtype=torch.bfloat16 if cfg == 5 else torch.float32, device=dev)
+    if cfg == 1:
+        centres = torch.randn((64, d), generator=g, device=dev)
+    elif cfg == 2:
+        centres = torch.rand((256, d), generator=g, device=dev) * 255.0
+    elif cfg == 3:
+        centres = torch.randn((1024, d), generator=g, device=dev)
+    elif cfg == 4:
+        rot, _ = torch.linalg.qr(torch.randn((d, d), generator=g, device=dev, dtype=torch.float64))
+        rot = rot.float()
+        scale = torch.arange(1, d + 1, device=dev, dtype=torch.float32) ** -0.6
+        centres = torch.randn((512, d), generator=g, device=dev)
+    elif cfg == 5:
+        basis = torch.randn((64, d), generator=g, device=dev) / (d ** 0.5)
+        noise_sd = float(((basis.double() ** 2).sum() / d / 3.0).sqrt())
+    else:
+        raise ConfigError(f"unknown config {cfg}")
+    for lo in range(0, n, chunk):
+        s = min(chunk, n - lo)
+        if cfg in (1, 2, 3, 4):
+            k = centres.shape[0]
+            a = torch.randint(0, k, (s,), generator=g, device=dev)
+            if cfg == 4:
+                x = centres[a] + (torch.randn((s, d), generator=g, device=dev) * scale) @ rot.T
+            else:
+                sd = {1: 0.3, 2: 20.0, 3: 0.3}[cfg]
+                x = centres[a] + torch.randn((s, d), generator=g, device=dev) * sd
+            if cfg == 2:
+                x = x.round_().clamp_(0, 255)
+            if cfg == 3:
+                x = x / x.norm(dim=1, keepdim=True)
+        else:
+            x = torch.randn((s, 64), generator=g, device=dev) @ basis
+            x += torch.randn((s, d), generator=g, device=dev) * noise_sd
+            x = x / x.norm(dim=1, keepdim=True)
+        out[lo: lo + s] = x.to(out.dtype)
+    return out

@@ -249,23 +249,26 @@ class FlashProvider:
         self.dev = {"vecs": x, "proj": proj, "codes": codes, **_model_dev(self.model)}
         self._prov = None
 
-    def reproject(self) -> None:
-        """Recompute projection + codes of the attached rows in place (the
-        device buffers keep their addresses, so a device index stays valid)."""
-        proj = pca_project_all_dev(self.model.pca, self.dev["vecs"])
-        self.dev["proj"].copy_(proj)
+    def reproject(self, lo: int = 0, hi: int | None = None) -> None:
+        """Recompute projection + codes of the attached rows [lo, hi) in place
+        (the device buffers keep their addresses, so a device index stays
+        valid)."""
+        hi = self.dev["codes"].shape[0] if hi is None else hi
+        if hi <= lo:
+            return
+        proj = pca_project_all_dev(self.model.pca, self.dev["vecs"][lo:hi])
+        self.dev["proj"][lo:hi].copy_(proj)
         del proj
         lib = _lib_()
         dm = _model_dev(self.model)
         codes = self.dev["codes"]
-        n = codes.shape[0]
-        if n:
-            check(lib.fa_encode_adt_dev(self.dev["proj"].data_ptr(), n, self.dev["proj"].shape[1],
-                                        dm["cent"].data_ptr(), dm["dims"].data_ptr(),
-                                        dm["offs"].data_ptr(), self.model.m,
-                                        self.model.cent.shape[2], self.model.dist_min,
-                                        self.model.delta, codes.data_ptr(), codes.shape[1],
-                                        None, 0, None))
+        pr = self.dev["proj"]
+        check(lib.fa_encode_adt_dev(pr[lo].data_ptr(), hi - lo, pr.shape[1],
+                                    dm["cent"].data_ptr(), dm["dims"].data_ptr(),
+                                    dm["offs"].data_ptr(), self.model.m,
+                                    self.model.cent.shape[2], self.model.dist_min,
+                                    self.model.delta, codes[lo].data_ptr(), codes.shape[1],
+                                    None, 0, None))
         self._prov = None
 
     def core_arrays(self) -> dict:

@@ -123,11 +123,12 @@ class GraphIndex:
             return
         model = provider.model
         d.n, d.m, d.R = self.n, model.m, self.params.R
-        d.dim = int(dev["vecs"].shape[1])
         d.dproj = int(dev["proj"].shape[1])
         d.dmax = int(model.cent.shape[2])
         d.dist_min, d.delta = float(model.dist_min), float(model.delta)
-        d.vecs, d.proj = dev["vecs"].data_ptr(), dev["proj"].data_ptr()
+        d.proj = dev["proj"].data_ptr()
+        if dev["vecs"].dtype == torch.float32:  # rerank reads fp32 vectors
+            d.vecs, d.dim = dev["vecs"].data_ptr(), int(dev["vecs"].shape[1])
         d.cent, d.dims = dev["cent"].data_ptr(), dev["dims"].data_ptr()
         d.offs, d.sdt = dev["offs"].data_ptr(), dev["sdt"].data_ptr()
         d.levels, d.uoff = lv.data_ptr(), uo.data_ptr()
