@@ -95,7 +95,10 @@ def build_device(g: graph.GraphIndex, provider: FlashProvider, params: graph.Bui
     """Batched insertion on the device index of `g`: every vertex, or the
     range [start, end) — start > 0 resumes the graph the earlier calls built
     (vertices [0, start)), the dynamic-rebuild workload of BASELINE config 5."""
+    from .sm100 import check_limits
+
     lib = _lib.load()
+    check_limits(g.n, params.C, params.R, provider.code_subspaces)
     if g.handle is None:
         g.create_device(provider)
     res = _lib.BuildResult()

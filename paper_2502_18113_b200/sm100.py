@@ -93,6 +93,29 @@ def _require_flash(kind: int) -> None:
                          f"got kind {kind}")
 
 
+# Capacities of the sm_100a build (checked up front with the limit named,
+# before any device work): layer-0 rows of 2R <= 127 slots (id rows of up to
+# four 32-slot chunks held in registers), candidate width C <= 2048, m <= 128
+# subspaces, and 24-bit vertex ids in the search keys.
+DEVICE_LIMITS = {"R_max": 63, "C_max": 2048, "m_max": 128, "n_max": (1 << 24) - 2}
+
+
+def check_limits(n: int, C_: int, R: int, m: int = 0) -> None:
+    from .errors import ConfigError
+
+    lim = DEVICE_LIMITS
+    if R > lim["R_max"]:
+        raise ConfigError(f"R={R}: the sm100 core supports R <= {lim['R_max']} "
+                          f"(layer-0 rows of 2R <= 127 slots)")
+    if C_ > lim["C_max"]:
+        raise ConfigError(f"C={C_}: the sm100 core supports C <= {lim['C_max']}")
+    if m > lim["m_max"]:
+        raise ConfigError(f"m={m}: the sm100 core supports m <= {lim['m_max']} subspaces")
+    if n > lim["n_max"]:
+        raise ConfigError(f"n={n}: the sm100 core addresses n <= {lim['n_max']} vertices "
+                          "(24-bit ids in the search keys)")
+
+
 def build_options(C_: int) -> _lib.BuildOpts:
     o = BUILD_OPTIONS
     return _lib.BuildOpts(C=C_, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
@@ -133,6 +156,7 @@ def build_graph(kind, prov, levels, base_blocks, upper_offsets, upper_blocks, C,
     if n == 0:
         return {"entry_point": -1, "max_layer": -1,
                 "counters": {"dist_comps": 0, "sym_comps": 0, "kernel_calls": 0, "visited": 0}}
+    check_limits(n, int(C), int(R), 0 if kind == KIND_EXACT else int(np.shape(prov["cent"])[0]))
     res = _lib.BuildResult()
     opts = build_options(int(C))
     if kind == KIND_EXACT:

@@ -86,3 +86,15 @@ def test_product_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f
+
+
+def test_device_limits_named_up_front():
+    """Capacities of the sm_100a build raise ConfigError naming the limit
+    before any device work (R <= 63, C <= 2048)."""
+    from paper_2502_18113_b200 import errors, sm100
+
+    sm100.check_limits(1000, 2048, 63, 128)
+    for args in ((1000, 200, 64, 16), (1000, 4096, 32, 16), (1000, 200, 32, 129),
+                 (1 << 24, 200, 32, 16)):
+        with pytest.raises(errors.ConfigError):
+            sm100.check_limits(*args)
