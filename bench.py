@@ -333,16 +333,19 @@ def scan_cpu_baseline(torch, blocks, stride, codes_off, cap, m, adt, nb, target_
                                sel.ctypes.data, ns, out.ctypes.data, threads, kern)
         return lanes, time.perf_counter() - t0
 
-    nq = 64
-    lanes, dt = run(nq)
-    while dt < target_s / 4 and nq < ha.shape[0]:
-        nq = min(ha.shape[0], nq * 4)
-        lanes, dt = run(nq)
+    nq = ha.shape[0]
+    lanes, dt = run(nq)  # warm-up and calibration
+    reps = max(1, int(target_s / max(dt, 1e-6)))
+    lanes, dt = 0, 0.0
+    for _ in range(reps):
+        lr, tr = run(nq)
+        lanes += lr
+        dt += tr
     evals = lanes / dt
-    bytes_s = nq * ns * (4 + nb * 16 * (m + 4)) / dt
+    bytes_s = reps * nq * ns * (4 + nb * 16 * (m + 4)) / dt
     return {"evals_per_s": evals, "gbs": bytes_s / 1e9, "cores": threads, "kind": "reference",
             "kernel": ["scalar", "vector128", "vector256", "vector512"][kern],
-            "sample": f"{nq} queries x {ns} random blocks of {nblk} (host copy, "
+            "sample": f"{reps} x {nq} queries x {ns} random blocks of {nblk} (host copy, "
                       f"{nblk * stride / 1e9:.2f} GB), {dt:.1f} s"}
 
 
