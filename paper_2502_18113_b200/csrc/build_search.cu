@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     const int wid = threadIdx.x >> 5;
     WarpWS ws(smem, wid, blockDim.x >> 5, L);  // fewer warps per CTA for wide searches
     CounterTotals total;
+    GSlot gs = gslot_claim(g, lane);  // this warp's global visited table, for the launch
     // persistent warps pull vertices from the batch; a slow search never holds
     // its CTA siblings' slots idle
     for (;;) {
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         for (int layer = top; layer >= 0; --layer) {
             int ts = 0;
             bool ok = layer_search<P, J, EM, RC, 9>(g, layer, cur, curd, C, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
-                                   ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
+                                   ws.fdist, ws.H, L.hash_log2, cnt, to, gs, lane);
             if (!ok) {
                 if (lane == 0) atomicExch(err, 1);
                 for (int l = layer; l >= 0; --l)
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         }
         total.add(cnt);
     }
+    gslot_release(gs, lane);
     flush_counters(total, ctr, lane);
 }
 

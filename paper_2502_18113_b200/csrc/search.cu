@@ -52,8 +52,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     for (int layer = ml; layer > 0; --layer)
         hill_climb<P>(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
     int ts = 0;
+    GSlot gs = gslot_claim(g, lane);
     bool ok = layer_search<P, J, 1>(g, 0, cur, curd, ef, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh, ws.fdist,
-                           ws.H, L.hash_log2, cnt, to, lane);
+                           ws.H, L.hash_log2, cnt, to, gs, lane);
+    gslot_release(gs, lane);
     int64_t *oid = out_ids + (size_t)q * k;
     double *od = out_d + (size_t)q * k;
     if (!ok) {
@@ -128,8 +130,10 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     uint32_t d0 = P::one(g, ws.adt, entry, lane);
     cnt.dist += 1;
     int ts = 0;
+    GSlot gs = gslot_claim(g, lane);
     bool ok = layer_search<P, J, 1>(g, layer, entry, d0, width, ws.adt, ws.T, ts, ws.S, ws.TQ, ws.fresh,
-                           ws.fdist, ws.H, L.hash_log2, cnt, to, lane);
+                           ws.fdist, ws.H, L.hash_log2, cnt, to, gs, lane);
+    gslot_release(gs, lane);
     if (!ok) {
         if (lane == 0) atomicExch(err, 1);
         ts = 0;

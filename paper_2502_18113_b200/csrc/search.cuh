@@ -270,6 +270,51 @@ static __device__ __noinline__ int global_visit(uint32_t *G, int glog2, uint32_t
     }
 }
 
+// A warp's claimed global-tier table: claimed once per warp per launch (the
+// build kernel's persistent warps keep it across their insertions), its epoch
+// counted in a register and written back at release.
+struct GSlot {
+    uint32_t *G = nullptr;     // the table (null: no global tier)
+    uint32_t *own = nullptr;   // its owner word
+    uint32_t *ep = nullptr;    // its epoch word
+    uint32_t epoch = 0;
+};
+
+__device__ __forceinline__ uint32_t gslot_hint() {
+    uint32_t sm, w;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(w));
+    return sm * kMaxWarpsPerSM + w;
+}
+
+// Claim a free slot (the probe starts at %smid / %warpid, free in the common
+// case; the pool holds one slot per resident warp, so one is always free).
+__device__ inline GSlot gslot_claim(const Graph &g, int lane) {
+    GSlot gs;
+    if (!g.gvis) return gs;
+    uint32_t slot = 0, e = 0;
+    if (lane == 0) {
+        const uint32_t ns = (uint32_t)g.gvis_nslots;
+        slot = gslot_hint() % ns;
+        while (atomicCAS(g.gvis_owner + slot, 0u, 1u) != 0u) slot = (slot + 1u) % ns;
+        e = atomicAdd(g.gvis_epoch + slot, 0u);  // the last owner's epoch (L2, coherent)
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    gs.epoch = __shfl_sync(0xffffffffu, e, 0);
+    gs.G = g.gvis + ((size_t)slot << g.gvis_log2);
+    gs.own = g.gvis_owner + slot;
+    gs.ep = g.gvis_epoch + slot;
+    return gs;
+}
+__device__ inline void gslot_release(const GSlot &gs, int lane) {
+    __syncwarp();
+    if (gs.G && lane == 0) {
+        atomicExch(gs.ep, gs.epoch);
+        __threadfence();
+        atomicExch(gs.own, 0u);
+    }
+}
+
 // KB: log2 of the shared tier's bucket count compiled in (0 = from hlog2 at
 // run time); the build kernels fix it at 9 (the 8 KB table).
 template <int KB = 0>
@@ -277,20 +322,15 @@ struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
     int nslots;        // usable slots per bucket
-    uint32_t *G;       // global tier of the claimed slot
-    uint32_t *gown;    // its owner word
+    uint32_t *G;       // global tier (the warp's claimed table)
     int glog2;
     uint32_t epoch;
     int gcount, glimit;
 
-    __device__ static uint32_t slot_hint() {
-        uint32_t sm, w;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-        asm volatile("mov.u32 %0, %%warpid;" : "=r"(w));
-        return sm * kMaxWarpsPerSM + w;
-    }
-
-    __device__ void begin(void *H, int hlog2, const Graph &g, int lane) {
+    // a new search: clear the shared tier, advance the global tier's epoch
+    // (entries of older epochs count as empty; the table is wiped once every
+    // 255 searches)
+    __device__ void begin(void *H, int hlog2, const Graph &g, GSlot &gs, int lane) {
         B = reinterpret_cast<uint4 *>(H);
         kb = KB ? KB : vis_buckets_log2(hlog2);
         nslots = vis_bucket_slots(hlog2);
@@ -298,42 +338,19 @@ struct VisitedSet {
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
         gcount = 0;
         glog2 = g.gvis_log2;
-        glimit = g.gvis ? (1 << glog2) * 3 / 4 : (1 << 30);  // no tier: visit() reports 3
-        G = nullptr;
-        gown = nullptr;
-        if (g.gvis) {
-            uint32_t slot = 0, e = 0;
-            if (lane == 0) {
-                const uint32_t ns = (uint32_t)g.gvis_nslots;
-                slot = slot_hint() % ns;
-                while (atomicCAS(g.gvis_owner + slot, 0u, 1u) != 0u) slot = (slot + 1u) % ns;
-                e = atomicAdd(g.gvis_epoch + slot, 1u) + 1u;
-            }
-            slot = __shfl_sync(0xffffffffu, slot, 0);
-            e = __shfl_sync(0xffffffffu, e, 0);
-            G = g.gvis + ((size_t)slot << glog2);
-            gown = g.gvis_owner + slot;
+        G = gs.G;
+        glimit = G ? (1 << glog2) * 3 / 4 : (1 << 30);  // no tier: visit() reports 3
+        if (G) {
+            uint32_t e = gs.epoch + 1u;
             if (e > 255u) {  // wrap: clear this slot's table once
                 for (int i = lane; i < (1 << glog2) / 4; i += 32)
                     __stcg(reinterpret_cast<uint4 *>(G) + i, z);
                 e = 1u;
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence();
-                    atomicExch(g.gvis_epoch + slot, 1u);
-                }
             }
+            gs.epoch = e;
             epoch = e;
         }
         __syncwarp();
-    }
-    // release the global-tier slot (every exit of a search)
-    __device__ void end(int lane) {
-        __syncwarp();
-        if (gown && lane == 0) {
-            __threadfence();
-            atomicExch(gown, 0u);
-        }
     }
 
     // bucket of id and its remainder r (1 .. 2^(24 - kb))
@@ -831,7 +848,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                                                  unsigned long long *S, int32_t *TQ,
                                                  int32_t *fresh, uint32_t *fdist, uint32_t *H,
                                                  int hlog2, SearchCounters &cnt,
-                                                 const TieOrder &to, int lane) {
+                                                 const TieOrder &to, GSlot &gs, int lane) {
     constexpr unsigned FULL = 0xffffffffu;
     const int cap = layer_cap(g, layer);
     using K = typename P::Key;
@@ -839,7 +856,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     K *Sb = Sa + cand_capacity(g);
     const unsigned lt = (1u << lane) - 1u;
     VisitedSet<KB> vs;
-    vs.begin(H, hlog2, g, lane);
+    vs.begin(H, hlog2, g, gs, lane);
     if (lane == 0) vs.visit(entry);
     RegSet<J, K> rs;
 #pragma unroll
@@ -932,7 +949,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) { vs.end(lane); return false; }
+        if (vs.gcount + npop * cap > vs.glimit) return false;
         // visited filter over the rows (pop order, slot order), compacted
         bool over = false;
         int nf = 0;
@@ -957,7 +974,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
-        if (__any_sync(FULL, over)) { vs.end(lane); return false; }
+        if (__any_sync(FULL, over)) return false;
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
@@ -968,7 +985,6 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     }
     sort_out<J>(rs, ts, T, lane);
     ts_out = ts;
-    vs.end(lane);
     return true;
 }
 
@@ -1020,7 +1036,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
                                     const uint8_t *qc, unsigned long long *T, int &ts,
                                     unsigned long long *S, int32_t *TQ, int32_t *fresh,
                                     uint32_t *fdist, uint32_t *H, int hlog2, SearchCounters &cnt,
-                                    const TieOrder &to, int lane) {
+                                    const TieOrder &to, GSlot &gs, int lane) {
     using Kt = typename P::Key;
     constexpr Kt NONE = ~Kt(0);
     const int cap = layer_cap(g, layer);
@@ -1032,7 +1048,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
     Kt *Sa = reinterpret_cast<Kt *>(S);
     Kt *Sb = Sa + cand_capacity(g);
     VisitedSet<> vs;
-    vs.begin(H, hlog2, g, lane);
+    vs.begin(H, hlog2, g, gs, lane);
     if (lane == 0) {
         vs.visit(entry);
         K[0] = P::key(entry_d, to.fwd((uint32_t)entry));
@@ -1095,7 +1111,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) { vs.end(lane); return false; }
+        if (vs.gcount + npop * cap > vs.glimit) return false;
         bool over = false;
         // visited filter over the rows (pop order, slot order), compacted
         int nf = 0;
@@ -1120,7 +1136,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
-        if (__any_sync(0xffffffffu, over)) { vs.end(lane); return false; }
+        if (__any_sync(0xffffffffu, over)) return false;
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
@@ -1198,7 +1214,6 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         T[r] = make_key((uint32_t)(k >> 24), (int)(k & 0xffffffu));
     }
     __syncwarp();
-    vs.end(lane);
     return true;
 }
 
@@ -1212,13 +1227,13 @@ __device__ __forceinline__ bool layer_search(const Graph &g, int layer, int entr
                                              int &ts, unsigned long long *S, int32_t *TQ,
                                              int32_t *fresh, uint32_t *fdist, uint32_t *H,
                                              int hlog2, SearchCounters &cnt, const TieOrder &to,
-                                             int lane) {
+                                             GSlot &gs, int lane) {
     if constexpr (J == 0) {
         return layer_search_smem<P>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ, fresh, fdist, H,
-                                 hlog2, cnt, to, lane);
+                                 hlog2, cnt, to, gs, lane);
     } else {
         return layer_search_reg<P, J, EM, RC, KB>(g, layer, entry, entry_d, W, qc, T, ts, S, TQ,
-                                                  fresh, fdist, H, hlog2, cnt, to, lane);
+                                                  fresh, fdist, H, hlog2, cnt, to, gs, lane);
     }
 }
 
