@@ -295,16 +295,18 @@ static uint32_t tie_inv(void) {
 }
 /* tie = 2 salts the scramble per search (salt = hash of the inserted vertex
  * or query), so different insertions break ties differently, as the compiled
- * core's history-dependent heap order does. */
+ * core's history-dependent heap order does.  tie = 3 / 4: modes 1 / 2 over
+ * 32-bit tie ids (the GPU's wide-id kernels, n >= 2^24). */
+static uint32_t tie_mask(int tie) { return tie >= 3 ? 0xffffffffu : 0xffffffu; }
 static uint32_t tie_salt(int tie, uint32_t who) {
-    return tie == 2 ? ((who + 1u) * 0x9E3779B1u) & 0xffffffu : 0u;
+    return (tie == 2 || tie == 4) ? ((who + 1u) * 0x9E3779B1u) & tie_mask(tie) : 0u;
 }
-/* tie ids are 24-bit bijections of the vertex id (ids < 2^24) */
+/* tie ids are 24-bit (32-bit) bijections of the vertex id */
 static uint32_t tie_fwd(int tie, uint32_t salt, uint32_t u) {
-    return tie ? ((u ^ salt) * TIE_MUL) & 0xffffffu : u;
+    return tie ? ((u ^ salt) * TIE_MUL) & tie_mask(tie) : u;
 }
 static uint32_t tie_back(int tie, uint32_t salt, uint32_t t) {
-    return tie ? ((t * tie_inv()) & 0xffffffu) ^ salt : t;
+    return tie ? ((t * tie_inv()) & tie_mask(tie)) ^ salt : t;
 }
 
 /* Best-first layer search with the semantics of the reference's semantic

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         const int q = __ldg(order + p);
         const int x = start + q;
         const long long t_begin = clock64();
-        const TieOrder to = TieOrder::make(g.tie, (uint32_t)x);
+        const TieOrder to = TieOrder::make(g.tie, (uint32_t)x, P::kWide);
         __syncwarp();
         if constexpr (P::kExact) {
             float *qv = reinterpret_cast<float *>(ws.adt);
@@ -166,8 +166,12 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         default: break;                                       \
     }
 
-BuildSearchFn build_search_variant(int W, int expand, int cap0) {
+BuildSearchFn build_search_variant(int W, int expand, int cap0, bool wide) {
     const int v = set_variant(W);
+    if (wide) {  // 32-bit ids (n >= 2^24): one expansion per step, any row size
+        FA_BUILD_J(FlashDistW, 1, kRowChunks)
+        return build_search_kernel<FlashDistW, 0, 1, kRowChunks>;
+    }
     if (expand > 1) {
         if (v == 0) return build_search_kernel<FlashDist, 0, 1, kRowChunks>;
         return v <= 8 ? build_search_kernel<FlashDist, 8, kMaxExpand, kRowChunks>
@@ -181,8 +185,12 @@ BuildSearchFn build_search_variant(int W, int expand, int cap0) {
     return build_search_kernel<FlashDist, 0, 1, kRowChunks>;
 }
 
-BuildSearchFn build_search_exact_variant(int W, int cap0) {
+BuildSearchFn build_search_exact_variant(int W, int cap0, bool wide) {
     const int v = set_variant(W);
+    if (wide) {
+        FA_BUILD_J(ExactDistW, 1, kRowChunks)
+        return build_search_kernel<ExactDistW, 0, 1, kRowChunks>;
+    }
     if (cap0 <= 64) {
         FA_BUILD_J(ExactDist, 1, 2)
     } else {

@@ -40,6 +40,7 @@ struct fa_index {
     int32_t *upper_owner = nullptr;
     uint32_t *gvis = nullptr, *gvis_epoch = nullptr, *gvis_owner = nullptr;  // global visited tier
     int search_tie = 0;
+    bool wide = false;       // 32-bit-id kernels (n >= 2^24 - 1, or forced)
     int64_t n_inserted = 0;  // vertices [0, n_inserted) are in the graph
     int64_t entry = -1;
     int max_layer = -1;
@@ -102,8 +103,8 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
 // Global visited tier (VisitedSet): a pool of tables claimed per search.  The
 // pool holds one slot per warp the launch can keep resident (occupancy x SMs)
 // and each table 2^gvis_log2_for(W) entries; it grows on demand (reallocated
-// only when a launch needs more slots or a wider table).  Absent for n >= 2^24
-// (the tier packs ids into 24 bits), where the shared tier alone must suffice.
+// only when a launch needs more slots or a wider table).  Wide indexes (32-bit
+// ids) use 64-bit entries.
 // Warps per CTA of a search launch: kSearchWarps, fewer when the per-warp
 // workspace (wide searches) does not fit; 0 if one warp does not fit.
 static int search_warps_for(int per_warp_bytes) {
@@ -113,7 +114,6 @@ static int search_warps_for(int per_warp_bytes) {
 }
 
 static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t smem, int W) {
-    if (ix->g.n >= (1ll << 24) - 1) return FA_OK;
     int dev = 0, nsm = 0, per_sm = 0;
     FA_CUDA(cudaGetDevice(&dev));
     FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -131,7 +131,8 @@ static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t sme
     pool_free(ix->gvis_owner);
     ix->gvis = ix->gvis_epoch = ix->gvis_owner = nullptr;
     ix->g.gvis = ix->g.gvis_epoch = ix->g.gvis_owner = nullptr;
-    const size_t tab = ((size_t)ns << lg) * sizeof(uint32_t);
+    // entries: 32-bit (epoch << 24 | id) or, wide, 64-bit (epoch << 32 | id)
+    const size_t tab = ((size_t)ns << lg) * (ix->wide ? 8 : 4);
     FA_TRY(dev_alloc((void **)&ix->gvis, tab));
     FA_TRY(dev_alloc((void **)&ix->gvis_epoch, (size_t)ns * sizeof(uint32_t)));
     FA_TRY(dev_alloc((void **)&ix->gvis_owner, (size_t)ns * sizeof(uint32_t)));
@@ -276,8 +277,9 @@ using namespace fa;
 
 extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     FA_CHECK_ARG(desc && out, "null argument");
-    // search keys carry 24-bit vertex ids (d << 24 | tie id)
-    FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 24), "n=%lld out of range [0, 2^24)",
+    // n < 2^24 - 1: 24-bit tie ids in 32-bit search keys; above, the wide
+    // kernels (32-bit ids, 64-bit keys).  Ids are int32.
+    FA_CHECK_ARG(desc->n >= 0 && desc->n < (1ll << 31) - 1, "n=%lld out of range [0, 2^31 - 1)",
                  (long long)desc->n);
     // m = 0: the exact strategy (kind 0, code_subspaces = 0): fp32 L2 over vecs
     FA_CHECK_ARG(desc->m >= 0 && desc->m <= 128, "m=%d outside [0,128]", desc->m);
@@ -287,6 +289,8 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     FA_CHECK_ARG(2 * desc->R <= 127, "base capacity 2R=%d exceeds 127", 2 * desc->R);
     fa_index *ix = new fa_index();
     ix->d = *desc;
+    ix->wide = desc->n >= (1ll << 24) - 1;
+    if (const char *e = getenv("FLASHANN_B200_WIDE")) ix->wide = ix->wide || atoi(e) > 0;
     Graph &g = ix->g;
     g.n = desc->n;
     g.m = desc->m;
@@ -543,7 +547,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
 
     // ---- scratch ----
     const int capmax = std::max(g.cap0, g.capU);
-    if (exact) gb.expand = 1;
+    if (exact || ix->wide) gb.expand = 1;
     // Visited table: 2^12 16-bit slots (8 KB) unless requested — a larger one
     // costs occupancy (the ids it cannot hold go to the global tier).  The
     // forward selection's workspace always lives in the dead table; the
@@ -558,13 +562,14 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const bool t_alias =
         sel_bytes + (size_t)round_up(C, 32) * 8 <= ((size_t)16 << vis_buckets_log2(hl));
     WarpLayout L;
-    L.init(g.mpad, C, capmax, hl, gb.expand, t_alias, exact ? g.dim * 4 : -1, exact ? 8 : 4);
+    L.init(g.mpad, C, capmax, hl, gb.expand, t_alias, exact ? g.dim * 4 : -1, (exact || ix->wide) ? 8 : 4);
     const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
     const int bw = search_warps_for(L.total);  // warps per CTA
     const size_t smem_search = (size_t)bw * L.total;
     FA_CHECK_ARG(bw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
     const BuildSearchFn search_fn =
-        exact ? build_search_exact_variant(C, g.cap0) : build_search_variant(C, gb.expand, g.cap0);
+        exact ? build_search_exact_variant(C, g.cap0, ix->wide)
+              : build_search_variant(C, ix->wide ? 1 : gb.expand, g.cap0, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
     ReverseLayout RL;
@@ -696,6 +701,20 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         fprintf(stderr, "[fa timing] build host setup (schedule, scratch) %8.2f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                           t_host0).count());
+    size_t l2pin_bytes = 0;
+    if (const char *e = getenv("FLASHANN_B200_L2PIN")) {
+        if (atoi(e) > 0) {
+            int dev = 0, maxwin = 0, maxpers = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            l2pin_bytes = std::min<size_t>((size_t)g.n * g.mpad, (size_t)maxwin);
+            FA_BUILD_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                             std::min<size_t>(l2pin_bytes, (size_t)maxpers)));
+            fprintf(stderr, "[fa] L2 pin %zu B (window max %d, persisting max %d)\n", l2pin_bytes,
+                    maxwin, maxpers);
+        }
+    }
     int64_t launches = r0 == 0 ? 3 : 1;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
@@ -743,10 +762,35 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         // work counter, nheads[2]: the bucketing cursor
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 3 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
-        search_fn<<<grid, bw * 32, smem_search, st>>>(
-            gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
-            order_d + b.start,
-            req, ctr, err, opts->point_stats, nheads + 1);
+        if (l2pin_bytes) {
+            // experiment (FLASHANN_B200_L2PIN=1): the code table as a persisting
+            // L2 window of the search launches
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(bw * 32);
+            cfg.dynamicSmemBytes = smem_search;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+            at[0].val.accessPolicyWindow.base_ptr = (void *)g.codes;
+            at[0].val.accessPolicyWindow.num_bytes = l2pin_bytes;
+            at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+            at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            FA_BUILD_CUDA(cudaLaunchKernelEx(&cfg, search_fn, gb, (const uint8_t *)sdtT,
+                                             (const uint8_t *)adt_batch, (int)b.start, b.size,
+                                             b.ep, b.ml, C, R, L,
+                                             (const int64_t *)(req_off_d + b.start),
+                                             (const int32_t *)(order_d + b.start), req, ctr, err,
+                                             opts->point_stats, nheads + 1));
+        } else {
+            search_fn<<<grid, bw * 32, smem_search, st>>>(
+                gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+                order_d + b.start,
+                req, ctr, err, opts->point_stats, nheads + 1);
+        }
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         // bucket the requests by row: segments for the touched rows, then
@@ -863,11 +907,11 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     L.init(ix->g.mpad, ef, capmax,
            pick_hash_log2(ef, capmax, 1, ix->g.mpad, 0,
                           (size_t)8 * std::min(std::max(rerank_depth, 0), ef)),
-           1, false, exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
+           1, false, exact ? ix->d.dim * 4 : -1, (exact || ix->wide) ? 8 : 4);
     const int qw = search_warps_for(L.total);  // warps per CTA
     FA_CHECK_ARG(qw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
     size_t smem = (size_t)qw * L.total;
-    const QuerySearchFn qfn = query_search_variant(ef, exact);
+    const QuerySearchFn qfn = query_search_variant(ef, exact, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     FA_TRY(ensure_gvis(ix, (const void *)qfn, qw * 32, smem, ef));
@@ -927,11 +971,11 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     const int capmax = std::max(ix->g.cap0, ix->g.capU);
     WarpLayout L;
     L.init(ix->g.mpad, width, capmax, pick_hash_log2(width, capmax, 1, ix->g.mpad, 0), 1, false,
-           exact ? ix->d.dim * 4 : -1, exact ? 8 : 4);
+           exact ? ix->d.dim * 4 : -1, (exact || ix->wide) ? 8 : 4);
     const int qw = search_warps_for(L.total);  // warps per CTA
     FA_CHECK_ARG(qw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
     size_t smem = (size_t)qw * L.total;
-    const LayerSearchFn lfn = layer_search_variant(width, exact);
+    const LayerSearchFn lfn = layer_search_variant(width, exact, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     FA_TRY(ensure_gvis(ix, (const void *)lfn, qw * 32, smem, width));

@@ -71,11 +71,12 @@ using LayerSearchFn = void (*)(Graph, const uint8_t *, int, const int64_t *, int
 
 // Kernel instantiations per result-set variant (set_variant(W)) and, for the
 // build, per expansion width (1 or kMaxExpand).
-BuildSearchFn build_search_variant(int W, int expand, int cap0);
-BuildSearchFn build_search_exact_variant(int W, int cap0);
+// wide: 32-bit vertex ids (n >= 2^24; 64-bit keys, FlashDistW / ExactDistW)
+BuildSearchFn build_search_variant(int W, int expand, int cap0, bool wide);
+BuildSearchFn build_search_exact_variant(int W, int cap0, bool wide);
 // exact = true: the exact-kind instantiations
-QuerySearchFn query_search_variant(int W, bool exact);
-LayerSearchFn layer_search_variant(int W, bool exact);
+QuerySearchFn query_search_variant(int W, bool exact, bool wide);
+LayerSearchFn layer_search_variant(int W, bool exact, bool wide);
 
 struct ReverseLayout {
     int tdom, tkeep, row, rowd, keptd, cand, sel, total;

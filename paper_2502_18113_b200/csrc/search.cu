@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) query_search_kernel(
     const int q = blockIdx.x * nw + wid;
     if (q >= nq) return;
     WarpWS ws(smem, wid, nw, L);
-    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
+    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q, P::kWide);
     load_query_ctx<P>(g, ws.adt, P::kExact ? reinterpret_cast<const uint8_t *>(queries) : adt_q,
                       q, lane);
     __syncwarp();
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
     const int q = blockIdx.x * nw + wid;
     if (q >= nq) return;
     WarpWS ws(smem, wid, nw, L);
-    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q);
+    const TieOrder to = TieOrder::make(g.tie, (uint32_t)q, P::kWide);
     load_query_ctx<P>(g, ws.adt, adt_q, q, lane);
     __syncwarp();
     SearchCounters cnt = {};
@@ -157,19 +157,35 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 4) layer_search_kernel(
         default: break;                   \
     }
 
-QuerySearchFn query_search_variant(int W, bool exact) {
+QuerySearchFn query_search_variant(int W, bool exact, bool wide) {
     if (exact) {
+        if (wide) {
+            FA_VARIANTS(query_search_kernel, ExactDistW)
+            return query_search_kernel<ExactDistW, 0>;
+        }
         FA_VARIANTS(query_search_kernel, ExactDist)
         return query_search_kernel<ExactDist, 0>;
+    }
+    if (wide) {
+        FA_VARIANTS(query_search_kernel, FlashDistW)
+        return query_search_kernel<FlashDistW, 0>;
     }
     FA_VARIANTS(query_search_kernel, FlashDist)
     return query_search_kernel<FlashDist, 0>;
 }
 
-LayerSearchFn layer_search_variant(int W, bool exact) {
+LayerSearchFn layer_search_variant(int W, bool exact, bool wide) {
     if (exact) {
+        if (wide) {
+            FA_VARIANTS(layer_search_kernel, ExactDistW)
+            return layer_search_kernel<ExactDistW, 0>;
+        }
         FA_VARIANTS(layer_search_kernel, ExactDist)
         return layer_search_kernel<ExactDist, 0>;
+    }
+    if (wide) {
+        FA_VARIANTS(layer_search_kernel, FlashDistW)
+        return layer_search_kernel<FlashDistW, 0>;
     }
     FA_VARIANTS(layer_search_kernel, FlashDist)
     return layer_search_kernel<FlashDist, 0>;

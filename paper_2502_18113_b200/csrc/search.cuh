@@ -14,6 +14,8 @@
 // m code bytes from the L2-resident code table.
 #pragma once
 
+#include <type_traits>
+
 #include "select.cuh"
 
 #ifndef FA_PHASE_PROFILE
@@ -252,16 +254,22 @@ __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
 // kept out of line so the hot loop stays compact).  0 = already visited,
 // 2 = inserted.  Reads bypass L1 (the table may have been written on another SM
 // by the slot's previous owner).
-static __device__ __noinline__ int global_visit(uint32_t *G, int glog2, uint32_t epoch, int id) {
+// Narrow entries are 32-bit (epoch << 24 | id), wide ones 64-bit
+// (epoch << 32 | id).
+template <bool W>
+static __device__ __noinline__ int global_visit(uint32_t *G32, int glog2, uint32_t epoch, int id) {
+    using E = typename std::conditional<W, unsigned long long, uint32_t>::type;
+    constexpr int kEpochShift = W ? 32 : 24;
+    E *G = reinterpret_cast<E *>(G32);
     const uint32_t key = (uint32_t)id + 1u;
-    const uint32_t gk = (epoch << 24) | ((uint32_t)id & 0xFFFFFFu);
+    const E gk = ((E)epoch << kEpochShift) | (E)((uint32_t)id & (W ? 0xffffffffu : 0xFFFFFFu));
     const uint32_t gmask = (1u << glog2) - 1u;
     uint32_t p = (key * 2654435761u) >> (32 - glog2);
     while (true) {
-        const uint32_t v = __ldcg(G + p);
+        const E v = __ldcg(G + p);
         if (v == gk) return 0;
-        if ((v >> 24) != epoch) {
-            const uint32_t old = atomicCAS(G + p, v, gk);
+        if ((uint32_t)(v >> kEpochShift) != epoch) {
+            const E old = atomicCAS(G + p, v, gk);
             if (old == v) return 2;
             if (old == gk) return 0;
             continue;
@@ -317,7 +325,9 @@ __device__ inline void gslot_release(const GSlot &gs, int lane) {
 
 // KB: log2 of the shared tier's bucket count compiled in (0 = from hlog2 at
 // run time); the build kernels fix it at 9 (the 8 KB table).
-template <int KB = 0>
+// W: wide ids (n >= 2^24): 32-bit shared slots (4 per bucket) holding a
+// 32 - kb bit remainder + 1, 64-bit global entries.
+template <int KB = 0, bool W = false>
 struct VisitedSet {
     uint4 *B;          // shared tier buckets
     int kb;            // log2 buckets
@@ -333,7 +343,7 @@ struct VisitedSet {
     __device__ void begin(void *H, int hlog2, const Graph &g, GSlot &gs, int lane) {
         B = reinterpret_cast<uint4 *>(H);
         kb = KB ? KB : vis_buckets_log2(hlog2);
-        nslots = vis_bucket_slots(hlog2);
+        nslots = W ? min(4, vis_bucket_slots(hlog2)) : vis_bucket_slots(hlog2);
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
         gcount = 0;
@@ -343,7 +353,7 @@ struct VisitedSet {
         if (G) {
             uint32_t e = gs.epoch + 1u;
             if (e > 255u) {  // wrap: clear this slot's table once
-                for (int i = lane; i < (1 << glog2) / 4; i += 32)
+                for (int i = lane; i < (1 << glog2) / (W ? 2 : 4); i += 32)
                     __stcg(reinterpret_cast<uint4 *>(G) + i, z);
                 e = 1u;
             }
@@ -353,12 +363,13 @@ struct VisitedSet {
         __syncwarp();
     }
 
-    // bucket of id and its remainder r (1 .. 2^(24 - kb))
+    // bucket of id and its remainder r (1 .. 2^(bits - kb)), bits = 24 or 32
     __device__ __forceinline__ uint4 *bucket(int id, uint32_t &r) const {
+        constexpr int bits = W ? 32 : 24;
         const int k = KB ? KB : kb;
-        const uint32_t h = ((uint32_t)id * kVisMul) & 0xffffffu;
-        r = (h & ((1u << (24 - k)) - 1u)) + 1u;
-        return B + (h >> (24 - k));
+        const uint32_t h = ((uint32_t)id * kVisMul) & (W ? 0xffffffffu : 0xffffffu);
+        r = (h & ((1u << (bits - k)) - 1u)) + 1u;
+        return B + (h >> (bits - k));
     }
     // some 16-bit slot of v equals the remainder (rr = r in both halves):
     // unsigned 16x2 minimum of v ^ rr (VIMNMX) has a zero half
@@ -378,6 +389,18 @@ struct VisitedSet {
     __device__ int visit(int id) {
         uint32_t r;
         uint4 *bk = bucket(id, r);
+        if constexpr (W) {
+            uint4 v = *bk;
+            while (true) {
+                if ((v.x == r) | (v.y == r) | (v.z == r) | (v.w == r)) return 0;
+                const int e = (v.x != 0u) + (v.y != 0u) + (v.z != 0u) + (v.w != 0u);
+                if (e >= nslots) break;
+                const uint32_t ow = (e & 2) ? ((e & 1) ? v.w : v.z) : ((e & 1) ? v.y : v.x);
+                if (atomicCAS(reinterpret_cast<uint32_t *>(bk) + e, ow, r) == ow) return 1;
+                v = lds128_volatile(bk);
+            }
+            return G == nullptr ? 3 : global_visit<true>(G, glog2, epoch, id);
+        }
         const uint32_t rr = r * 0x10001u;
         uint4 v = *bk;  // the common case (a visited id) needs this one read
         while (true) {
@@ -391,17 +414,18 @@ struct VisitedSet {
             // another lane took the slot: re-read the bucket
             v = lds128_volatile(bk);
         }
-        return G == nullptr ? 3 : global_visit(G, glog2, epoch, id);
+        return G == nullptr ? 3 : global_visit<false>(G, glog2, epoch, id);
     }
 };
 
 // ---- sorted top-W buffer ---------------------------------------------------
 constexpr unsigned long long KEY_MAX = ~0ull;
 
-__device__ __forceinline__ unsigned long long make_key(uint32_t d, int id) {
-    return ((unsigned long long)d << 32) | ((unsigned long long)(uint32_t)id << 1);
+// sorted results: (d << 32 | tie id), the tie id a full 32 bits (wide keys)
+__device__ __forceinline__ unsigned long long make_key(uint32_t d, uint32_t tie) {
+    return ((unsigned long long)d << 32) | (unsigned long long)tie;
 }
-__device__ __forceinline__ int key_id(unsigned long long k) { return (int)((k >> 1) & 0x7fffffffu); }
+__device__ __forceinline__ uint32_t key_id(unsigned long long k) { return (uint32_t)k; }
 __device__ __forceinline__ uint32_t key_d(unsigned long long k) { return (uint32_t)(k >> 32); }
 
 // Order among equal distances inside one search.  mode 0: vertex id (the
@@ -420,18 +444,20 @@ __host__ __device__ constexpr uint32_t tie_inverse(uint32_t a) {
 struct TieOrder {
     int mode;
     uint32_t salt;
-    // tie ids are 24 bits (vertex ids < 2^24): keys are (d << 24 | tie id)
-    __device__ static TieOrder make(int mode, uint32_t who) {
+    uint32_t mask;  // tie-id bits: 24 (narrow keys, n < 2^24) or 32 (wide)
+    __device__ static TieOrder make(int mode, uint32_t who, bool wide = false) {
         TieOrder t;
         t.mode = mode;
-        t.salt = mode == 2 ? ((who + 1u) * 0x9E3779B1u) & 0xffffffu : 0u;
+        t.mask = wide ? 0xffffffffu : 0xffffffu;
+        t.salt = mode == 2 ? ((who + 1u) * 0x9E3779B1u) & t.mask : 0u;
         return t;
     }
+    // an odd multiplier is a bijection modulo 2^24 and 2^32 alike
     __device__ __forceinline__ uint32_t fwd(uint32_t u) const {
-        return mode ? ((u ^ salt) * kTieMul) & 0xffffffu : u;
+        return mode ? ((u ^ salt) * kTieMul) & mask : u;
     }
     __device__ __forceinline__ int back(uint32_t t) const {
-        return (int)(mode ? ((t * tie_inverse(kTieMul)) & 0xffffffu) ^ salt : t);
+        return (int)(mode ? ((t * tie_inverse(kTieMul)) & mask) ^ salt : t);
     }
 };
 
@@ -500,7 +526,6 @@ __device__ __forceinline__ void load_row(const int32_t *ids, int cap, int lane, 
 // ascending, and empties when the worst distance drops.
 // On return T[0..ts) holds the result as 64-bit keys (make_key of the tie id)
 // ascending by (d, tie id).  false = visited-set overflow.
-__device__ __forceinline__ uint32_t k32(uint32_t d, uint32_t tie) { return (d << 24) | tie; }
 
 // ---- distance policies -------------------------------------------------------
 // fp32 L2 (fa_l2sq_f32 tree, common.cuh l2_tree) of four (query, vector) pairs
@@ -541,12 +566,28 @@ __device__ __forceinline__ float warp_l2_group8(const float *q, const float *__r
     return sum;
 }
 
-// Flash (kind 4): keys (d << 24 | tie id) with the uint8 table distance d; the
-// query context is the query's ADT in shared memory.
-struct FlashDist {
-    using Key = uint32_t;
+// Key layout of a policy: (d << kShift) | tie id, tie ids of kShift bits.
+// Narrow (W = false): 24-bit ids (n < 2^24), Flash keys fit 32 bits.  Wide
+// (W = true, n >= 2^24): 32-bit ids, 64-bit keys (d << 32 | tie), 32-bit
+// visited-set slots and 64-bit global-tier entries.
+template <typename KeyT, bool W>
+struct KeyLayout {
+    using Key = KeyT;
+    static constexpr bool kWide = W;
+    static constexpr int kShift = W ? 32 : 24;
+    static constexpr uint32_t kTieMask = W ? 0xffffffffu : 0xffffffu;
+    __device__ static __forceinline__ Key key(uint32_t d, uint32_t tie) {
+        return ((Key)d << kShift) | (Key)tie;
+    }
+    __device__ static __forceinline__ uint32_t dist(Key k) { return (uint32_t)(k >> kShift); }
+    __device__ static __forceinline__ uint32_t tie(Key k) { return (uint32_t)k & kTieMask; }
+};
+
+// Flash (kind 4): keys (d << 24 | tie id) with the uint8 table distance d
+// (wide: d << 32 | tie); the query context is the query's ADT in shared memory.
+template <bool W>
+struct FlashDistT : KeyLayout<typename std::conditional<W, uint64_t, uint32_t>::type, W> {
     static constexpr bool kExact = false;
-    __device__ static __forceinline__ Key key(uint32_t d, uint32_t tie) { return (d << 24) | tie; }
     __device__ static __forceinline__ void dists(const Graph &g, const uint8_t *qc,
                                                  const int32_t *ids, int nf, uint32_t *out,
                                                  int lane) {
@@ -557,17 +598,16 @@ struct FlashDist {
         return adt_one(qc, g.codes + (size_t)v * g.mpad, g.mpad, lane);
     }
 };
+using FlashDist = FlashDistT<false>;
+using FlashDistW = FlashDistT<true>;
 
 // Exact (kind 0, asym_one / sym_one of K_EXACT, _core.pyx:167-191): every
 // distance is the fp32 L2 of the vectors; keys (fp32 bits << 24 | tie id) —
-// the bit pattern of a non-negative float orders like its value.  The query
-// context is the query vector in shared memory.
-struct ExactDist {
-    using Key = uint64_t;
+// the bit pattern of a non-negative float orders like its value (wide: << 32).
+// The query context is the query vector in shared memory.
+template <bool W>
+struct ExactDistT : KeyLayout<uint64_t, W> {
     static constexpr bool kExact = true;
-    __device__ static __forceinline__ Key key(uint32_t d, uint32_t tie) {
-        return ((uint64_t)d << 24) | tie;
-    }
     __device__ static __forceinline__ void dists(const Graph &g, const uint8_t *qc,
                                                  const int32_t *ids, int nf, uint32_t *out,
                                                  int lane) {
@@ -589,14 +629,17 @@ struct ExactDist {
         return __shfl_sync(0xffffffffu, __float_as_uint(s), 0);
     }
 };
+using ExactDist = ExactDistT<false>;
+using ExactDistW = ExactDistT<true>;
 
 // ---- register-resident result set (W <= kRegSetMax) -------------------------
 // Lane l owns slots l + 32 j (j < J); slot s is live iff s < ts.  Bit j of `fl`
 // marks slot j expanded.  Every loop over j is unrolled (no dynamic register
 // indexing), so pop / worst distance / eviction are register compares plus one
 // warp reduction instead of passes over shared memory.
-template <int J, typename K = uint32_t>
+template <int J, typename P>
 struct RegSet {
+    using K = typename P::Key;
     K key[J];
     uint32_t fl;
     // this lane's live slots when the set holds ts entries (a prefix of j)
@@ -624,25 +667,25 @@ struct RegSet {
         }
     }
     // eviction victim over the slots of mask lm: the largest distance, smallest
-    // tie among those = the largest key ^ 0xFFFFFF (vf; vj = -1 if none)
+    // tie among those = the largest key ^ tie mask (vf; vj = -1 if none)
     __device__ __forceinline__ void victim(uint32_t lm, K &vf, int &vj) const {
         vf = 0;
         vj = -1;
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const K kf = key[j] ^ K(0xffffffu);
+            const K kf = key[j] ^ K(P::kTieMask);
             if (((lm >> j) & 1u) && (vj < 0 || kf > vf)) {
                 vf = kf;
                 vj = j;
             }
         }
     }
-    // largest distance (key >> 24) over the live slots
+    // largest distance over the live slots
     __device__ __forceinline__ uint32_t maxd(int ts, int lane) const {
         uint32_t mx = 0;
 #pragma unroll
         for (int j = 0; j < J; ++j)
-            if (lane + 32 * j < ts) mx = max(mx, (uint32_t)(key[j] >> 24));
+            if (lane + 32 * j < ts) mx = max(mx, P::dist(key[j]));
         return __reduce_max_sync(0xffffffffu, mx);
     }
     __device__ __forceinline__ void put(int js, K k) {
@@ -732,7 +775,7 @@ __device__ __forceinline__ void warp_bitonic(K (&k)[J], int lane) {
 // (d, tie) order, filling free slots first, then each evicting the current
 // victim (largest d, smallest tie) while it is still below the worst.
 template <typename P, int J>
-__device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, int &ts, int W,
+__device__ __forceinline__ void accept_offers(RegSet<J, P> &rs, int &ts, int W,
                                               uint32_t &wd, int &tq_h, int &tq_t, int32_t *TQ,
                                               typename P::Key *Sa, typename P::Key *Sb,
                                               const int32_t *fresh, const uint32_t *fdist, int nf,
@@ -779,7 +822,7 @@ __device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, in
     // stale = the set changed since wd was last known
     bool stale = ts == W && nfill > 0;
     if (nfill < ns) {
-        const uint32_t lm = RegSet<J, K>::live_mask(ts, lane);
+        const uint32_t lm = RegSet<J, P>::live_mask(ts, lane);
         for (int j = nfill; j < ns; ++j) {
             const K s = src[j];
             // victim: largest distance, smallest tie; its distance is the
@@ -790,7 +833,7 @@ __device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, in
             K m = 0;
             int owner = 0;
             warp_pick_max(vj >= 0, vf, m, owner);
-            const uint32_t cur = (uint32_t)(m >> 24);
+            const uint32_t cur = P::dist(m);
             if (cur < wd) {
                 // the evicted ties are beyond the new worst (none before the
                 // set first fills)
@@ -798,10 +841,10 @@ __device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, in
                 wd = cur;
             }
             stale = false;
-            if ((uint32_t)(s >> 24) >= wd) break;  // sorted: later offers are rejected too
+            if (P::dist(s) >= wd) break;  // sorted: later offers are rejected too
             const uint32_t expd = __shfl_sync(FULL, (rs.fl >> vj) & 1u, owner);
             if (!expd) {
-                if (lane == 0) TQ[tq_t] = (int32_t)((m ^ 0xffffffu) & 0xffffffu);
+                if (lane == 0) TQ[tq_t] = (int32_t)P::tie(m ^ K(P::kTieMask));
                 ++tq_t;
             }
             if (lane == owner) rs.put(vj, s);
@@ -819,9 +862,10 @@ __device__ __forceinline__ void accept_offers(RegSet<J, typename P::Key> &rs, in
 }
 
 // The result set out, ascending, as 64-bit keys: T[0..ts).
-template <int J, typename K>
-__device__ __forceinline__ void sort_out(const RegSet<J, K> &rs, int ts, unsigned long long *T,
+template <typename P, int J>
+__device__ __forceinline__ void sort_out(const RegSet<J, P> &rs, int ts, unsigned long long *T,
                                          int lane) {
+    using K = typename P::Key;
     // sort once: bitonic network over the 32 * J register slots (empty slots
     // hold the largest key and sort last), then the first ts go out
     // (J not a power of two: the network runs over JP registers, the extra
@@ -835,7 +879,7 @@ __device__ __forceinline__ void sort_out(const RegSet<J, K> &rs, int ts, unsigne
 #pragma unroll
     for (int j = 0; j < JP; ++j) {
         const int e = 32 * j + lane;
-        if (e < ts) T[e] = make_key((uint32_t)(ks[j] >> 24), (int)(ks[j] & 0xffffffu));
+        if (e < ts) T[e] = make_key(P::dist(ks[j]), P::tie(ks[j]));
     }
     __syncwarp();
 }
@@ -855,10 +899,10 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     K *Sa = reinterpret_cast<K *>(S);
     K *Sb = Sa + cand_capacity(g);
     const unsigned lt = (1u << lane) - 1u;
-    VisitedSet<KB> vs;
+    VisitedSet<KB, P::kWide> vs;
     vs.begin(H, hlog2, g, gs, lane);
     if (lane == 0) vs.visit(entry);
-    RegSet<J, K> rs;
+    RegSet<J, P> rs;
 #pragma unroll
     for (int j = 0; j < J; ++j) rs.key[j] = K(0);
     rs.fl = 0u;
@@ -880,7 +924,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         if (EM == 1) {
             K b1, b2;
             int j1;
-            const uint32_t um = RegSet<J, K>::live_mask(ts, lane) & ~rs.fl;
+            const uint32_t um = RegSet<J, P>::live_mask(ts, lane) & ~rs.fl;
             rs.min2(um, b1, j1, b2);
             const int nl = __popc(um);
             K m = 0;
@@ -890,7 +934,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             if (!anyT && !anyQ) break;
             const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
             const bool fromT = anyT && (!anyQ || m < kQ);
-            pv[0] = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
+            pv[0] = to.back(P::tie(fromT ? m : kQ));
             npop = 1;
             if (fromT) {
                 if (lane == owner) rs.fl |= 1u << j1;
@@ -913,7 +957,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             const bool anyQ2 = tq_h < tq_t;
             if (anyT2 || anyQ2) {
                 const K kQ2 = anyQ2 ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
-                pre_v = to.back((uint32_t)((anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2) & 0xffffffu));
+                pre_v = to.back(P::tie(anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2));
                 load_row(row_ids(g, layer, pre_v), cap, lane, pre);
             } else {
                 pre_v = -1;
@@ -924,7 +968,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                 if (r >= E) break;
                 K best, b2;
                 int bj;
-                rs.min2(RegSet<J, K>::live_mask(ts, lane) & ~rs.fl, best, bj, b2);
+                rs.min2(RegSet<J, P>::live_mask(ts, lane) & ~rs.fl, best, bj, b2);
                 const bool has = bj >= 0;
                 K m = 0;
                 int owner = -1;
@@ -933,7 +977,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                 if (!anyT && !anyQ) break;
                 const K kQ = anyQ ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
                 const bool fromT = anyT && (!anyQ || m < kQ);
-                pv[r] = to.back((uint32_t)((fromT ? m : kQ) & 0xffffffu));
+                pv[r] = to.back(P::tie(fromT ? m : kQ));
                 ++npop;
                 if (fromT) {
                     if (lane == owner) rs.fl |= 1u << bj;
@@ -983,15 +1027,15 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         phase_mark(cnt, 2, tph);
         accept_offers<P, J>(rs, ts, W, wd, tq_h, tq_t, TQ, Sa, Sb, fresh, fdist, nf, to, lane);
     }
-    sort_out<J>(rs, ts, T, lane);
+    sort_out<P, J>(rs, ts, T, lane);
     ts_out = ts;
     return true;
 }
 
 // Generic-key warp helpers of the shared-memory result set.  Keys are distinct.
 // min key over the entries not yet expanded (F[i] == 0), or, with dsel_on,
-// over the entries whose distance (key >> 24) equals dsel; idx = its slot.
-template <typename Kt>
+// over the entries whose distance equals dsel; idx = its slot.
+template <typename P, typename Kt = typename P::Key>
 __device__ __forceinline__ Kt warp_argmin_key(const Kt *K, const uint8_t *F, int n, bool dsel_on,
                                               uint32_t dsel, int lane, int &idx) {
     Kt best = ~Kt(0);
@@ -1001,7 +1045,7 @@ __device__ __forceinline__ Kt warp_argmin_key(const Kt *K, const uint8_t *F, int
         const int i = c + lane;
         if (i < n) {
             const Kt k = K[i];
-            const bool ok = dsel_on ? ((uint32_t)(k >> 24) == dsel) : (F[i] == 0);
+            const bool ok = dsel_on ? (P::dist(k) == dsel) : (F[i] == 0);
             if (ok && k < best) {
                 best = k;
                 bi = i;
@@ -1018,13 +1062,13 @@ __device__ __forceinline__ Kt warp_argmin_key(const Kt *K, const uint8_t *F, int
     return m;
 }
 
-template <typename Kt>
+template <typename P, typename Kt = typename P::Key>
 __device__ __forceinline__ uint32_t warp_maxd_key(const Kt *K, int n, int lane) {
     uint32_t mx = 0;
 #pragma unroll 4
     for (int c = 0; c < n; c += 32) {
         const int i = c + lane;
-        if (i < n) mx = max(mx, (uint32_t)(K[i] >> 24));
+        if (i < n) mx = max(mx, P::dist(K[i]));
     }
     return __reduce_max_sync(0xffffffffu, mx);
 }
@@ -1047,7 +1091,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
     uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
     Kt *Sa = reinterpret_cast<Kt *>(S);
     Kt *Sb = Sa + cand_capacity(g);
-    VisitedSet<> vs;
+    VisitedSet<0, P::kWide> vs;
     vs.begin(H, hlog2, g, gs, lane);
     if (lane == 0) {
         vs.visit(entry);
@@ -1073,11 +1117,11 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         for (int r = 0; r < kMaxExpand; ++r) {
             if (r >= E) break;
             int ia;
-            const Kt kT = warp_argmin_key(K, F, ts, false, 0u, lane, ia);
+            const Kt kT = warp_argmin_key<P>(K, F, ts, false, 0u, lane, ia);
             const Kt kQ = tq_h < tq_t ? P::key(wd, (uint32_t)TQ[tq_h]) : NONE;
             if (kT == NONE && kQ == NONE) break;
             const bool fromT = kT < kQ;
-            pv[r] = to.back((uint32_t)((fromT ? kT : kQ) & 0xffffffu));
+            pv[r] = to.back(P::tie(fromT ? kT : kQ));
             ++npop;
             __syncwarp();
             if (fromT) {
@@ -1103,10 +1147,10 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         if (E == 1) {  // predict the next pop assuming nothing new enters
             int ib;
-            const Kt k1 = warp_argmin_key(K, F, ts, false, 0u, lane, ib);
+            const Kt k1 = warp_argmin_key<P>(K, F, ts, false, 0u, lane, ib);
             const Kt k2 = tq_h < tq_t ? P::key(wd, (uint32_t)TQ[tq_h]) : NONE;
             const Kt kn = k1 < k2 ? k1 : k2;
-            pre_v = kn != NONE ? to.back((uint32_t)(kn & 0xffffffu)) : -1;
+            pre_v = kn != NONE ? to.back(P::tie(kn)) : -1;
             if (pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         }
         cnt.visited += npop;
@@ -1166,7 +1210,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
             }
             ts += ns;
             __syncwarp();
-            if (ts == W) wd = warp_maxd_key(K, ts, lane);
+            if (ts == W) wd = warp_maxd_key<P>(K, ts, lane);
             continue;
         }
         // offers are processed in ascending order: rank-sort them
@@ -1183,14 +1227,14 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         ts += nfill;
         __syncwarp();
-        wd = warp_maxd_key(K, ts, lane);
+        wd = warp_maxd_key<P>(K, ts, lane);
         for (int j = nfill; j < ns; ++j) {
             const Kt s = Sb[j];
-            if ((uint32_t)(s >> 24) >= wd) break;  // sorted: every later offer is rejected too
+            if (P::dist(s) >= wd) break;  // sorted: every later offer is rejected too
             int e;
-            const Kt ev = warp_argmin_key(K, F, ts, true, wd, lane, e);
+            const Kt ev = warp_argmin_key<P>(K, F, ts, true, wd, lane, e);
             if (!F[e]) {
-                if (lane == 0) TQ[tq_t] = (int32_t)(ev & 0xffffffu);
+                if (lane == 0) TQ[tq_t] = (int32_t)P::tie(ev);
                 ++tq_t;
             }
             __syncwarp();
@@ -1199,7 +1243,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
                 F[e] = 0;
             }
             __syncwarp();
-            const uint32_t nwd = warp_maxd_key(K, ts, lane);
+            const uint32_t nwd = warp_maxd_key<P>(K, ts, lane);
             if (nwd < wd) {
                 wd = nwd;
                 tq_h = tq_t = 0;  // the evicted ties are beyond the new worst
@@ -1211,7 +1255,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         const Kt k = K[i];
         int r = 0;
         for (int t = 0; t < ts; ++t) r += K[t] < k;
-        T[r] = make_key((uint32_t)(k >> 24), (int)(k & 0xffffffu));
+        T[r] = make_key(P::dist(k), P::tie(k));
     }
     __syncwarp();
     return true;

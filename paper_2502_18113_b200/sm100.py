@@ -96,8 +96,9 @@ def _require_flash(kind: int) -> None:
 # Capacities of the sm_100a build (checked up front with the limit named,
 # before any device work): layer-0 rows of 2R <= 127 slots (id rows of up to
 # four 32-slot chunks held in registers), candidate width C <= 2048, m <= 128
-# subspaces, and 24-bit vertex ids in the search keys.
-DEVICE_LIMITS = {"R_max": 63, "C_max": 2048, "m_max": 128, "n_max": (1 << 24) - 2}
+# subspaces, and int32 vertex ids (n >= 2^24 - 1 selects the wide-id kernels:
+# 64-bit search keys with 32-bit tie ids).
+DEVICE_LIMITS = {"R_max": 63, "C_max": 2048, "m_max": 128, "n_max": (1 << 31) - 2}
 
 
 def check_limits(n: int, C_: int, R: int, m: int = 0) -> None:
@@ -113,7 +114,7 @@ def check_limits(n: int, C_: int, R: int, m: int = 0) -> None:
         raise ConfigError(f"m={m}: the sm100 core supports m <= {lim['m_max']} subspaces")
     if n > lim["n_max"]:
         raise ConfigError(f"n={n}: the sm100 core addresses n <= {lim['n_max']} vertices "
-                          "(24-bit ids in the search keys)")
+                          "(int32 ids)")
 
 
 def build_options(C_: int) -> _lib.BuildOpts:

@@ -95,6 +95,6 @@ def test_device_limits_named_up_front():
 
     sm100.check_limits(1000, 2048, 63, 128)
     for args in ((1000, 200, 64, 16), (1000, 4096, 32, 16), (1000, 200, 32, 129),
-                 (1 << 24, 200, 32, 16)):
+                 (1 << 31, 200, 32, 16)):
         with pytest.raises(errors.ConfigError):
             sm100.check_limits(*args)
