@@ -701,20 +701,6 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         fprintf(stderr, "[fa timing] build host setup (schedule, scratch) %8.2f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                           t_host0).count());
-    size_t l2pin_bytes = 0;
-    if (const char *e = getenv("FLASHANN_B200_L2PIN")) {
-        if (atoi(e) > 0) {
-            int dev = 0, maxwin = 0, maxpers = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-            cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev);
-            l2pin_bytes = std::min<size_t>((size_t)g.n * g.mpad, (size_t)maxwin);
-            FA_BUILD_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
-                                             std::min<size_t>(l2pin_bytes, (size_t)maxpers)));
-            fprintf(stderr, "[fa] L2 pin %zu B (window max %d, persisting max %d)\n", l2pin_bytes,
-                    maxwin, maxpers);
-        }
-    }
     int64_t launches = r0 == 0 ? 3 : 1;  // the two row resets of reset_graph, the SDT transpose
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
@@ -762,35 +748,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         // work counter, nheads[2]: the bucketing cursor
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 3 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
-        if (l2pin_bytes) {
-            // experiment (FLASHANN_B200_L2PIN=1): the code table as a persisting
-            // L2 window of the search launches
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(bw * 32);
-            cfg.dynamicSmemBytes = smem_search;
-            cfg.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-            at[0].val.accessPolicyWindow.base_ptr = (void *)g.codes;
-            at[0].val.accessPolicyWindow.num_bytes = l2pin_bytes;
-            at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-            at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            FA_BUILD_CUDA(cudaLaunchKernelEx(&cfg, search_fn, gb, (const uint8_t *)sdtT,
-                                             (const uint8_t *)adt_batch, (int)b.start, b.size,
-                                             b.ep, b.ml, C, R, L,
-                                             (const int64_t *)(req_off_d + b.start),
-                                             (const int32_t *)(order_d + b.start), req, ctr, err,
-                                             opts->point_stats, nheads + 1));
-        } else {
-            search_fn<<<grid, bw * 32, smem_search, st>>>(
-                gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
-                order_d + b.start,
-                req, ctr, err, opts->point_stats, nheads + 1);
-        }
+        search_fn<<<grid, bw * 32, smem_search, st>>>(
+            gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+            order_d + b.start,
+            req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         // bucket the requests by row: segments for the touched rows, then
