@@ -144,6 +144,7 @@ static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t sme
     ix->g.gvis_owner = ix->gvis_owner;
     ix->g.gvis_nslots = ns;
     ix->g.gvis_log2 = lg;
+    ix->g.gvis_words = ix->wide ? 2 : 1;
     return FA_OK;
 }
 
@@ -332,6 +333,7 @@ extern "C" int fa_index_create(const fa_index_desc *desc, fa_index **out) {
     g.gvis_owner = nullptr;
     g.gvis_log2 = 14;
     g.gvis_nslots = 0;
+    g.gvis_words = 1;
     g.rowcnt = nullptr;
     g.touched = nullptr;
     g.ntouched = nullptr;
@@ -608,6 +610,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     gb.gvis_owner = g.gvis_owner;
     gb.gvis_log2 = g.gvis_log2;
     gb.gvis_nslots = g.gvis_nslots;
+    gb.gvis_words = g.gvis_words;
 
     uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;

@@ -43,6 +43,7 @@ struct Graph {
     uint32_t *gvis_epoch;  // their epoch counters
     uint32_t *gvis_owner;  // 1 while a search holds the slot (claimed atomically)
     int gvis_log2, gvis_nslots;
+    int gvis_words;        // u32 words per entry: 1 (narrow ids), 2 (wide: 64-bit entries)
     const float *vecs;     // n x dim vectors (exact kind: every distance; rerank)
     int dim;
     // reverse-request bucketing of a build batch (reverse.cu): requests per
@@ -309,7 +310,7 @@ __device__ inline GSlot gslot_claim(const Graph &g, int lane) {
     }
     slot = __shfl_sync(0xffffffffu, slot, 0);
     gs.epoch = __shfl_sync(0xffffffffu, e, 0);
-    gs.G = g.gvis + ((size_t)slot << g.gvis_log2);
+    gs.G = g.gvis + ((size_t)slot << g.gvis_log2) * g.gvis_words;
     gs.own = g.gvis_owner + slot;
     gs.ep = g.gvis_epoch + slot;
     return gs;
