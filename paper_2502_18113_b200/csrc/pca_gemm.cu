@@ -12,12 +12,14 @@
 // Accumulation: the tensor core's fp32 accumulator does not round to nearest
 // (it truncates after aligning to the largest term), so a long chain of MMAs
 // into one TMEM tile drifts (4.6e-6 relative over 375 MMAs, measured, against
-// 3e-7 for the reference's sgemm).  Each stage (K = 32) therefore goes into a
-// fresh pair of TMEM accumulators — hi*hi (4 MMAs) and the two small cross
-// terms (8 MMAs, whose truncation is relative to their own 2^-11-smaller
-// magnitude) — and the epilogue warps add every stage's pair into fp32
-// running sums in registers with round-to-nearest FADDs.  Two such pairs
-// alternate, so the epilogue drains one while the tensor core fills the other.
+// 3e-7 for the reference's sgemm).  The hi*hi term of each stage (K = 32, 4
+// MMAs) therefore goes into a fresh TMEM accumulator, which the epilogue warps
+// add into fp32 running sums in registers with round-to-nearest FADDs; two
+// such accumulators alternate, so the epilogue drains one while the tensor
+// core fills the other.  The two cross terms (lo*hi, hi*lo) are 2^-11 smaller,
+// so their truncation drift is ~2^-11 smaller too: they accumulate over the
+// whole tile in a third accumulator (double-buffered across tiles) drained
+// once at the end.
 //
 // One persistent CTA per SM, warp-specialised (448 threads):
 //   warp 0      TMA producer: raw X tiles (and, for the projection, the
@@ -34,7 +36,8 @@
 //               global fp32 at the end of the tile.
 // Barriers: full (TMA -> converters, transaction bytes), conv (converters ->
 // MMA), empty (MMA commit -> TMA), tfull / tempty (MMA <-> epilogue, per
-// stage, double-buffered accumulator pairs).
+// stage, the hi*hi accumulators), sfull / sempty (per tile, the cross-term
+// accumulators).
 //
 // The covariance is symmetric: only tiles with n-block >= m-block are
 // computed, split over K (rows of X) into per-split fp32 partials that a
@@ -53,9 +56,14 @@ namespace pg {
 
 constexpr int BM = 128;   // tile rows (MMA M, TMEM lanes)
 constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row = one stage's K
-constexpr int kThreads = 448;
+// 14 warps (4 converter warps: the conversion is on the critical path); with
+// 4 warps on some SM sub-partitions a thread holds at most 128 registers, so
+// the epilogue drains TMEM 16 columns at a time
+constexpr int kConvWarps = 4, kEpiWarps = 8;
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kThreads = 32 * (2 + kConvWarps + kEpiWarps);
 constexpr int kStages = 2;
-constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
+constexpr int kConvWarp0 = 2, kEpiWarp0 = kConvWarp0 + kConvWarps;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -228,22 +236,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *empty = conv + kStages;
     uint64_t *tfull = empty + kStages;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *sfull = tempty + 2;
+    uint64_t *sempty = sfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sempty + 2);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // two accumulator pairs (hi*hi, cross terms) of BN columns each
+    // TMEM: hi*hi accumulators of stages (2 x BN columns), then the cross-term
+    // accumulators of tiles (2 x BN)
     constexpr uint32_t kTmemCols = 4 * BN;
     static_assert(4 * BN <= 512, "TMEM holds 512 fp32 columns");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(conv + s, 128);
+            mbar_init(conv + s, kConvThreads);
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 256);
+            mbar_init(sfull + a, 1);
+            mbar_init(sempty + a, 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -309,8 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = idesc_tf32(BN);
             int s = 0;
             uint32_t ph = 0;
-            uint32_t fl = 0;  // stages flushed so far (accumulator pair = fl & 1)
-            for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
+            uint32_t fl = 0;  // stages flushed so far (hi*hi accumulator = fl & 1)
+            uint32_t it = 0;  // tiles so far (cross-term accumulator = it & 1)
+            for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x, ++it) {
                 int k0, k1;
                 bool diag = false;
                 if constexpr (COV) {
@@ -322,14 +336,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     k0 = 0;
                     k1 = p.nk;
                 }
+                const uint32_t sa = it & 1u;
+                mbar_wait(sempty + sa, ((it >> 1) & 1u) ^ 1u);
+                const uint32_t d_small = tmem_base + 2 * BN + sa * BN;
                 for (int kb = k0; kb < k1; ++kb, ++fl) {
                     const uint32_t acc = fl & 1u;
                     mbar_wait(tempty + acc, ((fl >> 1) & 1u) ^ 1u);
                     mbar_wait(full + s, ph);
                     mbar_wait(conv + s, ph);
                     tc_fence_after();
-                    const uint32_t d_big = tmem_base + acc * (2 * BN);
-                    const uint32_t d_small = d_big + BN;
+                    const uint32_t d_big = tmem_base + acc * BN;
                     uint8_t *st = smem + s * L::stage;
                     const uint32_t ahi = smem_u32(st + L::off_ahi), alo = smem_u32(st + L::off_alo);
                     const uint32_t bhi = COV && diag ? ahi : smem_u32(st + L::off_bhi);
@@ -338,22 +354,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < BK / 8; ++k) {
                         const uint32_t o = (uint32_t)k * 32u;  // 8 tf32 = 32 bytes along K
                         const uint32_t more = k > 0 ? 1u : 0u;
+                        const uint32_t smore = (kb > k0 || k > 0) ? 1u : 0u;
                         mma_tf32(d_big, sdesc(ahi + o), sdesc(bhi + o), idesc, more);
-                        mma_tf32(d_small, sdesc(alo + o), sdesc(bhi + o), idesc, more);
+                        mma_tf32(d_small, sdesc(alo + o), sdesc(bhi + o), idesc, smore);
                         mma_tf32(d_small, sdesc(ahi + o), sdesc(blo + o), idesc, 1u);
                     }
                     tc_commit(empty + s);       // the stage's smem is free once these retire
-                    tc_commit(tfull + acc);     // and the pair is ready for the epilogue
+                    tc_commit(tfull + acc);     // and its hi*hi sums are ready to drain
                     if (++s == kStages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
+                tc_commit(sfull + sa);  // the tile's cross terms are complete
             }
         }
     } else if (warp >= kConvWarp0 && warp < kEpiWarp0) {
         // ===== converters: raw -> centred -> hi / lo, K-major SW128 =====
-        const int t = threadIdx.x - kConvWarp0 * 32;  // 0..127
+        const int t = threadIdx.x - kConvWarp0 * 32;  // 0 .. kConvThreads - 1
         int s = 0;
         uint32_t ph = 0;
         for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
@@ -374,10 +392,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(full + s, ph);
                 uint8_t *st = smem + s * L::stage;
                 if constexpr (COV) {
-                    // thread t owns column t of the block: rows k of the raw
-                    // tile become the K of operand row t (a transpose)
-                    for (int op = 0; op < (diag ? 1 : 2); ++op) {
-                        const int col = (op ? n0 : m0) + t;
+                    // thread t owns columns t, t + kConvThreads, ... of the
+                    // block: rows k of the raw tile become the K of operand
+                    // row t (a transpose)
+                    for (int op = 0; op < (diag ? 1 : 2); ++op)
+                    for (int tc = t; tc < BM; tc += kConvThreads) {
+                        const int col = (op ? n0 : m0) + tc;
                         const bool cin = col < p.D;
                         const float mu = cin ? __ldg(p.mean + col) : 0.f;
                         const T *raw = reinterpret_cast<const T *>(st + (op ? L::off_rawB : L::off_rawA));
@@ -392,9 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int j = 0; j < 4; ++j) {
                                 const int kr = 4 * c + j;
                                 const bool in = cin && kr0 + kr < p.n;
-                                av[j] = in ? widen(raw[kr * BM + t]) - mu : 0.f;
+                                av[j] = in ? widen(raw[kr * BM + tc]) - mu : 0.f;
                             }
-                            split_store(hi, lo, sw128(t, c), a);
+                            split_store(hi, lo, sw128(tc, c), a);
                         }
                     }
                 } else {
@@ -403,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t *lo = st + L::off_alo;
                     constexpr int per16 = 16 / (int)sizeof(T);  // elements per 16-byte chunk
                     constexpr int cpr = BK / per16;             // chunks per raw row
-                    constexpr int iters = BM * cpr / 128;
+                    constexpr int iters = BM * cpr / kConvThreads;
                     const int ch = t % cpr;  // fixed per thread
                     float mu[per16];
 #pragma unroll
@@ -413,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
 #pragma unroll
                     for (int i = 0; i < iters; ++i) {
-                        const int idx = t + 128 * i;
+                        const int idx = t + kConvThreads * i;
                         const int row = idx / cpr;
                         const uint4 v = *reinterpret_cast<const uint4 *>(raw + row * BK + ch * per16);
                         const T *e = reinterpret_cast<const T *>(&v);
@@ -443,8 +463,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;     // TMEM lane quarter this warp may access
         const int h = (warp - kEpiWarp0) >> 2;
         const int r = 32 * q + lane;
-        uint32_t fl = 0;
-        for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
+        uint32_t fl = 0, it = 0;
+        for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x, ++it) {
             int m0, n0, k0, k1;
             float *dst;
             int64_t ld;
@@ -471,24 +491,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             float sum[HC];
 #pragma unroll
             for (int j = 0; j < HC; ++j) sum[j] = 0.f;
+            const uint32_t lanebase = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * HC);
             for (int kb = k0; kb < k1; ++kb, ++fl) {
                 const uint32_t acc = fl & 1u;
                 mbar_wait(tfull + acc, (fl >> 1) & 1u);
                 tc_fence_after();
-                const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * (2 * BN) +
-                                    (uint32_t)(h * HC);
+                const uint32_t tb = lanebase + acc * BN;
 #pragma unroll
                 for (int c = 0; c < HC / 16; ++c) {
-                    uint32_t vb[16], vs[16];
+                    uint32_t vb[16];
                     tmem_ld16(tb + 16 * c, vb);
-                    tmem_ld16(tb + BN + 16 * c, vs);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        sum[16 * c + j] += __uint_as_float(vb[j]) + __uint_as_float(vs[j]);
+                    for (int j = 0; j < 16; ++j) sum[16 * c + j] += __uint_as_float(vb[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(tempty + acc);
+            }
+            {  // the tile's cross terms, once
+                const uint32_t sa = it & 1u;
+                mbar_wait(sfull + sa, (it >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t tb = lanebase + 2 * BN + sa * BN;
+#pragma unroll
+                for (int c = 0; c < HC / 16; ++c) {
+                    uint32_t vs[16];
+                    tmem_ld16(tb + 16 * c, vs);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sum[16 * c + j] += __uint_as_float(vs[j]);
+                }
+                tc_fence_before();
+                mbar_arrive(sempty + sa);
             }
             const int64_t row = (int64_t)m0 + r;
             const int col0 = n0 + h * HC;
