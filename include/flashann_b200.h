@@ -210,6 +210,9 @@ typedef struct {
                              pop / row+visited / distances / acceptance (0
                              unless built with FA_PHASE_PROFILE=1),
                              forward-selection cycles, distance evaluations   */
+    int batch_min;        /* batches of at least min(inserted, batch_min) while
+                             frac * inserted is smaller (fills the GPU sooner);
+                             < 0 = auto: clamp(n / 256, 1, 4096); 0 = off    */
     int64_t start, end;   /* insert vertices [start, end) (end 0 = n).  start 0
                              resets the graph; start > 0 resumes a graph whose
                              vertices [0, start) were inserted by earlier

@@ -75,10 +75,11 @@ def lib():
         L.or_hill_climb.argtypes = [C.POINTER(Graph), vp, C.c_int, C.c_int, vp,
                                     C.POINTER(Counters)]
         L.or_schedule.restype = C.c_int
-        L.or_schedule.argtypes = [vp, i64, C.c_int, f64, C.c_int, vp, vp]
+        L.or_schedule.argtypes = [vp, i64, C.c_int, f64, C.c_int, C.c_int, vp, vp]
         L.or_build.restype = C.c_int
         L.or_build.argtypes = [C.POINTER(Graph), vp, C.c_int, vp, vp, vp, C.c_int, f64, f64, vp,
-                               C.c_int, C.c_int, C.c_int, f64, C.c_int, C.POINTER(BuildResult)]
+                               C.c_int, C.c_int, C.c_int, f64, C.c_int, C.c_int,
+                               C.POINTER(BuildResult)]
         L.or_search.restype = C.c_int
         L.or_search.argtypes = [C.POINTER(Graph), vp, C.c_int, vp, vp, vp, C.c_int, f64, f64,
                                 C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int,
@@ -152,12 +153,13 @@ def select(sdt, codes, cand_ids, cand_d, cap):
     return [int(x) for x in out[:nk]]
 
 
-def schedule(levels, batch_max, batch_frac, seq_prefix):
+def schedule(levels, batch_max, batch_frac, seq_prefix, batch_min=-1):
     levels = _c(levels, np.int32)
     n = levels.shape[0]
     st = np.zeros(max(n, 1), np.int32)
     sz = np.zeros(max(n, 1), np.int32)
-    nb = lib().or_schedule(_p(levels), n, batch_max, batch_frac, seq_prefix, _p(st), _p(sz))
+    nb = lib().or_schedule(_p(levels), n, batch_max, batch_frac, seq_prefix, batch_min, _p(st),
+                           _p(sz))
     return st[:nb].copy(), sz[:nb].copy()
 
 
@@ -244,7 +246,7 @@ class HostGraph:
         return cur, d.value, c.as_dict()
 
     def build(self, proj, cent, dims, offs, dmin, delta, sdt, C_, batch_max=4096,
-              batch_frac=0.02, seq_prefix=256):
+              batch_frac=0.02, seq_prefix=256, batch_min=-1):
         proj = _c(proj, np.float32)
         cent, dims, offs = _c(cent, np.float32), _c(dims, np.int32), _c(offs, np.int32)
         sdt = _c(sdt, np.uint8)
@@ -252,18 +254,18 @@ class HostGraph:
         rc = lib().or_build(C.byref(self.s), _p(proj), proj.shape[1], _p(cent), _p(dims),
                             _p(offs), cent.shape[2], float(dmin), float(delta), _p(sdt), int(C_),
                             self.R, int(batch_max), float(batch_frac), int(seq_prefix),
-                            C.byref(res))
+                            int(batch_min), C.byref(res))
         if rc:
             raise MemoryError("oracle build failed")
         return {"entry_point": int(res.entry_point), "max_layer": int(res.max_layer),
                 "n_batches": int(res.n_batches), "counters": res.counters.as_dict()}
 
-    def build_exact(self, C_, batch_max=4096, batch_frac=0.02, seq_prefix=256):
+    def build_exact(self, C_, batch_max=4096, batch_frac=0.02, seq_prefix=256, batch_min=-1):
         """Exact kind: every distance is the fp32 L2 of the vectors."""
         z = np.zeros((1, 16, 1), np.float32)
         zi = np.zeros(1, np.int32)
         return self.build(self.vecs, z, zi, zi, 0.0, 1.0, np.zeros((1, 16, 16), np.uint8), C_,
-                          batch_max, batch_frac, seq_prefix)
+                          batch_max, batch_frac, seq_prefix, batch_min)
 
     def search_exact(self, entry, max_layer, queries, ef, k):
         z = np.zeros((1, 16, 1), np.float32)

@@ -512,8 +512,10 @@ void or_reset(or_graph *g) {
 }
 
 int or_schedule(const int32_t *levels, int64_t n, int batch_max, double batch_frac, int seq_prefix,
-                int32_t *starts, int32_t *sizes) {
+                int batch_min, int32_t *starts, int32_t *sizes) {
     if (n <= 1) return 0;
+    /* batch_min < 0: auto, clamp(n / 256, 1, 4096) (the GPU build's rule) */
+    if (batch_min < 0) batch_min = n / 256 < 1 ? 1 : (n / 256 > 4096 ? 4096 : (int)(n / 256));
     int ml = levels[0], nb = 0;
     int64_t x = 1;
     while (x < n) {
@@ -523,6 +525,8 @@ int or_schedule(const int32_t *levels, int64_t n, int batch_max, double batch_fr
         else {
             double f = batch_frac * (double)x;
             B = (int)f;
+            int bm = x < batch_min ? (int)x : batch_min;
+            if (B < bm) B = bm;
             if (B > batch_max) B = batch_max;
             if (B < 1) B = 1;
         }
@@ -549,7 +553,8 @@ typedef struct {
 
 int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const int32_t *dims,
              const int32_t *offs, int dmax, double dmin, double delta, const uint8_t *sdt, int C,
-             int R, int batch_max, double batch_frac, int seq_prefix, or_build_result *res) {
+             int R, int batch_max, double batch_frac, int seq_prefix, int batch_min,
+             or_build_result *res) {
     memset(res, 0, sizeof(*res));
     res->entry_point = -1;
     res->max_layer = -1;
@@ -566,7 +571,8 @@ int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const
                           g->codes + (size_t)v * g->cs, NULL);
     int32_t *starts = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
     int32_t *sizes = (int32_t *)malloc(sizeof(int32_t) * (size_t)g->n);
-    int nb = or_schedule(g->levels, g->n, batch_max, batch_frac, seq_prefix, starts, sizes);
+    int nb = or_schedule(g->levels, g->n, batch_max, batch_frac, seq_prefix, batch_min, starts,
+                         sizes);
     int maxB = 1;
     for (int b = 0; b < nb; ++b)
         if (sizes[b] > maxB) maxB = sizes[b];

@@ -52,10 +52,11 @@ int or_layer_search_exact(or_graph *g, const float *qvec, int layer, int entry, 
 int or_hill_climb(or_graph *g, const uint8_t *adt, int layer, int entry, int *out_d,
                   or_counters *c);
 int or_schedule(const int32_t *levels, int64_t n, int batch_max, double batch_frac, int seq_prefix,
-                int32_t *starts, int32_t *sizes);
+                int batch_min, int32_t *starts, int32_t *sizes);
 int or_build(or_graph *g, const float *proj, int dproj, const float *cent, const int32_t *dims,
              const int32_t *offs, int dmax, double dmin, double delta, const uint8_t *sdt, int C,
-             int R, int batch_max, double batch_frac, int seq_prefix, or_build_result *res);
+             int R, int batch_max, double batch_frac, int seq_prefix, int batch_min,
+             or_build_result *res);
 int or_search(or_graph *g, const float *vecs, int dim, const float *cent, const int32_t *dims,
               const int32_t *offs, int dmax, double dmin, double delta, int dproj, int entry,
               int max_layer, const float *queries, const float *qproj, int nq, int ef, int k,

@@ -37,7 +37,7 @@ class BuildOpts(C.Structure):
     _fields_ = [("C", C.c_int), ("batch_max", C.c_int), ("batch_frac", f64),
                 ("seq_prefix", C.c_int), ("hash_log2", C.c_int), ("profile", C.c_int),
                 ("tie", C.c_int), ("expand", C.c_int), ("point_stats", vp),
-                ("start", i64), ("end", i64)]
+                ("batch_min", C.c_int), ("start", i64), ("end", i64)]
 
 
 class BuildResult(C.Structure):

@@ -87,7 +87,8 @@ def build_options(params: graph.BuildParams, start: int = 0, end: int = 0,
     return _lib.BuildOpts(C=params.C, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
                           seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
                           profile=o.get("profile", 0), tie=o.get("tie", 2),
-                          expand=o.get("expand", 1), start=int(start), end=int(end))
+                          expand=o.get("expand", 1), batch_min=o.get("batch_min", -1),
+                          start=int(start), end=int(end))
 
 
 def build_device(g: graph.GraphIndex, provider: FlashProvider, params: graph.BuildParams,

@@ -492,6 +492,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int Bmax = opts->batch_max > 0 ? opts->batch_max : 65536;
     const double frac = opts->batch_frac > 0 ? opts->batch_frac : 0.2;
     const int prefix = opts->seq_prefix >= 0 ? opts->seq_prefix : 256;
+    const int Bmin = opts->batch_min >= 0 ? opts->batch_min
+                                          : (int)std::min<int64_t>(4096, std::max<int64_t>(1, g.n / 256));
 
     // ---- schedule (pure function of the layer draws) ----
     // O(batches) from the level prefix sums and the record positions; the
@@ -529,7 +531,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             size = 1;  // a new top layer goes alone
             b.nreq = (int64_t)(ml + 1) * R;
         } else {
-            const int B = x < prefix ? 1 : std::max(1, std::min(Bmax, (int)(frac * (double)x)));
+            const int B = x < prefix ? 1
+                          : std::max(1, std::min(Bmax, std::max((int)(frac * (double)x),
+                                                                (int)std::min<int64_t>(x, Bmin))));
             int64_t end = std::min<int64_t>(r1, x + B);
             if (ri < ix->raisers.size()) end = std::min<int64_t>(end, ix->raisers[ri]);
             size = (int)(end - x);

@@ -49,6 +49,9 @@ BUILD_OPTIONS = {
     "batch_max": int(os.environ.get("FLASHANN_B200_BATCH_MAX", "65536")),
     "batch_frac": float(os.environ.get("FLASHANN_B200_BATCH_FRAC", "0.2")),
     "seq_prefix": int(os.environ.get("FLASHANN_B200_SEQ_PREFIX", "0")),
+    # batches of at least min(inserted, batch_min) while batch_frac * inserted
+    # is smaller: the GPU fills sooner (-1 = clamp(n / 256, 1, 4096))
+    "batch_min": int(os.environ.get("FLASHANN_B200_BATCH_MIN", "-1")),
     "hash_log2": int(os.environ.get("FLASHANN_B200_HASH_LOG2", "0")),
     # tie order among equal distances during insertion searches: 2 = id
     # scramble salted per inserted vertex; 0 reproduces
@@ -122,7 +125,7 @@ def build_options(C_: int) -> _lib.BuildOpts:
     return _lib.BuildOpts(C=C_, batch_max=o["batch_max"], batch_frac=o["batch_frac"],
                           seq_prefix=o["seq_prefix"], hash_log2=o["hash_log2"],
                           profile=o.get("profile", 0), tie=o.get("tie", 2),
-                          expand=o.get("expand", 1))
+                          expand=o.get("expand", 1), batch_min=o.get("batch_min", -1))
 
 
 def _prov_arrays(prov: dict):
