@@ -19,7 +19,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-LIBDIR = PKG / "lib"
+# FLASHANN_B200_LIBDIR: build into another directory (A/B experiment variants)
+LIBDIR = Path(os.environ.get("FLASHANN_B200_LIBDIR") or PKG / "lib")
 OBJDIR = LIBDIR / "obj"
 LIB = LIBDIR / "libflashann_b200.so"
 INCLUDE = PKG.parent / "include"

@@ -13,7 +13,9 @@ from pathlib import Path
 
 from .errors import DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libflashann_b200.so"
+# FLASHANN_B200_LIB: an alternative build of the core (A/B experiments)
+LIB_PATH = Path(os.environ.get("FLASHANN_B200_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libflashann_b200.so")
 
 FA_OK, FA_EINVAL, FA_ENOMEM, FA_ECUDA, FA_EOVERFLOW, FA_EEMPTY = 0, -1, -2, -3, -4, -5
 FA_DTYPE_F32, FA_DTYPE_BF16 = 0, 1
