@@ -21,13 +21,6 @@
 #ifndef FA_PHASE_PROFILE
 #define FA_PHASE_PROFILE 0
 #endif
-// A/B switches of experiments (FLASHANN_B200_NVCC_DEFS="-DFA_EXP_...=1")
-#ifndef FA_EXP_BRANCHY
-#define FA_EXP_BRANCHY 0
-#endif
-#ifndef FA_EXP_ROWBR
-#define FA_EXP_ROWBR 0
-#endif
 
 namespace fa {
 
@@ -74,14 +67,7 @@ __host__ __device__ inline int cand_capacity(const Graph &g) {
 }
 
 __device__ __forceinline__ const int32_t *row_ids(const Graph &g, int layer, int v) {
-#if FA_EXP_ROWBR
-    // layer is warp-uniform: a real branch, the upper-layer path (its uoff
-    // load and multiply) skipped at layer 0 instead of predicated
-    if (__builtin_expect(layer == 0, 1)) return g.adj0 + (int64_t)v * g.cap0p;
-    asm volatile("" ::: "memory");
-#else
     if (layer == 0) return g.adj0 + (int64_t)v * g.cap0p;
-#endif
     return g.adjU + (__ldg(g.uoff + v) + layer - 1) * g.capUp;
 }
 __device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
@@ -667,7 +653,6 @@ struct RegSet {
     __device__ __forceinline__ void min2(uint32_t um, K &b1, int &j1, K &b2) const {
         b1 = b2 = ~K(0);
         j1 = -1;
-#if FA_EXP_BRANCHY
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const K k = key[j];
@@ -681,17 +666,6 @@ struct RegSet {
                 }
             }
         }
-#else
-        // branch-free: masked slots read as the largest key (keys are distinct)
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const K k = ((um >> j) & 1u) ? key[j] : ~K(0);
-            const bool lt = k < b1;
-            b2 = lt ? b1 : min(b2, k);
-            j1 = lt ? j : j1;
-            b1 = lt ? k : b1;
-        }
-#endif
     }
     // eviction victim over the slots of mask lm: the largest distance, smallest
     // tie among those = the largest key ^ tie mask (vf; vj = -1 if none)
@@ -701,16 +675,10 @@ struct RegSet {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const K kf = key[j] ^ K(P::kTieMask);
-#if FA_EXP_BRANCHY
             if (((lm >> j) & 1u) && (vj < 0 || kf > vf)) {
                 vf = kf;
                 vj = j;
             }
-#else
-            const bool take = (((lm >> j) & 1u) != 0u) & ((vj < 0) | (kf > vf));
-            vf = take ? kf : vf;
-            vj = take ? j : vj;
-#endif
         }
     }
     // largest distance over the live slots
