@@ -218,6 +218,21 @@ def load_traffic():
     return json.loads(files[-1].read_text()) if files else {}
 
 
+def load_k4_issue():
+    """Issue-slot roofline of K4 from the newest committed ncu capture summary
+    (profiles/*_k4_roofline.json), or None."""
+    files = sorted((ROOT / "profiles").glob("*_k4_roofline.json"))
+    if not files:
+        return None
+    d = json.loads(files[-1].read_text())
+    return {"bound": "issue", "issue_active_frac": d["issue_active_frac"],
+            "warp_inst_per_expansion": d["warp_inst_per_expansion"],
+            "lts_bytes_per_s": d["lts_bytes_per_s"],
+            "lts_sector_frac_of_peak": d["lts_sector_frac_of_peak"],
+            "l2_hit_rate": d["l2_hit_rate"], "warps_active": d["warps_active"],
+            "source": files[-1].name}
+
+
 def query_benchmark(torch, g, provider, data, queries, reps=3):
     """§8(f) row 1: search_batch over the built graph (K2 query tables + K8),
     device-resident queries, ef 64, k 10; recall@10 against GPU brute force."""
@@ -441,7 +456,10 @@ def config_leg(cfg, torch, peak, tf32_peak, steps=2, warmup=3, cpu_seconds=0.0):
                         "traffic": None, "evals_per_s": evals / (prof["ms_search"] * 1e-3),
                         "bytes_basis": "SURVEY 8(d): 16 x kernel_calls x (m + 4) B + 4 B "
                                        "per block",
-                        "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}}
+                        "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9),
+                # what actually bounds K4: issue slots and L2
+                # latency, not HBM — from the committed ncu capture
+                "issue_roofline": load_k4_issue()}}
     if split:
         leg["timed"] = (f"project + encode + insert vectors {split}..{n} in batches of "
                         f"{builder.build_options(params).batch_max} onto the existing "
@@ -619,7 +637,10 @@ def main():
                 "touched_frac": touched / (prof["ms_search"] * 1e-3) / 1e9 / peak,
                 "traffic_basis": "per build: ncu DRAM bytes per inserted vector of one captured "
                                  "launch x n (profiles/*_traffic.json)",
-                "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9)}
+                "kernel_share": prof["ms_search"] / max(sum(kernel_ms.values()), 1e-9),
+                # what actually bounds K4: issue slots and L2
+                # latency, not HBM — from the committed ncu capture
+                "issue_roofline": load_k4_issue()}
 
     out = {"metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
