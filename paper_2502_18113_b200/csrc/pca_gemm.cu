@@ -62,7 +62,6 @@ constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row = one stage'
 constexpr int kConvWarps = 4, kEpiWarps = 8;
 constexpr int kConvThreads = 32 * kConvWarps;
 constexpr int kThreads = 32 * (2 + kConvWarps + kEpiWarps);
-constexpr int kStages = 2;
 constexpr int kConvWarp0 = 2, kEpiWarp0 = kConvWarp0 + kConvWarps;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -171,23 +170,36 @@ struct Tile {
     static constexpr int op_bytes = BM * BK * 4;  // 16 KB per hi / lo tile of 128 rows
 };
 
-// Shared-memory carve-up of one stage.  COV: rawA, rawB, Ahi, Alo, Bhi, Blo;
-// PROJ: rawA, Ahi, Alo, Bhi, Blo (B tiles BN rows).
+// Shared memory: three rings with their own depths, so the TMA loads run
+// ahead of the conversion and of the MMAs instead of waiting for a whole
+// stage to retire:
+//   raw ring  (RS stages, freed by the converters once read): raw X tiles
+//             (COV: the A and the B column blocks);
+//   B ring    (BS stages, freed by the MMA commit; projection only): the
+//             pre-split basis tiles hi / lo, TMA'd straight into UMMA layout;
+//   op ring   (2 stages, freed by the MMA commit): the converted hi / lo
+//             tiles (COV: A and B).
 template <bool COV, int BN, typename T>
 struct Layout {
     static constexpr int raw = Tile<T>::raw_bytes;
     static constexpr int raw_pad = (raw + 1023) / 1024 * 1024;
     static constexpr int a_op = Tile<T>::op_bytes;
     static constexpr int b_op = BN * BK * 4;
-    static constexpr int stage = raw_pad * (COV ? 2 : 1) + 2 * a_op + 2 * b_op;
-    static constexpr int off_rawA = 0;
-    static constexpr int off_rawB = raw_pad;  // COV only
-    static constexpr int off_ahi = raw_pad * (COV ? 2 : 1);
-    static constexpr int off_alo = off_ahi + a_op;
-    static constexpr int off_bhi = off_alo + a_op;
-    static constexpr int off_blo = off_bhi + b_op;
-    static constexpr int bars = kStages * stage;  // barrier block after the stages
-    static constexpr int total = bars + 256 + 1024;  // + barriers + alignment slack
+    static constexpr int RS = COV ? (sizeof(T) == 4 ? 2 : 3) : (sizeof(T) == 4 ? 3 : 4);
+    static constexpr int BS = COV ? 0 : 3;
+    static constexpr int OS = 2;
+    static constexpr int raw_stage = raw_pad * (COV ? 2 : 1);
+    static constexpr int b_stage = 2 * b_op;                      // hi, lo
+    static constexpr int op_stage = 2 * a_op + (COV ? 2 * b_op : 0);  // A hi, lo (+ B hi, lo)
+    static constexpr int off_raw = 0;
+    static constexpr int off_b = off_raw + RS * raw_stage;
+    static constexpr int off_op = off_b + BS * b_stage;
+    static constexpr int bars = off_op + OS * op_stage;  // barrier block after the rings
+    static constexpr int total = bars + 512 + 1024;      // + barriers + alignment slack
+    static_assert(total <= 227 * 1024, "shared memory");
+    // raw stage: rawA at 0, rawB at raw_pad; op stage: Ahi, Alo, Bhi, Blo
+    static constexpr int off_ahi = 0, off_alo = a_op, off_bhi = 2 * a_op,
+                         off_blo = 2 * a_op + b_op;
 };
 
 struct Params {
@@ -231,10 +243,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem =
         reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::bars);
-    uint64_t *conv = full + kStages;
-    uint64_t *empty = conv + kStages;
-    uint64_t *tfull = empty + kStages;
+    uint64_t *raw_full = reinterpret_cast<uint64_t *>(smem + L::bars);
+    uint64_t *raw_empty = raw_full + L::RS;
+    uint64_t *b_full = raw_empty + L::RS;
+    uint64_t *b_empty = b_full + 4;
+    uint64_t *op_full = b_empty + 4;
+    uint64_t *op_empty = op_full + L::OS;
+    uint64_t *tfull = op_empty + L::OS;
     uint64_t *tempty = tfull + 2;
     uint64_t *sfull = tempty + 2;
     uint64_t *sempty = sfull + 2;
@@ -247,10 +262,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(4 * BN <= 512, "TMEM holds 512 fp32 columns");
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(conv + s, kConvThreads);
-            mbar_init(empty + s, 1);
+        for (int s = 0; s < L::RS; ++s) {
+            mbar_init(raw_full + s, 1);
+            mbar_init(raw_empty + s, kConvThreads);
+        }
+        for (int s = 0; s < L::BS; ++s) {
+            mbar_init(b_full + s, 1);
+            mbar_init(b_empty + s, 1);
+        }
+        for (int s = 0; s < L::OS; ++s) {
+            mbar_init(op_full + s, kConvThreads);
+            mbar_init(op_empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
@@ -273,11 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer: raw tiles run up to RS stages ahead of the
+        // converters, basis tiles up to BS stages ahead of the MMAs =====
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapX)));
-            int s = 0;
-            uint32_t ph = 0;
+            int rs = 0, bs = 0;
+            uint32_t rph = 0, bph = 0;
             for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
                 int k0, k1, m0, n0;
                 bool diag = false;
@@ -295,23 +318,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     k1 = p.nk;
                 }
                 for (int kb = k0; kb < k1; ++kb) {
-                    mbar_wait(empty + s, ph ^ 1);
-                    uint8_t *st = smem + s * L::stage;
+                    mbar_wait(raw_empty + rs, rph ^ 1);
+                    uint8_t *rst = smem + L::off_raw + rs * L::raw_stage;
                     if constexpr (COV) {
                         // X[k rows, m / n column blocks]: box {BM cols, BK rows}
-                        const uint32_t bytes = (diag ? 1 : 2) * L::raw;
-                        mbar_expect_tx(full + s, bytes);
-                        tma_2d(st + L::off_rawA, &mapX, m0, kb * BK, full + s);
-                        if (!diag) tma_2d(st + L::off_rawB, &mapX, n0, kb * BK, full + s);
+                        mbar_expect_tx(raw_full + rs, (diag ? 1 : 2) * L::raw);
+                        tma_2d(rst, &mapX, m0, kb * BK, raw_full + rs);
+                        if (!diag) tma_2d(rst + L::raw_pad, &mapX, n0, kb * BK, raw_full + rs);
                     } else {
-                        mbar_expect_tx(full + s, L::raw + 2 * L::b_op);
-                        tma_2d(st + L::off_rawA, &mapX, kb * BK, m0, full + s);
-                        tma_2d(st + L::off_bhi, &mapBhi, kb * BK, n0, full + s);
-                        tma_2d(st + L::off_blo, &mapBlo, kb * BK, n0, full + s);
+                        mbar_expect_tx(raw_full + rs, L::raw);
+                        tma_2d(rst, &mapX, kb * BK, m0, raw_full + rs);
                     }
-                    if (++s == kStages) {
-                        s = 0;
-                        ph ^= 1;
+                    if (++rs == L::RS) {
+                        rs = 0;
+                        rph ^= 1;
+                    }
+                    if constexpr (!COV) {
+                        mbar_wait(b_empty + bs, bph ^ 1);
+                        uint8_t *bst = smem + L::off_b + bs * L::b_stage;
+                        mbar_expect_tx(b_full + bs, L::b_stage);
+                        tma_2d(bst, &mapBhi, kb * BK, n0, b_full + bs);
+                        tma_2d(bst + L::b_op, &mapBlo, kb * BK, n0, b_full + bs);
+                        if (++bs == L::BS) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
                     }
                 }
             }
@@ -320,8 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== MMA issuer: every stage into a fresh accumulator pair =====
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(BN);
-            int s = 0;
-            uint32_t ph = 0;
+            int s = 0, bs = 0;  // op ring, B ring
+            uint32_t ph = 0, bph = 0;
             uint32_t fl = 0;  // stages flushed so far (hi*hi accumulator = fl & 1)
             uint32_t it = 0;  // tiles so far (cross-term accumulator = it & 1)
             for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x, ++it) {
@@ -342,14 +373,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = k0; kb < k1; ++kb, ++fl) {
                     const uint32_t acc = fl & 1u;
                     mbar_wait(tempty + acc, ((fl >> 1) & 1u) ^ 1u);
-                    mbar_wait(full + s, ph);
-                    mbar_wait(conv + s, ph);
+                    mbar_wait(op_full + s, ph);
+                    if constexpr (!COV) mbar_wait(b_full + bs, bph);
                     tc_fence_after();
                     const uint32_t d_big = tmem_base + acc * BN;
-                    uint8_t *st = smem + s * L::stage;
-                    const uint32_t ahi = smem_u32(st + L::off_ahi), alo = smem_u32(st + L::off_alo);
-                    const uint32_t bhi = COV && diag ? ahi : smem_u32(st + L::off_bhi);
-                    const uint32_t blo = COV && diag ? alo : smem_u32(st + L::off_blo);
+                    uint8_t *ost = smem + L::off_op + s * L::op_stage;
+                    const uint32_t ahi = smem_u32(ost + L::off_ahi), alo = smem_u32(ost + L::off_alo);
+                    uint32_t bhi, blo;
+                    if constexpr (COV) {
+                        bhi = diag ? ahi : smem_u32(ost + L::off_bhi);
+                        blo = diag ? alo : smem_u32(ost + L::off_blo);
+                    } else {
+                        uint8_t *bst = smem + L::off_b + bs * L::b_stage;
+                        bhi = smem_u32(bst);
+                        blo = smem_u32(bst + L::b_op);
+                    }
 #pragma unroll
                     for (int k = 0; k < BK / 8; ++k) {
                         const uint32_t o = (uint32_t)k * 32u;  // 8 tf32 = 32 bytes along K
@@ -359,9 +397,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mma_tf32(d_small, sdesc(alo + o), sdesc(bhi + o), idesc, smore);
                         mma_tf32(d_small, sdesc(ahi + o), sdesc(blo + o), idesc, 1u);
                     }
-                    tc_commit(empty + s);       // the stage's smem is free once these retire
-                    tc_commit(tfull + acc);     // and its hi*hi sums are ready to drain
-                    if (++s == kStages) {
+                    tc_commit(op_empty + s);  // the converted tiles are free once these retire
+                    if constexpr (!COV) {
+                        tc_commit(b_empty + bs);  // and the basis tiles
+                        if (++bs == L::BS) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                    tc_commit(tfull + acc);  // the hi*hi sums are ready to drain
+                    if (++s == L::OS) {
                         s = 0;
                         ph ^= 1;
                     }
@@ -372,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= kConvWarp0 && warp < kEpiWarp0) {
         // ===== converters: raw -> centred -> hi / lo, K-major SW128 =====
         const int t = threadIdx.x - kConvWarp0 * 32;  // 0 .. kConvThreads - 1
-        int s = 0;
-        uint32_t ph = 0;
+        int rs = 0, s = 0;  // raw ring, op ring
+        uint32_t rph = 0, ph = 0;
         for (int64_t w = blockIdx.x; w < p.nwork; w += gridDim.x) {
             int k0, k1, m0 = 0, n0 = 0;
             bool diag = false;
@@ -389,8 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 k1 = p.nk;
             }
             for (int kb = k0; kb < k1; ++kb) {
-                mbar_wait(full + s, ph);
-                uint8_t *st = smem + s * L::stage;
+                mbar_wait(raw_full + rs, rph);
+                mbar_wait(op_empty + s, ph ^ 1);
+                const uint8_t *rst = smem + L::off_raw + rs * L::raw_stage;
+                uint8_t *st = smem + L::off_op + s * L::op_stage;
                 if constexpr (COV) {
                     // thread t owns columns t, t + kConvThreads, ... of the
                     // block: rows k of the raw tile become the K of operand
@@ -400,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int col = (op ? n0 : m0) + tc;
                         const bool cin = col < p.D;
                         const float mu = cin ? __ldg(p.mean + col) : 0.f;
-                        const T *raw = reinterpret_cast<const T *>(st + (op ? L::off_rawB : L::off_rawA));
+                        const T *raw = reinterpret_cast<const T *>(rst + (op ? L::raw_pad : 0));
                         uint8_t *hi = st + (op ? L::off_bhi : L::off_ahi);
                         uint8_t *lo = st + (op ? L::off_blo : L::off_alo);
                         const int64_t kr0 = (int64_t)kb * BK;
@@ -418,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
-                    const T *raw = reinterpret_cast<const T *>(st + L::off_rawA);
+                    const T *raw = reinterpret_cast<const T *>(rst);
                     uint8_t *hi = st + L::off_ahi;
                     uint8_t *lo = st + L::off_alo;
                     constexpr int per16 = 16 / (int)sizeof(T);  // elements per 16-byte chunk
@@ -450,8 +497,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(conv + s);
-                if (++s == kStages) {
+                mbar_arrive(raw_empty + rs);  // the raw tile is consumed
+                mbar_arrive(op_full + s);     // the converted tiles are ready
+                if (++rs == L::RS) {
+                    rs = 0;
+                    rph ^= 1;
+                }
+                if (++s == L::OS) {
                     s = 0;
                     ph ^= 1;
                 }
