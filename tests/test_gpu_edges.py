@@ -145,3 +145,50 @@ def test_late_projected_rows(core, model, early, monkeypatch):
     assert res["counters"] == ref[0]["counters"]
     assert np.array_equal(base, ref[3]) and np.array_equal(upper, ref[4])
     _check_oracle(p2, levels, uoff, base, upper, res, **sched)
+
+
+def test_resumed_build_equals_one_pass(cuda):
+    """fa_build_opts.start / end (the dynamic-rebuild workload): inserting
+    [0, A) and then resuming [A, n) gives the same graph as one pass, when A
+    is a batch boundary of the one-pass schedule."""
+    from oracle import native
+    from paper_2502_18113_b200 import builder, flash, graph
+    import golden_inputs as gi
+
+    data, _ = gi.graph_data()
+    n = data.shape[0]
+    model = flash.flash_train(data, 32, 16, seed=0, kmeans_iters=4)
+    params = graph.BuildParams(C=48, R=8, seed=0)
+    levels = graph.assign_layers(n, 0, params.R)
+    sched = dict(batch_max=128, batch_frac=0.2, seq_prefix=16, batch_min=0)
+    starts, _ = native.schedule(levels, **sched)
+    A = int(starts[len(starts) // 2])
+
+    def rows(g):
+        import torch
+        from paper_2502_18113_b200 import _lib
+
+        lib = _lib.load()
+        r0 = torch.empty((n, 1 + 2 * params.R), dtype=torch.int32, device="cuda")
+        rU = torch.empty((max(g.n_upper_rows, 1), 1 + params.R), dtype=torch.int32,
+                         device="cuda")
+        _lib.check(lib.fa_index_export_rows(g.handle, r0.data_ptr(), rU.data_ptr(), None))
+        return r0.cpu().numpy(), rU.cpu().numpy()
+
+    out = []
+    for split in (None, A):
+        prov = flash.FlashProvider(model)
+        prov.attach(data)
+        g = graph.GraphIndex(n, data.shape[1], params, "flash", model.m, levels)
+        if split is None:
+            builder.build_device(g, prov, params, **sched)
+        else:
+            builder.build_device(g, prov, params, end=split, **sched)
+            builder.build_device(g, prov, params, start=split, **sched)
+        out.append((rows(g), g.entry_point, g.max_layer))
+        g.close()
+    (a0, aU), ea, ma = out[0]
+    (b0, bU), eb, mb = out[1]
+    assert (ea, ma) == (eb, mb)
+    assert np.array_equal(a0, b0)
+    assert np.array_equal(aU, bU)
