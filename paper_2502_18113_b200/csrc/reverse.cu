@@ -254,6 +254,11 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
                     p += __popc(__ballot_sync(0xffffffffu, kj[c] < kx));
                 }
                 n_sym += cap + 1 + p;
+                // x after every member (p = cap; e.g. a saturated d(y, x) = 255
+                // with x newer than all members): the members alone fill the
+                // row before x is reached, so the prune leaves it unchanged
+                // (and still consistent) — whether or not x is dominated
+                if (p >= cap) continue;
                 // domination of x, one 32-member chunk at a time: the first
                 // dominating member settles it
                 bool xkept = true;
@@ -479,6 +484,7 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
                     p += __popc(__ballot_sync(0xffffffffu, lt));
                 }
                 n_sym += cap + 1 + p;
+                if (p >= cap) continue;  // x after every member: the row is unchanged
                 // domination of x by a closer member, four at a time
                 bool xkept = true;
                 for (int b0 = 0; b0 < p; b0 += 4) {
