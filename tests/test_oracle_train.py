@@ -61,3 +61,18 @@ def test_layout_rows_roundtrip_reference():
             assert np.array_equal(a[r], b[r])
             assert np.array_equal(layout.row_codes(a, r, cap, m), codes)
             assert np.array_equal(layout.row_ids(a, r, cap), ids)
+
+
+def test_workloads_prefix_stable():
+    """baseline_config draws the same first rows (and queries) for every n, so
+    a CPU prefix sample is exactly the start of the GPU arm's workload."""
+    from paper_2502_18113_b200 import dataset
+
+    for cfg in (1, 2, 3, 4, 5):
+        a, qa = dataset.baseline_config(cfg, n=700, nq=20)
+        b, qb = dataset.baseline_config(cfg, n=1500, nq=35)
+        assert np.array_equal(a, b[:700]), cfg
+        assert np.array_equal(qa, qb[:20]), cfg
+        assert a.dtype == np.float32 and a.shape[1] == dataset.CONFIGS[cfg]["dim"]
+    x5, _ = dataset.baseline_config(5, n=50, nq=0)
+    assert np.array_equal(dataset._round_bf16(x5), x5)  # config 5 rows are bf16 values
