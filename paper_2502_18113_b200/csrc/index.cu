@@ -113,7 +113,8 @@ static int search_warps_for(int per_warp_bytes) {
     return w;
 }
 
-static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t smem, int W) {
+static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t smem, int W,
+                       cudaStream_t st) {
     int dev = 0, nsm = 0, per_sm = 0;
     FA_CUDA(cudaGetDevice(&dev));
     FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -125,7 +126,7 @@ static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t sme
     // grow to cover both this launch and earlier ones
     const int ns = std::max(slots, ix->gvis ? ix->g.gvis_nslots : 0);
     const int lg = std::max(l2, ix->gvis ? ix->g.gvis_log2 : 0);
-    FA_CUDA(cudaDeviceSynchronize());  // no search may still hold the old pool
+    if (ix->gvis) FA_CUDA(cudaDeviceSynchronize());  // no search may still hold the old pool
     pool_free(ix->gvis);
     pool_free(ix->gvis_epoch);
     pool_free(ix->gvis_owner);
@@ -136,9 +137,10 @@ static int ensure_gvis(fa_index *ix, const void *kernel, int threads, size_t sme
     FA_TRY(dev_alloc((void **)&ix->gvis, tab));
     FA_TRY(dev_alloc((void **)&ix->gvis_epoch, (size_t)ns * sizeof(uint32_t)));
     FA_TRY(dev_alloc((void **)&ix->gvis_owner, (size_t)ns * sizeof(uint32_t)));
-    FA_CUDA(cudaMemset(ix->gvis, 0, tab));
-    FA_CUDA(cudaMemset(ix->gvis_epoch, 0, (size_t)ns * sizeof(uint32_t)));
-    FA_CUDA(cudaMemset(ix->gvis_owner, 0, (size_t)ns * sizeof(uint32_t)));
+    // on the launch's stream: ordered before the searches that use it
+    FA_CUDA(cudaMemsetAsync(ix->gvis, 0, tab, st));
+    FA_CUDA(cudaMemsetAsync(ix->gvis_epoch, 0, (size_t)ns * sizeof(uint32_t), st));
+    FA_CUDA(cudaMemsetAsync(ix->gvis_owner, 0, (size_t)ns * sizeof(uint32_t), st));
     ix->g.gvis = ix->gvis;
     ix->g.gvis_epoch = ix->gvis_epoch;
     ix->g.gvis_owner = ix->gvis_owner;
@@ -608,7 +610,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                      cudaFuncAttributePreferredSharedMemoryCarveout,
                                      std::min(100, std::max(0, pct))));
     }
-    FA_TRY(ensure_gvis(ix, (const void *)search_fn, bw * 32, smem_search, C));
+    FA_TRY(ensure_gvis(ix, (const void *)search_fn, bw * 32, smem_search, C, st));
     gb.gvis = g.gvis;
     gb.gvis_epoch = g.gvis_epoch;
     gb.gvis_owner = g.gvis_owner;
@@ -882,7 +884,7 @@ extern "C" int fa_index_search(fa_index *ix, const float *queries, const float *
     const QuerySearchFn qfn = query_search_variant(ef, exact, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)qfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    FA_TRY(ensure_gvis(ix, (const void *)qfn, qw * 32, smem, ef));
+    FA_TRY(ensure_gvis(ix, (const void *)qfn, qw * 32, smem, ef, st));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
@@ -946,7 +948,7 @@ extern "C" int fa_index_search_layer(fa_index *ix, const float *qproj, int nq,
     const LayerSearchFn lfn = layer_search_variant(width, exact, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)lfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    FA_TRY(ensure_gvis(ix, (const void *)lfn, qw * 32, smem, width));
+    FA_TRY(ensure_gvis(ix, (const void *)lfn, qw * 32, smem, width, st));
     uint8_t *adt_q = nullptr;
     if (!exact) FA_TRY(run_query_encode(ix, qproj, nq, &adt_q, st));
     unsigned long long *ctr = nullptr;
