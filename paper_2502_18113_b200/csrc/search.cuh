@@ -257,6 +257,7 @@ __device__ __forceinline__ uint4 lds128_volatile(const uint4 *p) {
 // by the slot's previous owner).
 // Narrow entries are 32-bit (epoch << 24 | id), wide ones 64-bit
 // (epoch << 32 | id).
+constexpr int kGlobalMaxProbe = 256;
 template <bool W>
 static __device__ __noinline__ int global_visit(uint32_t *G32, int glog2, uint32_t epoch, int id) {
     using E = typename std::conditional<W, unsigned long long, uint32_t>::type;
@@ -266,7 +267,9 @@ static __device__ __noinline__ int global_visit(uint32_t *G32, int glog2, uint32
     const E gk = ((E)epoch << kEpochShift) | (E)((uint32_t)id & (W ? 0xffffffffu : 0xFFFFFFu));
     const uint32_t gmask = (1u << glog2) - 1u;
     uint32_t p = (key * 2654435761u) >> (32 - glog2);
-    while (true) {
+    // a probe run this long only happens once the table is nearly full: report
+    // overflow (FA_EOVERFLOW upstream) instead of probing on
+    for (int probe = 0; probe < kGlobalMaxProbe;) {
         const E v = __ldcg(G + p);
         if (v == gk) return 0;
         if ((uint32_t)(v >> kEpochShift) != epoch) {
@@ -276,7 +279,9 @@ static __device__ __noinline__ int global_visit(uint32_t *G32, int glog2, uint32
             continue;
         }
         p = (p + 1u) & gmask;
+        ++probe;
     }
+    return 3;
 }
 
 // A warp's claimed global-tier table: claimed once per warp per launch (the
@@ -336,7 +341,6 @@ struct VisitedSet {
     uint32_t *G;       // global tier (the warp's claimed table)
     int glog2;
     uint32_t epoch;
-    int gcount, glimit;
 
     // a new search: clear the shared tier, advance the global tier's epoch
     // (entries of older epochs count as empty; the table is wiped once every
@@ -347,10 +351,8 @@ struct VisitedSet {
         nslots = W ? min(4, vis_bucket_slots(hlog2)) : vis_bucket_slots(hlog2);
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int i = lane; i < (1 << kb); i += 32) B[i] = z;
-        gcount = 0;
         glog2 = g.gvis_log2;
         G = gs.G;
-        glimit = G ? (1 << glog2) * 3 / 4 : (1 << 30);  // no tier: visit() reports 3
         if (G) {
             uint32_t e = gs.epoch + 1u;
             if (e > 255u) {  // wrap: clear this slot's table once
@@ -994,7 +996,6 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) return false;
         // visited filter over the rows (pop order, slot order), compacted
         bool over = false;
         int nf = 0;
@@ -1015,7 +1016,6 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                 if (fr) fresh[nf + __popc(bf & lt)] = x;
                 nf += __popc(bf);
                 nlive += __popc(bl);
-                vs.gcount += __popc(__ballot_sync(FULL, rr == 2));
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
@@ -1156,7 +1156,6 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
-        if (vs.gcount + npop * cap > vs.glimit) return false;
         bool over = false;
         // visited filter over the rows (pop order, slot order), compacted
         int nf = 0;
@@ -1177,7 +1176,6 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
                 if (fr) fresh[nf + __popc(bf & ((1u << lane) - 1u))] = x;
                 nf += __popc(bf);
                 nlive += __popc(bl);
-                vs.gcount += __popc(__ballot_sync(0xffffffffu, rr == 2));
             }
             cnt.kcalls += (nlive + 15) >> 4;
         }
