@@ -759,6 +759,11 @@ extern "C" int fa_pca_cov_dev(const void *x, int x_dtype, int64_t n, int D, cons
     // K splits: enough work items for every SM, at least 16 k-blocks each
     int ns = (int)std::max<int64_t>(1, (2 * num_sms() + ntri - 1) / ntri);
     ns = std::min(ns, std::max(1, p.nk / 16));
+    // every split must own at least one k-block: an empty split issues no MMA,
+    // and its epilogue would drain whatever an earlier kernel left in TMEM
+    // into the partial sums (cov_krange gives split sp blocks [sp * per, ...))
+    const int per = (p.nk + ns - 1) / ns;
+    ns = (p.nk + per - 1) / per;
     p.nsplit = ns;
     p.nwork = ntri * ns;
     float *part = nullptr;

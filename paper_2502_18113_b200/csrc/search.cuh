@@ -961,10 +961,10 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             if (anyT2 || anyQ2) {
                 const K kQ2 = anyQ2 ? P::key(wd, (uint32_t)TQ[tq_h]) : K(0);
                 pre_v = to.back(P::tie(anyT2 && (!anyQ2 || m2 < kQ2) ? m2 : kQ2));
-                load_row(row_ids(g, layer, pre_v), cap, lane, pre);
             } else {
                 pre_v = -1;
             }
+            // (its row is loaded below, once the visited filter has consumed u[0])
         } else {
 #pragma unroll
             for (int r = 0; r < EM; ++r) {
@@ -1023,6 +1023,12 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         cnt.dist += nf;
         __syncwarp();
         phase_mark(cnt, 1, tph);
+        // the predicted next pop's row: issued here, right before the code
+        // gather, and consumed at the next step.  (ptxas gives it the
+        // scoreboard of the miss path's row load; issued before the visited
+        // filter, the filter's wait on u[0] waited for it as well, and a
+        // full load latency per step: 230.7 -> 223.3 ms per config-2 build)
+        if (EM == 1 && pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
         if (nf == 0) continue;
         P::dists(g, qc, fresh, nf, fdist, lane);
         phase_mark(cnt, 2, tph);

@@ -27,6 +27,10 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--builds", type=int, default=1)
+    ap.add_argument("--hash", action="store_true",
+                    help="sha256 of the exported blocks after each build (determinism A/B)")
+    ap.add_argument("--profile", action="store_true",
+                    help="per-kernel device times (every build after the first)")
     args = ap.parse_args()
     c = dataset.CONFIGS[args.config]
     n = args.n or c["n"]
@@ -42,16 +46,25 @@ def main():
                          graph.assign_layers(n, 0, c["M"]))
     g.create_device(prov)
     lib = _lib.load()
-    for _ in range(args.builds):
+    for i in range(args.builds):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         prov.reproject()
         _lib.check(lib.fa_index_set_codes(g.handle, prov.dev["codes"].data_ptr(),
                                           prov.dev["codes"].shape[1], None))
-        ctr = builder.build_device(g, prov, params)
+        ctr = builder.build_device(g, prov, params, profile=int(args.profile and i > 0))
         torch.cuda.synchronize()
+        ks = "".join(f", {k} {ctr[k]:.2f}" for k in ("ms_encode", "ms_search", "ms_sort", "ms_reverse")
+                     if k in ctr)
         print(f"config {args.config} n {n}: {time.perf_counter() - t0:.3f} s, "
-              f"{ctr['n_batches']} batches, {ctr['launches']} launches", flush=True)
+              f"{ctr['n_batches']} batches, {ctr['launches']} launches{ks}", flush=True)
+        if args.hash:
+            import hashlib
+
+            g.invalidate()
+            h = hashlib.sha256(g.base_blocks.tobytes())
+            h.update(g.upper_blocks.tobytes())
+            print("blocks sha256", h.hexdigest()[:16], flush=True)
 
 
 if __name__ == "__main__":

@@ -10,7 +10,9 @@ reference's numpy arithmetic (flashann/providers/pca.py:27-71).
   largest, every one of the 256 basis columns up to sign with
   1 - |cos| <= 1e-6, and pca_project_all of 64 rows within 1e-5 of the
   reference's own fp32 sgemm (sign-aligned);
-* pca_project (float64 single vectors) against numpy float64.
+* pca_project (float64 single vectors) against numpy float64;
+* the covariance's K splits at the real sample sizes (each owns a k-block;
+  bitwise stable after other tensor-core work left TMEM dirty).
 """
 
 import numpy as np
@@ -43,6 +45,36 @@ def test_covariance_gemm(cuda, n, D, bf16):
     assert np.abs(cov - ref).max() / np.abs(ref).max() <= 2e-6
     assert (np.abs(cov - ref) / scale).max() <= 1e-5
     assert np.array_equal(cov, cov.T)
+
+
+@pytest.mark.parametrize("n", [20000, 100000])
+def test_covariance_after_other_tmem_work(cuda, n):
+    """Sample sizes whose k-block count does not divide evenly over the
+    K splits (20,000 rows = config 1's whole sample, 100,000 = the training
+    sample of configs 2-5, D = 128: one output tile, up to 2 x 148 splits).
+    Every split must own a k-block: an empty one would drain whatever an
+    earlier kernel left in TMEM into the sum.  A projection with large values
+    runs first, so such leftovers would be large; the covariance must match
+    float64 numpy and be bitwise stable across calls."""
+    torch = cuda
+    from paper_2502_18113_b200 import pca
+
+    rng = np.random.default_rng(n)
+    big = (rng.normal(size=(4096, 128)) * 1e4).astype(np.float32)
+    q, _ = np.linalg.qr(rng.normal(size=(128, 128)))
+    junk = pca.PCAModel(mean=np.zeros(128), basis=q, eigvals=np.ones(128), d=128)
+    x = rng.normal(size=(n, 128)).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    mean32 = x.astype(np.float64).mean(0).astype(np.float32)
+    mt = torch.from_numpy(mean32).cuda()
+    covs = []
+    for _ in range(3):
+        pca.pca_project_all(junk, big)  # leaves large accumulators in TMEM
+        covs.append(pca.covariance_dev(xt, mt).cpu().numpy())
+    xc = _centred(x, mean32).astype(np.float64)
+    ref = xc.T @ xc / n
+    assert np.abs(covs[0] - ref).max() / np.abs(ref).max() <= 2e-6
+    assert all(np.array_equal(c, covs[0]) for c in covs[1:])
 
 
 @pytest.mark.parametrize("n,D,d", [(1000, 128, 128), (1500, 960, 256), (700, 768, 300),
