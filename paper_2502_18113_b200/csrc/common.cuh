@@ -138,6 +138,7 @@ __device__ __forceinline__ float l2_tree(int d, Load ld) {
         float a[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = 0.f;
+#pragma unroll
         for (; i + 8 <= d; i += 8) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -162,6 +163,7 @@ __device__ __forceinline__ float l2_tree(int d, Load ld) {
     } else {
         s = 0.f;
     }
+#pragma unroll
     for (; i < d; ++i) {
         float e = ld(i);
         s = __fmaf_rn(e, e, s);

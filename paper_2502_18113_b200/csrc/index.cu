@@ -44,11 +44,6 @@ struct fa_index {
     int64_t n_inserted = 0;  // vertices [0, n_inserted) are in the graph
     int64_t entry = -1;
     int max_layer = -1;
-    // the build's side stream: query tables (K2) of batch k + 1 are encoded
-    // there while batch k searches; enc[k & 1] = tables of batch k ready,
-    // used[k & 1] = batch k's search has read its buffer
-    cudaStream_t side = nullptr;
-    cudaEvent_t enc[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr}, fence = nullptr;
 };
 
 namespace fa {
@@ -396,9 +391,6 @@ extern "C" int fa_index_destroy(fa_index *ix) {
                     (void *)ix->distU, (void *)ix->upper_owner, (void *)ix->gvis,
                     (void *)ix->gvis_epoch, (void *)ix->gvis_owner})
         pool_free(p);
-    for (cudaEvent_t e : {ix->enc[0], ix->enc[1], ix->used[0], ix->used[1], ix->fence})
-        if (e) cudaEventDestroy(e);
-    if (ix->side) cudaStreamDestroy(ix->side);
     delete ix;
     return FA_OK;
 }
@@ -626,11 +618,6 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     gb.gvis_nslots = g.gvis_nslots;
     gb.gvis_words = g.gvis_words;
 
-    if (!exact && !ix->side) {
-        FA_CUDA(cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking));
-        for (cudaEvent_t *e : {&ix->enc[0], &ix->enc[1], &ix->used[0], &ix->used[1], &ix->fence})
-            FA_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    }
     uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
@@ -640,10 +627,6 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // scratch is stream-ordered (cudaMallocAsync from the device's pool, kept
     // cached across builds): no allocation or free synchronises the device
     auto cleanup = [&]() {
-        if (ix->side) {  // the side stream's encodes may still use adt_batch
-            cudaEventRecord(ix->fence, ix->side);
-            cudaStreamWaitEvent(st, ix->fence, 0);
-        }
         for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
                         (void *)req_off_d, (void *)order_d, (void *)err, (void *)heads,
                         (void *)nheads, (void *)next_seg, (void *)sdtT, (void *)rev_sel,
@@ -660,8 +643,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     };
     keep_pool();  // scratch stays mapped in the pool between builds
     const int64_t nrows = g.n + g.nU;  // layer-0 rows, then the upper rows
-    const size_t adt_bytes = (size_t)maxB * g.mpad * 16;  // one batch's query tables
-    if ((rc = dev_alloc((void **)&adt_batch, 2 * adt_bytes)) ||
+    if ((rc = dev_alloc((void **)&adt_batch, (size_t)maxB * g.mpad * 16)) ||
         (rc = dev_alloc((void **)&req, sizeof(unsigned long long) * std::max<int64_t>(maxreq, 1))) ||
         (rc = dev_alloc((void **)&req_sorted, sizeof(unsigned long long) * (std::max<int64_t>(maxreq, 1) + 1))) ||
         (rc = dev_alloc((void **)&rowcnt, sizeof(int32_t) * nrows)) ||
@@ -729,40 +711,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                           t_host0).count());
     int64_t launches = r0 == 0 ? 3 : 1;  // the two row resets of reset_graph, the SDT transpose
-    // K2 runs one batch ahead on the side stream into the other half of
-    // adt_batch: batch k + 1's tables are encoded while batch k searches (its
-    // blocks fill the SMs the search's tail leaves idle).  Buffer k & 1 is
-    // reused by batch k + 2 once batch k's search has read it.
-    auto enqueue_tables = [&](size_t bj) -> int {
-        const Batch &b = batches[bj];
-        cudaStream_t s2 = ix->side;
-        if (bj >= 2) FA_CUDA(cudaStreamWaitEvent(s2, ix->used[bj & 1], 0));
-        if (ix->late_hook && ix->late_from >= 0 && (int64_t)b.start + b.size > ix->late_from) {
-            auto hook = std::move(ix->late_hook);
-            ix->late_hook = nullptr;
-            ix->late_from = -1;
-            FA_TRY(hook(s2));
-        }
-        FA_TRY(launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size,
-                                 ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs, g.m, ix->d.dmax,
-                                 ix->d.dist_min, ix->d.delta, nullptr, g.mpad,
-                                 adt_batch + (bj & 1) * adt_bytes, g.mpad, s2));
-        FA_CUDA(cudaEventRecord(ix->enc[bj & 1], s2));
-        return FA_OK;
-    };
-    if (!exact && !batches.empty()) {
-        // the side stream starts after everything enqueued on st so far
-        FA_BUILD_CUDA(cudaEventRecord(ix->fence, st));
-        FA_BUILD_CUDA(cudaStreamWaitEvent(ix->side, ix->fence, 0));
-        if ((rc = enqueue_tables(0))) {
-            cleanup();
-            return rc;
-        }
-    }
     for (size_t bi = 0; bi < batches.size(); ++bi) {
         const Batch &b = batches[bi];
-        if (exact && ix->late_hook && ix->late_from >= 0 &&
-            (int64_t)b.start + b.size > ix->late_from) {
+        if (ix->late_hook && ix->late_from >= 0 && (int64_t)b.start + b.size > ix->late_from) {
             auto hook = std::move(ix->late_hook);
             ix->late_hook = nullptr;
             ix->late_from = -1;
@@ -771,14 +722,17 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                 return rc;
             }
         }
-        if (!exact && bi + 1 < batches.size() && (rc = enqueue_tables(bi + 1))) {
-            cleanup();
-            return rc;
-        }
-        // (profiled: the encode interval is the time the search waits for
-        // its tables, i.e. the part of K2 the overlap does not hide)
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 0], st));
-        if (!exact) FA_BUILD_CUDA(cudaStreamWaitEvent(st, ix->enc[bi & 1], 0));
+        if (!exact) {
+            rc = launch_encode_adt(ix->d.proj + (size_t)b.start * ix->d.dproj, b.size,
+                                   ix->d.dproj, ix->d.cent, ix->d.dims, ix->d.offs, g.m,
+                                   ix->d.dmax, ix->d.dist_min, ix->d.delta, nullptr, g.mpad,
+                                   adt_batch, g.mpad, st);
+            if (rc) {
+                cleanup();
+                return rc;
+            }
+        }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
         {  // stable counting sort of the batch by level, descending
             int32_t *o = order_h + b.start;
@@ -804,11 +758,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 3 * sizeof(int), st));
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
         search_fn<<<grid, bw * 32, smem_search, st>>>(
-            gb, sdtT, adt_batch + (bi & 1) * adt_bytes, b.start, b.size, b.ep, b.ml, C, R, L,
-            req_off_d + b.start, order_d + b.start,
+            gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
+            order_d + b.start,
             req, ctr, err, opts->point_stats, nheads + 1);
         FA_BUILD_CUDA(cudaGetLastError());
-        if (!exact) FA_BUILD_CUDA(cudaEventRecord(ix->used[bi & 1], st));
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         // bucket the requests by row: segments for the touched rows, then
         // every request into its row's segment (no sort; reverse.cu)

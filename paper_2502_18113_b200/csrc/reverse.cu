@@ -221,17 +221,18 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
             }
             ++n_prune;
             const uint8_t *cx = g.codes + (size_t)x * g.mpad;
-            // Tdom[i][c] = sdt[i][c][x_i]: d(L_j, x) = sum_i Tdom[i][L_j,i] and
-            // d(y, x) = sum_i Tdom[i][y_i]
-            build_row_table(sdtT, g.m, g.mpad, cx, tdom, lane);
-            __syncwarp();
+            // d(y, x) = sum_i sdt[i][y_i][x_i], looked up directly (the SDT is
+            // L1-resident): most prunes end at the p = cap test below, which
+            // needs nothing else
             uint32_t dx;
             {
                 uint32_t acc = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int i = lane + 32 * k;
-                    if (i < g.m) acc += tdom[(i << 4) + ((cyl >> (8 * k)) & 0xffu)];
+                    if (i < g.m)
+                        acc += __ldg(sdt + (i << 8) + (((cyl >> (8 * k)) & 0xffu) << 4) +
+                                     __ldg(cx + i));
                 }
                 acc = __reduce_add_sync(0xffffffffu, acc);
                 dx = acc > 255u ? 255u : acc;
@@ -259,6 +260,11 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
                 // row before x is reached, so the prune leaves it unchanged
                 // (and still consistent) — whether or not x is dominated
                 if (p >= cap) continue;
+                // Tdom[i][c] = sdt[i][c][x_i]: d(L_j, x) = sum_i Tdom[i][L_j,i]
+                if (p > 0) {
+                    build_row_table(sdtT, g.m, g.mpad, cx, tdom, lane);
+                    __syncwarp();
+                }
                 // domination of x, one 32-member chunk at a time: the first
                 // dominating member settles it
                 bool xkept = true;

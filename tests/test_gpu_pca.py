@@ -60,7 +60,9 @@ def test_covariance_after_other_tmem_work(cuda, n):
     from paper_2502_18113_b200 import pca
 
     rng = np.random.default_rng(n)
-    big = (rng.normal(size=(4096, 128)) * 1e4).astype(np.float32)
+    # enough row tiles for a persistent CTA on every SM
+    g = torch.Generator(device="cuda").manual_seed(n)
+    big = torch.randn((300_000, 128), generator=g, device="cuda") * 1e4
     q, _ = np.linalg.qr(rng.normal(size=(128, 128)))
     junk = pca.PCAModel(mean=np.zeros(128), basis=q, eigvals=np.ones(128), d=128)
     x = rng.normal(size=(n, 128)).astype(np.float32)
@@ -69,7 +71,7 @@ def test_covariance_after_other_tmem_work(cuda, n):
     mt = torch.from_numpy(mean32).cuda()
     covs = []
     for _ in range(3):
-        pca.pca_project_all(junk, big)  # leaves large accumulators in TMEM
+        pca.pca_project_all_dev(junk, big)  # leaves large accumulators in TMEM
         covs.append(pca.covariance_dev(xt, mt).cpu().numpy())
     xc = _centred(x, mean32).astype(np.float64)
     ref = xc.T @ xc / n
