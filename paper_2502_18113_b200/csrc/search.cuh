@@ -70,6 +70,31 @@ __device__ __forceinline__ const int32_t *row_ids(const Graph &g, int layer, int
     if (layer == 0) return g.adj0 + (int64_t)v * g.cap0p;
     return g.adjU + (__ldg(g.uoff + v) + layer - 1) * g.capUp;
 }
+// Row addressing of one layer, set up once per layer search: base + index *
+// stride, the index the vertex itself on layer 0 and its upper-row offset
+// above (one predicated load); keeps the per-step address to a few
+// instructions instead of re-deriving both cases from the kernel parameters
+struct RowAddr {
+    const int32_t *base;
+    const int64_t *uoff;  // null on layer 0
+    int stride;
+    __device__ __forceinline__ RowAddr(const Graph &g, int layer) {
+        if (layer == 0) {
+            base = g.adj0;
+            uoff = nullptr;
+            stride = g.cap0p;
+        } else {
+            base = g.adjU + (int64_t)(layer - 1) * g.capUp;
+            uoff = g.uoff;
+            stride = g.capUp;
+        }
+    }
+    __device__ __forceinline__ const int32_t *operator()(int v) const {
+        // row indices and strides are below 2^31: one 32 x 32 -> 64 multiply
+        const uint32_t i = uoff ? (uint32_t)__ldg(uoff + v) : (uint32_t)v;
+        return base + (uint64_t)i * (uint32_t)stride;
+    }
+};
 __device__ __forceinline__ int layer_cap(const Graph &g, int layer) {
     return layer == 0 ? g.cap0 : g.capU;
 }
@@ -898,6 +923,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
                                                  const TieOrder &to, GSlot &gs, int lane) {
     constexpr unsigned FULL = 0xffffffffu;
     const int cap = layer_cap(g, layer);
+    const RowAddr ra(g, layer);
     using K = typename P::Key;
     K *Sa = reinterpret_cast<K *>(S);
     K *Sb = Sa + cand_capacity(g);
@@ -948,7 +974,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
 #pragma unroll
                 for (int k = 0; k < RC; ++k) u[0][k] = pre[k];
             } else {
-                load_row(row_ids(g, layer, pv[0]), cap, lane, u[0]);
+                load_row(ra(pv[0]), cap, lane, u[0]);
             }
             // predict the next pop assuming nothing new enters: the popped
             // lane offers its second smallest key
@@ -992,7 +1018,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
             // id rows of the popped vertices, all loads in flight together
 #pragma unroll
             for (int r = 0; r < EM; ++r)
-                if (r < npop) load_row(row_ids(g, layer, pv[r]), cap, lane, u[r]);
+                if (r < npop) load_row(ra(pv[r]), cap, lane, u[r]);
         }
         cnt.visited += npop;
         phase_mark(cnt, 0, tph);
@@ -1028,7 +1054,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
         // scoreboard of the miss path's row load; issued before the visited
         // filter, the filter's wait on u[0] waited for it as well, and a
         // full load latency per step: 230.7 -> 223.3 ms per config-2 build)
-        if (EM == 1 && pre_v >= 0) load_row(row_ids(g, layer, pre_v), cap, lane, pre);
+        if (EM == 1 && pre_v >= 0) load_row(ra(pre_v), cap, lane, pre);
         if (nf == 0) continue;
         P::dists(g, qc, fresh, nf, fdist, lane);
         phase_mark(cnt, 2, tph);
