@@ -56,6 +56,8 @@ def main():
         torch.cuda.synchronize()
         ks = "".join(f", {k} {ctr[k]:.2f}" for k in ("ms_encode", "ms_search", "ms_sort", "ms_reverse")
                      if k in ctr)
+        ks += "".join(f", {k} {ctr[k]}" for k in ("reverse_prunes", "reverse_full_prunes",
+                                                   "reverse_appends") if k in ctr and i == 0)
         print(f"config {args.config} n {n}: {time.perf_counter() - t0:.3f} s, "
               f"{ctr['n_batches']} batches, {ctr['launches']} launches{ks}", flush=True)
         if args.hash:
