@@ -77,7 +77,10 @@ __global__ void bucket_place_kernel(const int32_t *__restrict__ touched,
         base = __shfl_sync(0xffffffffu, base, 31);
         if (t < nt) {
             rowoff[row] = base + incl - c;
-            heads[t] = base + incl - c;
+            // the segment record: its length above its head (the row is
+            // touched[t]), so a reverse warp needs neither the keys nor a scan
+            // for the segment's end before it can fetch the row
+            heads[t] = ((int64_t)c << 32) | (int64_t)(base + incl - c);
         }
     }
 }
@@ -167,22 +170,12 @@ __global__ void __maxnreg__(FA_REV_MAXNREG) reverse_kernel(
         if (lane == 0) s = atomicAdd(next, 1);
         s = __shfl_sync(0xffffffffu, s, 0);
         if (s >= nseg) break;
-        const int64_t h = heads[s];
+        // segment s: row touched[s], requests keys[h, e)
+        const int64_t rec = heads[s];
+        const int64_t rowg = __ldg(g.touched + s);
+        const int64_t h = rec & 0xffffffffll, e = h + (rec >> 32);
         // the segment's first 32 keys stay in registers (lane j: keys[h + j])
-        const unsigned long long kk = h + lane < N ? keys[h + lane] : KEY_MAX;
-        const unsigned long long hk = __shfl_sync(0xffffffffu, kk, 0);
-        const int64_t rowg = (int64_t)(hk >> 32);
-        int64_t e = -1;
-        {
-            const unsigned nb = __ballot_sync(0xffffffffu, (kk >> 32) != (hk >> 32));
-            if (nb) e = h + __ffs(nb) - 1;
-        }
-        for (int64_t b = h + 32; e < 0; b += 32) {
-            int64_t j = b + lane;
-            bool same = j < N && (keys[j] >> 32) == (hk >> 32);
-            unsigned nb = __ballot_sync(0xffffffffu, !same);
-            if (nb) e = b + __ffs(nb) - 1;
-        }
+        const unsigned long long kk = h + lane < e ? keys[h + lane] : KEY_MAX;
         const bool l0 = rowg < g.n;
         const int y = l0 ? (int)rowg : upper_owner[rowg - g.n];
         const int cap = l0 ? g.cap0 : g.capU;
@@ -423,21 +416,10 @@ __global__ void __maxnreg__(96) reverse_exact_kernel(
         if (lane == 0) s = atomicAdd(next, 1);
         s = __shfl_sync(0xffffffffu, s, 0);
         if (s >= nseg) break;
-        const int64_t h = heads[s];
-        const unsigned long long kk = h + lane < N ? keys[h + lane] : KEY_MAX;
-        const unsigned long long hk = __shfl_sync(0xffffffffu, kk, 0);
-        const int64_t rowg = (int64_t)(hk >> 32);
-        int64_t e = -1;
-        {
-            const unsigned nb = __ballot_sync(0xffffffffu, (kk >> 32) != (hk >> 32));
-            if (nb) e = h + __ffs(nb) - 1;
-        }
-        for (int64_t b = h + 32; e < 0; b += 32) {
-            const int64_t j = b + lane;
-            const bool same = j < N && (keys[j] >> 32) == (hk >> 32);
-            const unsigned nb = __ballot_sync(0xffffffffu, !same);
-            if (nb) e = b + __ffs(nb) - 1;
-        }
+        const int64_t rec = heads[s];
+        const int64_t rowg = __ldg(g.touched + s);
+        const int64_t h = rec & 0xffffffffll, e = h + (rec >> 32);
+        const unsigned long long kk = h + lane < e ? keys[h + lane] : KEY_MAX;
         const bool l0 = rowg < g.n;
         const int y = l0 ? (int)rowg : upper_owner[rowg - g.n];
         const int cap = l0 ? g.cap0 : g.capU;

@@ -105,3 +105,32 @@ def test_select_asymmetric_table_matches_oracle(core):
         cap = int(rng.integers(1, 40))
         assert core.select_neighbors(4, {"codes": codes, "sdt": sdt}, ids, d, cap) == \
             native.select(sdt, codes, ids, d, cap)
+
+
+@pytest.mark.parametrize("dims_per", [1, 2, 3, 4, 8, 5])
+def test_encoder_threshold_quantiser_random_ranges(core, dims_per):
+    """K2's quantiser runs as per-coder float thresholds (csrc/encode.cu); the
+    tables must equal the oracle's IEEE-double formula (fa_quantize,
+    _simd.h:99-107) for arbitrary ranges: 40 random (dist_min, delta) pairs,
+    including tiny and huge deltas and dist_min above some distances, over
+    rows whose distances spread across the whole range.  Uniform and
+    non-uniform subspace widths (5 dims: the generic, non-unrolled path)."""
+    rng = np.random.default_rng(dims_per)
+    m = 12
+    dims = np.full(m, dims_per, np.int32)
+    if dims_per == 5:
+        dims[::3] = 4  # a split with two widths
+    offs = np.concatenate([[0], np.cumsum(dims)[:-1]]).astype(np.int32)
+    dmax = int(dims.max())
+    cent = np.zeros((m, 16, dmax), np.float32)
+    for i in range(m):
+        cent[i, :, :dims[i]] = rng.normal(size=(16, dims[i])) * rng.uniform(0.1, 10)
+    red = (rng.normal(size=(64, int(dims.sum()))) * rng.uniform(0.1, 10, 64)[:, None]).astype(np.float32)
+    for t in range(40):
+        scale = 10.0 ** rng.uniform(-3, 3)
+        dmin = float(rng.uniform(0, 2) * scale) if t % 4 else 0.0
+        delta = float(10.0 ** rng.uniform(-4, 4)) * scale
+        c_gpu, a_gpu = core.flash_encode_adt_many(cent, dims, offs, dmin, delta, red)
+        c_or, a_or = native.encode_adt(red, cent, dims, offs, dmin, delta)
+        assert np.array_equal(np.asarray(c_gpu).reshape(c_or.shape), c_or), (t, dmin, delta)
+        assert np.array_equal(np.asarray(a_gpu).reshape(a_or.shape), a_or), (t, dmin, delta)
