@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
     const int32_t *__restrict__ order, unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,
-    int64_t *__restrict__ stats, int *__restrict__ work) {
+    int64_t *__restrict__ stats, int *__restrict__ work, const int *__restrict__ start_v,
+    const uint32_t *__restrict__ start_d) {
     // sdtT: the transposed SDT in global memory (L1-resident; keeping it out of
     // shared memory leaves room for one more CTA per SM)
     extern __shared__ __align__(256) uint8_t smem[];
@@ -48,10 +49,16 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
         SearchCounters cnt = {};
         const int level = __ldg(g.levels + x);
         int cur = ep;
-        uint32_t curd = P::one(g, ws.adt, ep, lane);
-        cnt.dist += 1;
-        for (int layer = ml; layer > level; --layer)
-            hill_climb<P>(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+        uint32_t curd;
+        if (start_v) {  // the descent ran in batch_descend_kernel
+            cur = __ldg(start_v + q);
+            curd = __ldg(start_d + q);
+        } else {
+            curd = P::one(g, ws.adt, ep, lane);
+            cnt.dist += 1;
+            for (int layer = ml; layer > level; --layer)
+                hill_climb<P>(g, layer, cur, curd, ws.adt, ws.fresh, ws.fdist, cnt, lane);
+        }
         const int top = min(ml, level);
         unsigned long long *myreq = req + __ldg(req_off + q);
         long long sel_cycles = 0;
@@ -151,6 +158,98 @@ __global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
     }
     gslot_release(gs, lane);
     flush_counters(total, ctr, lane);
+}
+
+// The batch's greedy descents (hill_climb through the layers above each
+// vertex's level, _core.pyx:345-385, from the batch's entry point), ahead of
+// the beam searches: their end points and distances seed build_search_kernel,
+// and the distance orders the batch.  The length of a vertex's layer-0 search
+// correlates with how far its descent ends from it (0.64 at config 2), so
+// processing the far ones first leaves a shorter tail of long searches at the
+// end of the batch (a simulated 5.7 % off the makespan of the 65,536-vertex
+// batches).  Any processing order builds the same graph.  hist gets the
+// count of every (level, distance) key, key_of below.
+__device__ __forceinline__ int descend_key(int level, int maxlv, uint32_t d) {
+    return (maxlv - min(level, maxlv)) * 256 + (255 - (int)min(d, 255u));
+}
+
+template <typename P>
+__global__ void __launch_bounds__(kSearchWarps * 32) batch_descend_kernel(
+    Graph g, const uint8_t *__restrict__ adt_batch, int start, int size, int ep, int ml,
+    int maxlv, int ctx_bytes, int cand, int *__restrict__ start_v, uint32_t *__restrict__ start_d,
+    int *__restrict__ hist, unsigned long long *__restrict__ ctr, int *__restrict__ work) {
+    extern __shared__ __align__(256) uint8_t smem[];
+    const int lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    // (per-warp stride a multiple of 256: the ADT's PRMT-merged addresses)
+    uint8_t *ctx = smem + (size_t)wid * round_up(ctx_bytes + 8 * cand, 256);
+    int32_t *ids_s = reinterpret_cast<int32_t *>(ctx + ctx_bytes);
+    uint32_t *d_s = reinterpret_cast<uint32_t *>(ids_s + cand);
+    CounterTotals total;
+    for (;;) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(work, 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= size) break;
+        const int x = start + q;
+        load_adt_smem(ctx, adt_batch + (size_t)q * g.mpad * 16, g.mpad, lane);
+        __syncwarp();
+        SearchCounters cnt = {};
+        const int level = __ldg(g.levels + x);
+        int cur = ep;
+        uint32_t curd = P::one(g, ctx, ep, lane);
+        cnt.dist += 1;
+        for (int layer = ml; layer > level; --layer)
+            hill_climb<P>(g, layer, cur, curd, ctx, ids_s, d_s, cnt, lane);
+        if (lane == 0) {
+            start_v[q] = cur;
+            start_d[q] = curd;
+            atomicAdd(hist + descend_key(level, maxlv, curd), 1);
+        }
+        total.add(cnt);
+        __syncwarp();
+    }
+    flush_counters(total, ctr, lane);
+}
+template __global__ void batch_descend_kernel<FlashDist>(Graph, const uint8_t *, int, int, int, int,
+                                                         int, int, int, int *, uint32_t *, int *,
+                                                         unsigned long long *, int *);
+template __global__ void batch_descend_kernel<FlashDistW>(Graph, const uint8_t *, int, int, int, int,
+                                                          int, int, int, int *, uint32_t *, int *,
+                                                          unsigned long long *, int *);
+
+// hist -> exclusive offsets (one CTA; nkeys <= a few thousand)
+__global__ void __launch_bounds__(1024) descend_scan_kernel(int *__restrict__ hist, int nkeys) {
+    __shared__ int part[1024];
+    const int per = (nkeys + 1023) / 1024;
+    const int k0 = threadIdx.x * per, k1 = min(nkeys, k0 + per);
+    int sum = 0;
+    for (int k = k0; k < k1; ++k) sum += hist[k];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - sum;
+    for (int k = k0; k < k1; ++k) {
+        const int c = hist[k];
+        hist[k] = run;
+        run += c;
+    }
+}
+
+// the batch's processing order: vertices by key (higher levels first, then
+// the farthest descents first); within a key in any order
+__global__ void descend_order_kernel(const int32_t *__restrict__ levels, int start, int size,
+                                     int maxlv, const uint32_t *__restrict__ start_d,
+                                     int *__restrict__ offs, int32_t *__restrict__ order) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < size; q += gridDim.x * blockDim.x) {
+        const int key = descend_key(__ldg(levels + start + q), maxlv, __ldg(start_d + q));
+        order[atomicAdd(offs + key, 1)] = q;
+    }
 }
 
 // RC: id-row chunks compiled into the hot loop (2 when the base rows hold

@@ -618,6 +618,27 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     gb.gvis_nslots = g.gvis_nslots;
     gb.gvis_words = g.gvis_words;
 
+    // batch descents + processing order (Flash kind): for the batches with
+    // more vertices than resident search warps, where the order sets the tail
+    const bool descend = !exact;
+    int maxlv = 0;
+    for (int64_t v = 0; v < g.n; ++v) maxlv = std::max(maxlv, ix->levels_h[v]);
+    const int nkeys = (maxlv + 1) * 256;
+    const int desc_ctx = WarpLayout::adt_bytes(g.mpad);
+    const size_t smem_desc = (size_t)kSearchWarps * round_up(desc_ctx + 8 * capmax, 256);
+    int64_t desc_ctas = 0;
+    if (descend) {
+        const void *df = ix->wide ? (const void *)batch_descend_kernel<FlashDistW>
+                                  : (const void *)batch_descend_kernel<FlashDist>;
+        if (smem_desc > 48 * 1024)
+            FA_CUDA(cudaFuncSetAttribute(df, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_desc));
+        int per = 0;
+        FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, df, kSearchWarps * 32, smem_desc));
+        desc_ctas = (int64_t)std::max(per, 1) * num_sms();
+    }
+    int32_t *start_v = nullptr, *hist = nullptr;
+    uint32_t *start_d = nullptr;
     uint8_t *adt_batch = nullptr, *sdtT = nullptr, *rev_sel = nullptr;
     unsigned long long *req = nullptr, *req_sorted = nullptr, *ctr = nullptr;
     int64_t *req_off_d = nullptr, *heads = nullptr;
@@ -627,6 +648,8 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // scratch is stream-ordered (cudaMallocAsync from the device's pool, kept
     // cached across builds): no allocation or free synchronises the device
     auto cleanup = [&]() {
+        for (void *p : {(void *)start_v, (void *)start_d, (void *)hist})
+            if (p) cudaFreeAsync(p, st);
         for (void *p : {(void *)adt_batch, (void *)req, (void *)req_sorted, (void *)ctr,
                         (void *)req_off_d, (void *)order_d, (void *)err, (void *)heads,
                         (void *)nheads, (void *)next_seg, (void *)sdtT, (void *)rev_sel,
@@ -653,7 +676,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         (rc = dev_alloc((void **)&req_off_d, sizeof(int64_t) * g.n)) ||
         (rc = dev_alloc((void **)&order_d, sizeof(int32_t) * g.n)) ||
         (rc = dev_alloc((void **)&heads, sizeof(int64_t) * std::max<int64_t>(maxreq, 1))) ||
-        (rc = dev_alloc((void **)&nheads, 3 * sizeof(int))) ||
+        (rc = dev_alloc((void **)&nheads, 4 * sizeof(int))) ||
+        (descend && (rc = dev_alloc((void **)&start_v, sizeof(int32_t) * (size_t)maxB))) ||
+        (descend && (rc = dev_alloc((void **)&start_d, sizeof(uint32_t) * (size_t)maxB))) ||
+        (descend && (rc = dev_alloc((void **)&hist, sizeof(int32_t) * (size_t)nkeys))) ||
         (rc = dev_alloc((void **)&next_seg, sizeof(int))) ||
         (rc = dev_alloc((void **)&sdtT, sdt_bytes)) ||
         (rc = dev_alloc((void **)&rev_sel, (size_t)rev_ctas * kReverseWarps * rev_sel_bytes)) ||
@@ -696,8 +722,6 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         cleanup();
         return rc;
     }
-    int maxlv = 0;
-    for (int64_t v = 0; v < g.n; ++v) maxlv = std::max(maxlv, ix->levels_h[v]);
     std::vector<int> lvpos((size_t)maxlv + 2);
     // optional per-kernel-class timing: 5 events per batch on the build stream
     const bool prof = opts->profile != 0;
@@ -734,15 +758,20 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             }
         }
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 1], st));
-        {  // stable counting sort of the batch by level, descending
-            int32_t *o = order_h + b.start;
+        // more vertices than resident search warps: descents first, then the
+        // processing order from them (build_search.cu batch_descend_kernel)
+        const bool desc_b = descend && (int64_t)b.size > search_ctas * bw;
+        {
             const int32_t *lv = ix->levels_h.data() + b.start;
-            std::fill(lvpos.begin(), lvpos.end(), 0);
-            for (int k = 0; k < b.size; ++k) ++lvpos[maxlv - lv[k] + 1];
-            for (int l = 1; l <= maxlv + 1; ++l) lvpos[l] += lvpos[l - 1];
-            for (int k = 0; k < b.size; ++k) o[lvpos[maxlv - lv[k]]++] = k;
-            FA_BUILD_CUDA(cudaMemcpyAsync(order_d + b.start, o, sizeof(int32_t) * b.size,
-                                          cudaMemcpyHostToDevice, st));
+            if (!desc_b) {  // stable counting sort of the batch by level, descending
+                int32_t *o = order_h + b.start;
+                std::fill(lvpos.begin(), lvpos.end(), 0);
+                for (int k = 0; k < b.size; ++k) ++lvpos[maxlv - lv[k] + 1];
+                for (int l = 1; l <= maxlv + 1; ++l) lvpos[l] += lvpos[l - 1];
+                for (int k = 0; k < b.size; ++k) o[lvpos[maxlv - lv[k]]++] = k;
+                FA_BUILD_CUDA(cudaMemcpyAsync(order_d + b.start, o, sizeof(int32_t) * b.size,
+                                              cudaMemcpyHostToDevice, st));
+            }
             // request slots: (min(ml, level) + 1) R per vertex, in vertex order
             int64_t *ro = reqoff_h + b.start;
             int64_t off = 0;
@@ -755,12 +784,31 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
         // nheads[0]: touched rows (= row segments), nheads[1]: the search's
         // work counter, nheads[2]: the bucketing cursor
-        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 3 * sizeof(int), st));
+        FA_BUILD_CUDA(cudaMemsetAsync(nheads, 0, 4 * sizeof(int), st));
+        if (desc_b) {
+            FA_BUILD_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (size_t)nkeys, st));
+            const int dgrid = (int)std::min<int64_t>(desc_ctas, (b.size + kSearchWarps - 1) / kSearchWarps);
+            if (ix->wide)
+                batch_descend_kernel<FlashDistW><<<dgrid, kSearchWarps * 32, smem_desc, st>>>(
+                    gb, adt_batch, b.start, b.size, b.ep, b.ml, nkeys / 256 - 1, desc_ctx, capmax,
+                    start_v, start_d, hist, ctr, nheads + 3);
+            else
+                batch_descend_kernel<FlashDist><<<dgrid, kSearchWarps * 32, smem_desc, st>>>(
+                    gb, adt_batch, b.start, b.size, b.ep, b.ml, nkeys / 256 - 1, desc_ctx, capmax,
+                    start_v, start_d, hist, ctr, nheads + 3);
+            descend_scan_kernel<<<1, 1024, 0, st>>>(hist, nkeys);
+            descend_order_kernel<<<(int)std::min<int64_t>(num_sms() * 4, (b.size + 255) / 256), 256, 0,
+                                   st>>>(ix->d.levels, b.start, b.size, nkeys / 256 - 1, start_d, hist,
+                                         order_d + b.start);
+            FA_BUILD_CUDA(cudaGetLastError());
+            launches += 3;
+        }
         int grid = (int)std::min<int64_t>(search_ctas, (b.size + bw - 1) / bw);
         search_fn<<<grid, bw * 32, smem_search, st>>>(
             gb, sdtT, adt_batch, b.start, b.size, b.ep, b.ml, C, R, L, req_off_d + b.start,
             order_d + b.start,
-            req, ctr, err, opts->point_stats, nheads + 1);
+            req, ctr, err, opts->point_stats, nheads + 1, desc_b ? start_v : nullptr,
+            desc_b ? start_d : nullptr);
         FA_BUILD_CUDA(cudaGetLastError());
         if (prof) FA_BUILD_CUDA(cudaEventRecord(ev[bi * 5 + 2], st));
         // bucket the requests by row: segments for the touched rows, then

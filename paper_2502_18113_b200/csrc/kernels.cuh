@@ -62,7 +62,19 @@ __device__ __forceinline__ void flush_counters(const SearchCounters &c, unsigned
 
 using BuildSearchFn = void (*)(Graph, const uint8_t *, const uint8_t *, int, int, int, int, int,
                                int, WarpLayout, const int64_t *, const int32_t *,
-                               unsigned long long *, unsigned long long *, int *, int64_t *, int *);
+                               unsigned long long *, unsigned long long *, int *, int64_t *, int *,
+                               const int *, const uint32_t *);
+// the Flash build's batch descents and processing order (build_search.cu)
+template <typename P>
+__global__ void batch_descend_kernel(Graph g, const uint8_t *__restrict__ adt_batch, int start,
+                                     int size, int ep, int ml, int maxlv, int ctx_bytes, int cand,
+                                     int *__restrict__ start_v, uint32_t *__restrict__ start_d,
+                                     int *__restrict__ hist, unsigned long long *__restrict__ ctr,
+                                     int *__restrict__ work);
+__global__ void descend_scan_kernel(int *__restrict__ hist, int nkeys);
+__global__ void descend_order_kernel(const int32_t *__restrict__ levels, int start, int size,
+                                     int maxlv, const uint32_t *__restrict__ start_d,
+                                     int *__restrict__ offs, int32_t *__restrict__ order);
 using QuerySearchFn = void (*)(Graph, const uint8_t *, int, int, int, int, int, int, const float *,
                                int, const float *, WarpLayout, int64_t *, double *,
                                unsigned long long *, int *);
