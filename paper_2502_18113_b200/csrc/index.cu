@@ -24,9 +24,9 @@ struct fa_index {
     int cap0, capU;
     std::vector<int32_t> levels_h;
     std::vector<int64_t> uoff_h;
-    // derived once from levels_h (immutable): prefix sums of the levels and
-    // the record positions (a level above every earlier one: a new top layer)
-    std::vector<int64_t> lvl_prefix;
+    // derived once from levels_h (immutable): the record positions (a level
+    // above every earlier one: a new top layer) and the largest level
+    bool sched_ready = false;
     std::vector<int64_t> raisers;
     // host drop-in: projected rows >= late_from arrive while the build runs;
     // late_hook (wait for them, encode them) runs before the first batch
@@ -44,6 +44,7 @@ struct fa_index {
     int64_t n_inserted = 0;  // vertices [0, n_inserted) are in the graph
     int64_t entry = -1;
     int max_layer = -1;
+    int maxlv = 0;  // the largest level (with raisers)
 };
 
 namespace fa {
@@ -469,6 +470,16 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     res->entry_point = -1;
     res->max_layer = -1;
     const auto t_host0 = std::chrono::steady_clock::now();
+    // FLASHANN_B200_TIMING: the host set-up's phases (diagnostics)
+    const bool tmarks = getenv("FLASHANN_B200_TIMING") != nullptr;
+    auto t_last = t_host0;
+    auto tmark = [&](const char *what) {
+        if (!tmarks) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[fa timing]   build set-up: %-22s %7.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const int64_t r0 = opts->start, r1 = opts->end > 0 ? opts->end : g.n;
     FA_CHECK_ARG(r0 >= 0 && r0 <= r1 && r1 <= g.n, "insertion range [%lld, %lld) outside [0, %lld]",
                  (long long)r0, (long long)r1, (long long)g.n);
@@ -497,22 +508,25 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     const int Bmin = opts->batch_min >= 0 ? opts->batch_min
                                           : (int)std::min<int64_t>(4096, std::max<int64_t>(1, g.n / 256));
 
+    tmark("graph reset");
     // ---- schedule (pure function of the layer draws) ----
-    // O(batches) from the level prefix sums and the record positions; the
-    // per-vertex request offsets are written per batch in the launch loop.
-    if ((int64_t)ix->lvl_prefix.size() != g.n + 1) {
-        ix->lvl_prefix.assign(g.n + 1, 0);
+    // From the record positions and one pass over the inserted range's
+    // levels (each batch's request bound); the per-vertex request offsets are
+    // written per batch in the launch loop.
+    if (!ix->sched_ready) {
         ix->raisers.clear();
         int run = -1;
+        const int32_t *lvh = ix->levels_h.data();
         for (int64_t v = 0; v < g.n; ++v) {
-            const int lv = ix->levels_h[v];
-            ix->lvl_prefix[v + 1] = ix->lvl_prefix[v] + lv;
-            if (lv > run) {
+            if (lvh[v] > run) {
                 if (v > 0) ix->raisers.push_back(v);
-                run = lv;
+                run = lvh[v];
             }
         }
+        ix->maxlv = std::max(run, 0);
+        ix->sched_ready = true;
     }
+    tmark("record positions");
     std::vector<Batch> batches;
     // vertex 0 seeds an empty graph; a resumed build starts from the state
     // the earlier calls left (entry point, top layer)
@@ -539,7 +553,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             int64_t end = std::min<int64_t>(r1, x + B);
             if (ri < ix->raisers.size()) end = std::min<int64_t>(end, ix->raisers[ri]);
             size = (int)(end - x);
-            b.nreq = (int64_t)R * (size + (ix->lvl_prefix[end] - ix->lvl_prefix[x]));
+            int64_t lsum = 0;  // the batch's levels: its upper-layer request slots
+            const int32_t *lvh = ix->levels_h.data();
+            for (int64_t v = x; v < end; ++v) lsum += lvh[v];
+            b.nreq = (int64_t)R * (size + lsum);
         }
         b.size = size;
         b.raiser = raiser;
@@ -553,6 +570,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
         }
     }
 
+    tmark("batch schedule");
     // ---- scratch ----
     const int capmax = std::max(g.cap0, g.capU);
     if (exact || ix->wide) gb.expand = 1;
@@ -610,7 +628,9 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
                                      cudaFuncAttributePreferredSharedMemoryCarveout,
                                      std::min(100, std::max(0, pct))));
     }
+    tmark("schedule + launch set-up");
     FA_TRY(ensure_gvis(ix, (const void *)search_fn, bw * 32, smem_search, C, st));
+    tmark("global visited tier");
     gb.gvis = g.gvis;
     gb.gvis_epoch = g.gvis_epoch;
     gb.gvis_owner = g.gvis_owner;
@@ -621,8 +641,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // batch descents + processing order (Flash kind): for the batches with
     // more vertices than resident search warps, where the order sets the tail
     const bool descend = !exact;
-    int maxlv = 0;
-    for (int64_t v = 0; v < g.n; ++v) maxlv = std::max(maxlv, ix->levels_h[v]);
+    const int maxlv = ix->maxlv;
     const int nkeys = (maxlv + 1) * 256;
     const int desc_ctx = WarpLayout::adt_bytes(g.mpad);
     const size_t smem_desc = (size_t)kSearchWarps * round_up(desc_ctx + 8 * capmax, 256);
@@ -696,6 +715,7 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
             return FA_ECUDA;                                                             \
         }                                                                                \
     } while (0)
+    tmark("scratch");
     FA_BUILD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 8, st));
     // per-row request counts: zero here, re-zeroed by the reverse warps
     FA_BUILD_CUDA(cudaMemsetAsync(rowcnt, 0, sizeof(int32_t) * nrows, st));
