@@ -11,7 +11,7 @@ namespace fa {
 // selection uses the SDT (sdtT); P = ExactDist: the query is the inserted
 // vertex's own vector and every distance is fp32 L2.
 template <typename P, int J, int EM, int RC>
-__global__ void __launch_bounds__(kSearchWarps * 32, 5) build_search_kernel(
+__global__ void __maxnreg__(96) build_search_kernel(
     Graph g, const uint8_t *__restrict__ sdtT, const uint8_t *__restrict__ adt_batch, int start,
     int size, int ep, int ml, int C, int R, WarpLayout L, const int64_t *__restrict__ req_off,
     const int32_t *__restrict__ order, unsigned long long *__restrict__ req, unsigned long long *__restrict__ ctr, int *err,

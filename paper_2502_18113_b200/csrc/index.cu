@@ -108,8 +108,8 @@ static int reset_graph(fa_index *ix, cudaStream_t st) {
 // ids) use 64-bit entries.
 // Warps per CTA of a search launch: kSearchWarps, fewer when the per-warp
 // workspace (wide searches) does not fit; 0 if one warp does not fit.
-static int search_warps_for(int per_warp_bytes) {
-    int w = kSearchWarps;
+static int search_warps_for(int per_warp_bytes, int wmax = kSearchWarps) {
+    int w = wmax;
     while (w > 0 && (size_t)w * per_warp_bytes > 227 * 1024) --w;
     return w;
 }
@@ -585,19 +585,39 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     // selection workspace)
     int hl = opts->hash_log2 > 0 ? std::min(std::max(opts->hash_log2, 9), 12) : 12;
     while (((size_t)16 << vis_buckets_log2(hl)) < sel_bytes) ++hl;
-    const bool t_alias =
-        sel_bytes + (size_t)round_up(C, 32) * 8 <= ((size_t)16 << vis_buckets_log2(hl));
+    // (else they overlay the small block's search state, dead by then)
+    const int t_alias =
+        sel_bytes + (size_t)round_up(C, 32) * 8 <= ((size_t)16 << vis_buckets_log2(hl)) ? 1 : 2;
     WarpLayout L;
     L.init(g.mpad, C, capmax, hl, gb.expand, t_alias, exact ? g.dim * 4 : -1, (exact || ix->wide) ? 8 : 4);
     const size_t sdt_bytes = round_up(std::max(g.m, 1) * 256, 128);
-    const int bw = search_warps_for(L.total);  // warps per CTA
-    const size_t smem_search = (size_t)bw * L.total;
+    int bw = search_warps_for(L.total, kBuildWarpsMax);  // warps per CTA
     FA_CHECK_ARG(bw > 0, "search workspace %d B per warp exceeds shared memory", L.total);
     const BuildSearchFn search_fn =
         exact ? build_search_exact_variant(C, g.cap0, ix->wide)
               : build_search_variant(C, ix->wide ? 1 : gb.expand, g.cap0, ix->wide);
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_search));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, bw * L.total));
+    // the CTA width that keeps the most warps resident (each CTA also costs
+    // 1 KB of reserved shared memory): config 2's 10.9 KB per warp packs 21
+    // warps per SM as 3 CTAs of 7 (20 as 5 of 4), config 4's 11.3 KB 20 as
+    // 4 of 5 (16 as 4 of 4); ties go to the wider CTA
+    {
+        int best = 0;
+        const int wmax = bw;
+        for (int w = wmax; w >= 1; --w) {
+            int per = 0;
+            FA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_fn, w * 32,
+                                                                  (size_t)w * L.total));
+            if (per * w > best) {
+                best = per * w;
+                bw = w;
+            }
+        }
+        if (const char *e = getenv("FLASHANN_B200_SEARCH_WARPS"))
+            bw = std::min(std::max(atoi(e), 1), wmax);
+    }
+    const size_t smem_search = (size_t)bw * L.total;
     ReverseLayout RL;
     RL.init(capmax, g.m, g.mpad, exact ? g.dim : 0);
     const bool rc2 = g.cap0 <= 64;  // base rows of <= 64 slots: two 32-slot chunks

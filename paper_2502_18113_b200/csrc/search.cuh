@@ -128,29 +128,39 @@ struct WarpLayout {
     // forward selection's kept rows use only its start)
     // ctx_bytes: the query context (default: the ADT, mpad x 16; the exact
     // kind: the query vector, dim x 4); key_bytes: 4 (Flash) or 8 (exact)
+    // t_alias 2: the sorted results overlay the small block's search state
+    // (candidate keys, tie queue, fresh ids/distances: all dead once a layer
+    // search has sorted its results) -- the build, when the results do not
+    // fit beside the selection workspace in the visited table
     __host__ __device__ void init(int mpad, int W, int capmax, int hlog2, int expand,
-                                  bool t_alias = false, int ctx_bytes = -1, int key_bytes = 4) {
+                                  int t_alias = 0, int ctx_bytes = -1, int key_bytes = 4) {
         hash_log2 = hlog2;
         const int nc = cand_capacity(expand, capmax);
         const int Wp = round_up(W, 32);
         const int hbytes = 16 << vis_buckets_log2(hlog2);
-        t_big = t_alias && W <= kRegSetMax;
+        t_big = t_alias == 1 && W <= kRegSetMax;
+        const bool t_small = t_alias == 2 && W <= kRegSetMax;
         adt = 0;
         hash = ctx_bytes < 0 ? adt_bytes(mpad) : round_up(ctx_bytes, 256);
         big = hash + hbytes;  // a multiple of 256
         int o = 0;
         if (t_big) {
             T = hash + hbytes - Wp * 8;
+        } else if (t_small) {
+            T = 0;
         } else {
             // sorted 64-bit results (+ 32-bit keys and flags when the set lives here)
             T = o;
             o += Wp * (W > kRegSetMax ? 8 + key_bytes + 1 : 8);
             o = round_up(o, 16);
         }
-        S = o; o += 2 * nc * key_bytes;  // candidate keys (two buffers)
+        // candidate keys; their rank-sorted copy overlays fresh + fdist (read
+        // for the last time when the keys are formed)
+        S = o; o += nc * key_bytes;
         TQ = o; o += Wp * 4;     // tie queue
         fresh = o; o += nc * 4;
         fdist = o; o += nc * 4;
+        if (t_small && o < Wp * 8) o = Wp * 8;
         small = round_up(o, 16);
         total = big + small;
     }
@@ -209,12 +219,14 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
         K[q] = ((0x03020100u + 0x04040404u * (uint32_t)q + 0x01010101u * (uint32_t)c) &
                 0x0f0f0f0fu)
                << 4;
+    const uint8_t *cb = codes + c * 16;
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (gi < nf && active)
+        w = __ldg(reinterpret_cast<const uint4 *>(cb + (size_t)ids_s[gi] * mpad));
     for (int base = 0; base < nf; base += (32 >> lg)) {
         const int f = base + gi;
         uint32_t sum = 0;
         if (f < nf && active) {
-            const int id = ids_s[f];
-            const uint4 w = __ldg(reinterpret_cast<const uint4 *>(codes + (size_t)id * mpad + c * 16));
             const uint32_t W[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -228,6 +240,10 @@ __device__ __forceinline__ void dists_for(const uint8_t *adt_s, const uint8_t *_
                 sum += b[0] + b[1] + b[2] + b[3];
             }
         }
+        // the next pass's code rows, in flight under this pass's reduction
+        const int fn = f + (32 >> lg);
+        if (fn < nf && active)
+            w = __ldg(reinterpret_cast<const uint4 *>(cb + (size_t)ids_s[fn] * mpad));
         if (G > 1) sum += __shfl_xor_sync(0xffffffffu, sum, 1);
         if (G > 2) sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (G > 4) sum += __shfl_xor_sync(0xffffffffu, sum, 4);
@@ -825,7 +841,7 @@ __device__ __forceinline__ void accept_offers(RegSet<J, P> &rs, int &ts, int W,
     if (ns == 0) return;
     const int nfill = min(ns, W - ts);
     const K *src = Sa;
-    if (nfill < ns) {
+    if (nfill < ns && ns > 1) {
         // offers are processed in ascending order: rank-sort them
         for (int j = lane; j < ns; j += 32) {
             const K k = Sa[j];
@@ -836,16 +852,19 @@ __device__ __forceinline__ void accept_offers(RegSet<J, P> &rs, int &ts, int W,
         __syncwarp();
         src = Sb;
     }
-    // the first nfill offers fill slots ts .. ts + nfill
+    // the first nfill offers fill slots ts .. ts + nfill (none once the set
+    // is full: the common case)
+    if (nfill > 0) {
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-        const int o = lane + 32 * j - ts;
-        if (o >= 0 && o < nfill) {
-            rs.key[j] = src[o];
-            rs.fl &= ~(1u << j);
+        for (int j = 0; j < J; ++j) {
+            const int o = lane + 32 * j - ts;
+            if (o >= 0 && o < nfill) {
+                rs.key[j] = src[o];
+                rs.fl &= ~(1u << j);
+            }
         }
+        ts += nfill;
     }
-    ts += nfill;
     // worst distance wd: recomputed lazily (as the next victim's distance);
     // stale = the set changed since wd was last known
     bool stale = ts == W && nfill > 0;
@@ -926,7 +945,7 @@ __device__ __forceinline__ bool layer_search_reg(const Graph &g, int layer, int 
     const RowAddr ra(g, layer);
     using K = typename P::Key;
     K *Sa = reinterpret_cast<K *>(S);
-    K *Sb = Sa + cand_capacity(g);
+    K *Sb = reinterpret_cast<K *>(fresh);  // (WarpLayout: fresh + fdist hold nc keys)
     const unsigned lt = (1u << lane) - 1u;
     VisitedSet<KB, P::kWide> vs;
     vs.begin(H, hlog2, g, gs, lane);
@@ -1123,7 +1142,7 @@ __device__ inline bool layer_search_smem(const Graph &g, int layer, int entry, u
     Kt *K = reinterpret_cast<Kt *>(T + Wp);
     uint8_t *F = reinterpret_cast<uint8_t *>(K + Wp);
     Kt *Sa = reinterpret_cast<Kt *>(S);
-    Kt *Sb = Sa + cand_capacity(g);
+    Kt *Sb = reinterpret_cast<Kt *>(fresh);  // (WarpLayout: fresh + fdist hold nc keys)
     VisitedSet<0, P::kWide> vs;
     vs.begin(H, hlog2, g, gs, lane);
     if (lane == 0) {
