@@ -599,9 +599,10 @@ extern "C" int fa_index_build(fa_index *ix, const fa_build_opts *opts, fa_build_
     FA_CUDA(cudaFuncSetAttribute((const void *)search_fn,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bw * L.total));
     // the CTA width that keeps the most warps resident (each CTA also costs
-    // 1 KB of reserved shared memory): config 2's 10.9 KB per warp packs 21
-    // warps per SM as 3 CTAs of 7 (20 as 5 of 4), config 4's 11.3 KB 20 as
-    // 4 of 5 (16 as 4 of 4); ties go to the wider CTA
+    // 1 KB of reserved shared memory; 96 registers cap an SM at 5 warps per
+    // scheduler = 20): config 2's 10.9 KB per warp runs 20 warps as 4 CTAs of
+    // 5 (or 5 of 4), config 4's 11.3 KB 20 as 4 of 5 where CTAs of 4 reach
+    // only 16; ties go to the wider CTA
     {
         int best = 0;
         const int wmax = bw;

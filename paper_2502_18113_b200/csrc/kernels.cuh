@@ -7,8 +7,8 @@ namespace fa {
 
 constexpr int kSearchWarps = 4;   // warps (points) per CTA in the search kernels
 // The build's search kernel: CTAs of up to this many warps (the host picks the
-// width that keeps the most warps resident); launch bounds of (7 warps, 3
-// CTAs) give it the same 96-register budget as (4 warps, 5 CTAs)
+// width that keeps the most warps resident); __maxnreg__(96) keeps 5 warps
+// per scheduler whatever the width
 constexpr int kBuildWarpsMax = 7;
 constexpr int kReverseWarps = 4;  // warps per CTA in the reverse-edge kernel
 
