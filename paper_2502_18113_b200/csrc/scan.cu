@@ -182,16 +182,17 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_select_tma_kernel(
             if (HALF) {
                 const uint2 c = *reinterpret_cast<const uint2 *>(cod + (size_t)b * m * 16 + hrow * 16 +
                                                                  (hodd ? 8 : 0));
-                const uint32_t r0 = lut16x4(th[0], th[1], th[2], th[3], c.x);
-                const uint32_t r1 = lut16x4(th[0], th[1], th[2], th[3], c.y);
-                const uint32_t a[4] = {prmt(r0, 0u, 0x4240u), prmt(r0, 0u, 0x4341u),
-                                       prmt(r1, 0u, 0x4240u), prmt(r1, 0u, 0x4341u)};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (hodd) acc[4 + k] += a[k];
-                    else acc[k] += a[k];
+                uint32_t r0, r1;
+                lut16x8(th, c.x, c.y, r0, r1);
+                if (hodd) {
+                    acc_word(r0, acc[4], acc[5]);
+                    acc_word(r1, acc[6], acc[7]);
+                } else {
+                    acc_word(r0, acc[0], acc[1]);
+                    acc_word(r1, acc[2], acc[3]);
                 }
             }
+            finish_acc(acc);
             const uint32_t v = reduce_batch(acc, lane);
             const int slot = b * 16 + slot_of_lane(lane);
             if ((lane & 2) == 0 && slot < cnt) {
